@@ -1,0 +1,138 @@
+/*
+ * cutfem.h — C ABI of the B200-native matrix-free DG-CutFEM operator apply.
+ *
+ * The operator (§2.1 eq:bilinear_dg P:83-92 with the Nitsche terms of
+ * eq:bilinear_cg P:68-76, plus the face ghost penalty fixed by BASELINE.json
+ * configs[0]; SURVEY.md §8(c) "Definition"):
+ *
+ *   a(v,u) = sum_K int_{K∩Ω} ∇v·∇u
+ *          + sum_{K cut} int_{Γ∩K} [ -(∂_n v) u - v ∂_n u + (τ/h) v u ]
+ *          + sum_F int_{F∩Ω} [ -{∂_n v}[u] - [v]{∂_n u} + (γ/h)[v][u] ]
+ *          + sum_{F touching a cut cell} sum_{j=0..p} g_j h^(2j-1) int_F [∂_n^j v][∂_n^j u]
+ *
+ * evaluated matrix-free as v = A·u (eq:matrixfreeopcompact P:209-212):
+ * structured (tensor Gauss, sum factorisation) on uncut cells and faces,
+ * unstructured per-point tensor evaluation on cut cells / interface / cut faces
+ * (§3.2, Alg. 1-2).  All arithmetic is FP64.
+ *
+ * Conventions
+ *  - Background mesh: n_cells[0..2] cubic cells of edge h, lower corner `lower`.
+ *    Cell (i,j,k) has reference coords xi = (x - lower)/h - (i,j,k) in [0,1]^3.
+ *  - Basis: Lagrange polynomials of degree p on the p+1 Gauss-Lobatto nodes of
+ *    [0,1] per direction; local DoF l = a + n*b + n^2*c, n = p+1, x
+ *    fastest.  Global DoF = block*n^3 + l, block = row of active_ijk.
+ *  - Ω = {phi < 0}; [·] = (·)^- - (·)^+, {·} = mean; minus = the cell with
+ *    the lower coordinate on the face axis, n = +e_d.
+ *  - Faces between two active cells that are NOT listed in sf_* are full faces
+ *    fully inside Ω (structured SIPG).  A listed face uses its points (s,t = the
+ *    two in-face axes in ascending order, W physical); an empty point range
+ *    means face∩Ω = ∅ (no SIPG).  Faces of the background box carry no term.
+ *  - Ghost-penalty faces (both cells active, >= 1 is_cut) are derived here.
+ *
+ * Return codes: 0 OK, -1 EINVAL, -2 ENOMEM, -3 ECUDA, -4 ENCCL, -5 EUNSUPPORTED.
+ * On error cutfem_last_error() returns a thread-local message.
+ */
+#ifndef CUTFEM_H
+#define CUTFEM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CUTFEM_OK 0
+#define CUTFEM_EINVAL (-1)
+#define CUTFEM_ENOMEM (-2)
+#define CUTFEM_ECUDA (-3)
+#define CUTFEM_ENCCL (-4)
+#define CUTFEM_EUNSUPPORTED (-5)
+
+/* term_mask bits (per-term parity) */
+#define CUTFEM_TERM_CELL 1u    /* volume ∫∇v·∇u (uncut + cut cells)            */
+#define CUTFEM_TERM_SIPG 2u    /* interior-face SIPG (structured + cut faces)   */
+#define CUTFEM_TERM_NITSCHE 4u /* interface Nitsche terms on Γ                  */
+#define CUTFEM_TERM_GP 8u      /* face ghost penalty, orders 0..p              */
+#define CUTFEM_TERM_ALL 15u
+
+typedef struct cutfem_handle cutfem_handle; /* opaque */
+
+/* Problem description.  All pointers are HOST pointers; cutfem_setup deep-copies
+ * them, so the caller may free them as soon as it returns. */
+typedef struct {
+  int32_t n_cells[3];
+  double lower[3];
+  double h;                  /* cell edge (cubic cells)                           */
+  int32_t degree;            /* p in 1..8 (BASELINE "k")                          */
+  int64_t n_active;
+  const int32_t *active_ijk; /* [n_active][3]: defines the u/v block order         */
+  const uint8_t *is_cut;     /* [n_active]: 0 uncut (structured), 1 cut            */
+  const int64_t *vol_ptr;    /* [n_cut+1], cut cells in block order               */
+  const double *vol_pts;     /* [n_vol][4]: xi,eta,zeta in [0,1], W = physical JxW */
+  const int64_t *srf_ptr;    /* [n_cut+1]                                          */
+  const double *srf_pts;     /* [n_srf][7]: xi,eta,zeta, nx,ny,nz (unit, out of Ω), W */
+  int64_t n_sfaces;          /* faces between two active cells not fully inside Ω */
+  const int32_t *sf_cells;   /* [n_sfaces][2] (minus, plus) block ids              */
+  const uint8_t *sf_axis;    /* [n_sfaces] 0..2                                     */
+  const int64_t *sf_ptr;     /* [n_sfaces+1]                                        */
+  const double *sf_pts;      /* [n_fp][3]: s,t in [0,1], W physical                 */
+  double sipg_gamma;         /* sigma = sipg_gamma / h (BASELINE: 10 p^2)           */
+  double nitsche_tau;        /* tau   = nitsche_tau / h (BASELINE: 10 p^2)          */
+  const double *gp_gamma;    /* [degree+1]: weight gp_gamma[j] * h^(2j-1) (BASELINE 0.1) */
+  uint32_t term_mask;        /* CUTFEM_TERM_* bits; 0 means ALL                      */
+} cutfem_problem;
+
+typedef struct {
+  int64_t n_active, n_uncut, n_cut;
+  int64_t n_vol_pts, n_srf_pts, n_face_pts;
+  int64_t n_faces_struct;    /* interior faces with structured SIPG              */
+  int64_t n_faces_cut;       /* listed faces with >= 1 point                     */
+  int64_t n_faces_empty;     /* listed faces with no point                       */
+  int64_t n_faces_gp;        /* ghost-penalty faces                              */
+  int64_t n_dofs;
+  int32_t degree;
+  int32_t device;
+  int64_t dev_bytes;         /* device memory held by the handle                  */
+  int32_t launches_per_apply;
+  int32_t reserved;
+} cutfem_stats_t;
+
+/* Build device tables for `pb` on CUDA device `device`.  Validation failures
+ * (degree outside 1..8, points outside [0,1] by > 1e-12, |n|-1 > 1e-10, W < 0,
+ * inconsistent sizes, listed faces that are not between adjacent active cells
+ * or that touch an uncut cell) return CUTFEM_EINVAL and leave *out NULL. */
+int cutfem_setup(const cutfem_problem *pb, int device, cutfem_handle **out);
+
+/* v = A u.  u_dev, v_dev: DEVICE pointers to n_active*(p+1)^3 doubles
+ * (caller-owned, 8-byte aligned, must not alias).  v is fully overwritten.
+ * Stream-ordered on `cuda_stream` (a cudaStream_t, NULL = legacy default);
+ * no host synchronisation.  One apply in flight per handle. */
+int cutfem_apply(cutfem_handle *hd, const double *u_dev, double *v_dev, void *cuda_stream);
+
+/* Same operator with HOST buffers: copies u host->device, applies, copies
+ * v device->host, synchronises the stream (the end-to-end path). */
+int cutfem_apply_host(cutfem_handle *hd, const double *u_host, double *v_host, void *cuda_stream);
+
+/* Sparse-matrix comparison path (P:224-227 eq:matrixbasedop).
+ * cutfem_csr_assemble builds the global CSR matrix ON THE DEVICE from the same
+ * operator by probing (local matrices column by column through unit vectors,
+ * P:228), using a distance-2 colouring of the face-neighbour graph.
+ * cutfem_csr_setup instead uploads a host CSR (int32 columns).  Both replace
+ * any previously held matrix.  cutfem_csr_apply computes v = A_csr u
+ * (cuSPARSE SpMV, FP64).  *nnz_out (may be NULL) receives the nnz. */
+int cutfem_csr_assemble(cutfem_handle *hd, int64_t *nnz_out);
+int cutfem_csr_setup(cutfem_handle *hd, int64_t n_rows, const int64_t *row_ptr,
+                     const int32_t *col, const double *val);
+int cutfem_csr_apply(cutfem_handle *hd, const double *u_dev, double *v_dev, void *cuda_stream);
+/* Copy the device CSR to host arrays sized by cutfem_csr_nnz (for tests). */
+int64_t cutfem_csr_nnz(const cutfem_handle *hd);
+int cutfem_csr_download(const cutfem_handle *hd, int64_t *row_ptr, int32_t *col, double *val);
+
+int cutfem_stats(const cutfem_handle *hd, cutfem_stats_t *out);
+const char *cutfem_last_error(void);
+int cutfem_destroy(cutfem_handle *hd);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CUTFEM_H */

@@ -1,0 +1,231 @@
+"""ctypes binding of libcutfem.so (include/cutfem.h).  Marshalling only."""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+_SO = os.path.join(_HERE, "libcutfem.so")
+_SRC_DIR = os.path.join(_HERE, "csrc")
+_HDR = os.path.join(_ROOT, "include", "cutfem.h")
+
+TERM_CELL, TERM_SIPG, TERM_NITSCHE, TERM_GP = 1, 2, 4, 8
+TERM_ALL = 15
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+
+def lib_path() -> str:
+    return _SO
+
+
+def _sources():
+    return [os.path.join(_SRC_DIR, f) for f in sorted(os.listdir(_SRC_DIR))] + [_HDR]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libcutfem.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    stale = force or not os.path.exists(_SO) or any(
+        os.path.getmtime(s) > os.path.getmtime(_SO) for s in _sources())
+    if stale:
+        cmd = ["nvcc", *NVCC_FLAGS, "-I", os.path.join(_ROOT, "include"), "-o", _SO,
+               os.path.join(_SRC_DIR, "cutfem.cu"), "-lcusparse"]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.check_call(cmd)
+    return _SO
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [
+        ("n_cells", ctypes.c_int32 * 3), ("lower", ctypes.c_double * 3), ("h", ctypes.c_double),
+        ("degree", ctypes.c_int32), ("n_active", ctypes.c_int64),
+        ("active_ijk", ctypes.c_void_p), ("is_cut", ctypes.c_void_p),
+        ("vol_ptr", ctypes.c_void_p), ("vol_pts", ctypes.c_void_p),
+        ("srf_ptr", ctypes.c_void_p), ("srf_pts", ctypes.c_void_p),
+        ("n_sfaces", ctypes.c_int64), ("sf_cells", ctypes.c_void_p), ("sf_axis", ctypes.c_void_p),
+        ("sf_ptr", ctypes.c_void_p), ("sf_pts", ctypes.c_void_p),
+        ("sipg_gamma", ctypes.c_double), ("nitsche_tau", ctypes.c_double),
+        ("gp_gamma", ctypes.c_void_p), ("term_mask", ctypes.c_uint32),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in (
+        "n_active", "n_uncut", "n_cut", "n_vol_pts", "n_srf_pts", "n_face_pts", "n_faces_struct",
+        "n_faces_cut", "n_faces_empty", "n_faces_gp", "n_dofs")] + [
+        ("degree", ctypes.c_int32), ("device", ctypes.c_int32), ("dev_bytes", ctypes.c_int64),
+        ("launches_per_apply", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+EXPORTS = ["cutfem_setup", "cutfem_apply", "cutfem_apply_host", "cutfem_csr_assemble",
+           "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_nnz", "cutfem_csr_download",
+           "cutfem_stats", "cutfem_last_error", "cutfem_destroy"]
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load libcutfem.so; raises if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or _SO
+    if not os.path.exists(p):
+        raise RuntimeError(f"libcutfem.so not built ({p}); run __graft_entry__.build()")
+    L = ctypes.CDLL(p)
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    L.cutfem_setup.argtypes = [ctypes.POINTER(_Problem), i32, ctypes.POINTER(vp)]
+    L.cutfem_apply.argtypes = [vp, vp, vp, vp]
+    L.cutfem_apply_host.argtypes = [vp, vp, vp, vp]
+    L.cutfem_csr_assemble.argtypes = [vp, ctypes.POINTER(i64)]
+    L.cutfem_csr_setup.argtypes = [vp, i64, vp, vp, vp]
+    L.cutfem_csr_apply.argtypes = [vp, vp, vp, vp]
+    L.cutfem_csr_nnz.argtypes = [vp]
+    L.cutfem_csr_nnz.restype = i64
+    L.cutfem_csr_download.argtypes = [vp, vp, vp, vp]
+    L.cutfem_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+    L.cutfem_last_error.restype = ctypes.c_char_p
+    L.cutfem_destroy.argtypes = [vp]
+    for name in ("cutfem_setup", "cutfem_apply", "cutfem_apply_host", "cutfem_csr_assemble",
+                 "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_download", "cutfem_stats",
+                 "cutfem_destroy"):
+        getattr(L, name).restype = i32
+    if path is None:
+        _lib = L
+    return L
+
+
+def _check(rc):
+    if rc != 0:
+        raise RuntimeError(f"cutfem error {rc}: {load().cutfem_last_error().decode()}")
+
+
+def _ptr(a):
+    return a.ctypes.data if a is not None and a.size else None
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class CutFEM:
+    """Handle for v = A u on one GPU.  ``prob`` is a cutgen.Problem (or anything
+    with the same fields).  Device vectors are torch.float64 CUDA tensors."""
+
+    def __init__(self, prob, device: int = 0, term_mask: int = TERM_ALL):
+        L = load()
+        self._keep = keep = {
+            "ijk": np.ascontiguousarray(prob.active_ijk, dtype=np.int32),
+            "cut": np.ascontiguousarray(prob.is_cut, dtype=np.uint8),
+            "vp": np.ascontiguousarray(prob.vol_ptr, dtype=np.int64),
+            "vx": np.ascontiguousarray(prob.vol_pts, dtype=np.float64),
+            "sp": np.ascontiguousarray(prob.srf_ptr, dtype=np.int64),
+            "sx": np.ascontiguousarray(prob.srf_pts, dtype=np.float64),
+            "fc": np.ascontiguousarray(prob.sf_cells, dtype=np.int32),
+            "fa": np.ascontiguousarray(prob.sf_axis, dtype=np.uint8),
+            "fp": np.ascontiguousarray(prob.sf_ptr, dtype=np.int64),
+            "fx": np.ascontiguousarray(prob.sf_pts, dtype=np.float64),
+            "gp": np.ascontiguousarray(prob.gp_gamma, dtype=np.float64),
+        }
+        pb = _Problem()
+        for i in range(3):
+            pb.n_cells[i] = int(prob.n_cells[i])
+            pb.lower[i] = float(prob.lower[i])
+        pb.h = float(prob.h)
+        pb.degree = int(prob.degree)
+        pb.n_active = keep["ijk"].shape[0]
+        pb.active_ijk, pb.is_cut = _ptr(keep["ijk"]), _ptr(keep["cut"])
+        pb.vol_ptr, pb.vol_pts = _ptr(keep["vp"]), _ptr(keep["vx"])
+        pb.srf_ptr, pb.srf_pts = _ptr(keep["sp"]), _ptr(keep["sx"])
+        pb.n_sfaces = keep["fc"].shape[0]
+        pb.sf_cells, pb.sf_axis = _ptr(keep["fc"]), _ptr(keep["fa"])
+        pb.sf_ptr, pb.sf_pts = _ptr(keep["fp"]), _ptr(keep["fx"])
+        pb.sipg_gamma, pb.nitsche_tau = float(prob.sipg_gamma), float(prob.nitsche_tau)
+        pb.gp_gamma = _ptr(keep["gp"])
+        pb.term_mask = int(term_mask)
+        h = ctypes.c_void_p()
+        _check(L.cutfem_setup(ctypes.byref(pb), int(device), ctypes.byref(h)))
+        self._h = h
+        self._L = L
+        self.device = device
+        self.degree = int(prob.degree)
+        self.n_dofs = int(keep["ijk"].shape[0]) * (self.degree + 1) ** 3
+        del self._keep  # setup deep-copied everything
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(self._L.cutfem_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def apply(self, u, v=None, stream=None):
+        """v = A u on the device (torch float64 CUDA tensors), stream-ordered."""
+        import torch
+        if v is None:
+            v = torch.empty_like(u)
+        assert u.dtype == torch.float64 and v.dtype == torch.float64 and u.is_cuda and v.is_cuda
+        assert u.numel() == self.n_dofs and v.numel() == self.n_dofs
+        assert u.is_contiguous() and v.is_contiguous()
+        _check(self._L.cutfem_apply(self._h, u.data_ptr(), v.data_ptr(), _stream_ptr(stream)))
+        return v
+
+    def apply_host(self, u: np.ndarray, v: np.ndarray | None = None, stream=0) -> np.ndarray:
+        """End-to-end path: host u -> device -> A u -> host v (synchronous)."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        if v is None:
+            v = np.empty_like(u)
+        assert u.size == self.n_dofs and v.size == self.n_dofs and v.flags.c_contiguous
+        _check(self._L.cutfem_apply_host(self._h, u.ctypes.data, v.ctypes.data,
+                                         _stream_ptr(stream) if stream else None))
+        return v
+
+    def csr_assemble(self) -> int:
+        nnz = ctypes.c_int64()
+        _check(self._L.cutfem_csr_assemble(self._h, ctypes.byref(nnz)))
+        return int(nnz.value)
+
+    def csr_setup(self, row_ptr, col, val):
+        row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        col = np.ascontiguousarray(col, dtype=np.int32)
+        val = np.ascontiguousarray(val, dtype=np.float64)
+        _check(self._L.cutfem_csr_setup(self._h, row_ptr.size - 1, row_ptr.ctypes.data,
+                                        col.ctypes.data, val.ctypes.data))
+
+    def csr_apply(self, u, v=None, stream=None):
+        import torch
+        if v is None:
+            v = torch.empty_like(u)
+        _check(self._L.cutfem_csr_apply(self._h, u.data_ptr(), v.data_ptr(), _stream_ptr(stream)))
+        return v
+
+    def csr_download(self):
+        nnz = int(self._L.cutfem_csr_nnz(self._h))
+        rp = np.zeros(self.n_dofs + 1, dtype=np.int64)
+        col = np.zeros(nnz, dtype=np.int32)
+        val = np.zeros(nnz, dtype=np.float64)
+        _check(self._L.cutfem_csr_download(self._h, rp.ctypes.data, col.ctypes.data, val.ctypes.data))
+        return rp, col, val
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.cutfem_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

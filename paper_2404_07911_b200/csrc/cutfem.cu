@@ -1,0 +1,489 @@
+// cutfem.cu — C ABI (include/cutfem.h): setup, stream-ordered apply, CSR path.
+//
+// setup (host, once; SURVEY §3 call stack 2): validate the arrays, build the
+// 1-D tables (tables.h), the per-cell descriptors (face neighbours, face types,
+// ghost-penalty faces), sort cut cells by decreasing point count (heaviest
+// first: "cut cells are batched by quadrature-point count", north_star), and
+// upload everything.  apply: the structured kernel on the caller's stream and
+// the unstructured kernel on a forked side stream (they write disjoint v
+// blocks), joined by an event — no host synchronisation.
+#include <cuda_runtime.h>
+#include <cusparse.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/cutfem.h"
+#include "kernels.cuh"
+#include "tables.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(CUTFEM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+}  // namespace
+
+struct cutfem_handle {
+  int device = 0;
+  int degree = 1;
+  int n = 2;
+  double h = 1;
+  int64_t n_active = 0, n_uncut = 0, n_cut = 0;
+  uint32_t mask = CUTFEM_TERM_ALL;
+  KParams kp;
+  FaceTab ft;
+  UDesc *d_udesc = nullptr;
+  CDesc *d_cdesc = nullptr;
+  double *d_vol = nullptr, *d_srf = nullptr, *d_sfp = nullptr;
+  int64_t *d_volptr = nullptr, *d_srfptr = nullptr, *d_sfptr = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // host path buffers
+  double *d_u = nullptr, *d_v = nullptr;
+  // CSR
+  int64_t csr_nnz = 0;
+  bool csr_i64 = false;
+  void *d_rowptr = nullptr, *d_col = nullptr;
+  double *d_val = nullptr;
+  void *d_spbuf = nullptr;
+  size_t spbuf_size = 0;
+  cusparseHandle_t sp = nullptr;
+  cusparseSpMatDescr_t spA = nullptr;
+  std::vector<uint8_t> color;  // (i + 2j + 3k) mod 7, distance-2 colouring for CSR probing
+  cutfem_stats_t stats;
+  int64_t dev_bytes = 0;
+};
+
+namespace {
+
+template <class T>
+int upload(cutfem_handle *hd, T **dst, const T *src, size_t count) {
+  size_t bytes = sizeof(T) * std::max<size_t>(count, 1);
+  cudaError_t e = cudaMalloc((void **)dst, bytes);
+  if (e != cudaSuccess) return fail(CUTFEM_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  hd->dev_bytes += (int64_t)bytes;
+  if (count) CU(cudaMemcpy(*dst, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+void make_eo(int n, const std::vector<long double> &Mx, EO &out) {
+  std::memset(&out, 0, sizeof(out));
+  const int H = n / 2, HC = (n + 1) / 2;
+  for (int i = 0; i < HC; ++i) {
+    for (int j = 0; j < H; ++j)
+      out.E[i * HC + j] = (double)((Mx[i * n + j] + Mx[i * n + (n - 1 - j)]) / 2);
+    if (n & 1) out.E[i * HC + H] = (double)Mx[i * n + H];
+  }
+  for (int i = 0; i < H; ++i)
+    for (int j = 0; j < H; ++j) out.O[i * H + j] = (double)((Mx[i * n + j] - Mx[i * n + (n - 1 - j)]) / 2);
+}
+
+int upload_tables(int p) {
+  cutfem_tables::Ref r = cutfem_tables::build(p);
+  const int n = p + 1;
+  RefTab t;
+  std::memset(&t, 0, sizeof(t));
+  std::vector<long double> St(n * n);
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b < n; ++b) St[a * n + b] = r.S[b * n + a];
+  make_eo(n, r.S, t.S);
+  make_eo(n, St, t.St);
+  make_eo(n, r.Kc, t.Kc);
+  make_eo(n, r.M, t.M);
+  for (int a = 0; a < n; ++a) {
+    t.x[a] = (double)r.x[a];
+    t.cinv[a] = (double)r.cinv[a];
+    t.gw[a] = (double)r.w[a];
+    t.d0[a] = (double)r.tr[(1 * 2 + 0) * n + a];
+    t.d1[a] = (double)r.tr[(1 * 2 + 1) * n + a];
+  }
+  CU(cudaMemcpyToSymbol(c_ref, &t, sizeof(RefTab), sizeof(RefTab) * (n - 2)));
+  return 0;
+}
+
+void build_facetab(int p, double h, const double *gpg, FaceTab &ft) {
+  cutfem_tables::Ref r = cutfem_tables::build(p);
+  const int n = p + 1;
+  std::memset(&ft, 0, sizeof(ft));
+  for (int s = 0; s < 2; ++s) {
+    const int own = s == 0 ? 1 : 0, oth = 1 - own;  // s=0: own minus -> traces at xi=1
+    for (int m = 0; m < n; ++m)
+      for (int a = 0; a < n; ++a) {
+        long double goo = 0, gon = 0;
+        for (int j = 0; j <= p; ++j) {
+          long double em = r.tr[(j * 2 + own) * n + m];
+          goo += (long double)gpg[j] * em * r.tr[(j * 2 + own) * n + a];
+          gon += (long double)gpg[j] * em * r.tr[(j * 2 + oth) * n + a];
+        }
+        ft.Goo[s][m * n + a] = (double)(h * goo);
+        ft.Gon[s][m * n + a] = (double)(h * gon);
+      }
+  }
+}
+
+template <int N>
+int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st) {
+  const int64_t nu = hd->n_uncut, nc = hd->n_cut;
+  if (nc > 0) {
+    CU(cudaEventRecord(hd->ev_fork, st));
+    CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
+    k_cut<N><<<(unsigned)nc, CutCfg<N>::THREADS, CutCfg<N>::SMEM, hd->side>>>(
+        u, v, hd->d_cdesc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp,
+        hd->d_sfptr, hd->kp, hd->ft);
+    CU(cudaGetLastError());
+  }
+  if (nu > 0) {
+    using C = UncutCfg<N>;
+    const int per_block = C::WARPS * C::CPW;
+    const unsigned grid = (unsigned)((nu + per_block - 1) / per_block);
+    k_uncut<N><<<grid, 32 * C::WARPS, C::SMEM, st>>>(u, v, hd->d_udesc, (int)nu, hd->kp, hd->ft);
+    CU(cudaGetLastError());
+  }
+  if (nc > 0) {
+    CU(cudaEventRecord(hd->ev_join, hd->side));
+    CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
+  }
+  return 0;
+}
+
+template <int N>
+int set_attrs() {
+  CU(cudaFuncSetAttribute(k_cut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutCfg<N>::SMEM));
+  CU(cudaFuncSetAttribute(k_uncut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncutCfg<N>::SMEM));
+  return 0;
+}
+
+int dispatch_apply(cutfem_handle *hd, const double *u, double *v, cudaStream_t st) {
+  switch (hd->n) {
+    case 2: return launch<2>(hd, u, v, st);
+    case 3: return launch<3>(hd, u, v, st);
+    case 4: return launch<4>(hd, u, v, st);
+    case 5: return launch<5>(hd, u, v, st);
+    case 6: return launch<6>(hd, u, v, st);
+    case 7: return launch<7>(hd, u, v, st);
+    case 8: return launch<8>(hd, u, v, st);
+    case 9: return launch<9>(hd, u, v, st);
+  }
+  return fail(CUTFEM_EUNSUPPORTED, "degree");
+}
+
+int dispatch_attrs(int n) {
+  switch (n) {
+    case 2: return set_attrs<2>();
+    case 3: return set_attrs<3>();
+    case 4: return set_attrs<4>();
+    case 5: return set_attrs<5>();
+    case 6: return set_attrs<6>();
+    case 7: return set_attrs<7>();
+    case 8: return set_attrs<8>();
+    case 9: return set_attrs<9>();
+  }
+  return fail(CUTFEM_EUNSUPPORTED, "degree");
+}
+
+void free_handle(cutfem_handle *hd) {
+  if (!hd) return;
+  cudaFree(hd->d_udesc);
+  cudaFree(hd->d_cdesc);
+  cudaFree(hd->d_vol);
+  cudaFree(hd->d_srf);
+  cudaFree(hd->d_sfp);
+  cudaFree(hd->d_volptr);
+  cudaFree(hd->d_srfptr);
+  cudaFree(hd->d_sfptr);
+  cudaFree(hd->d_u);
+  cudaFree(hd->d_v);
+  cudaFree(hd->d_rowptr);
+  cudaFree(hd->d_col);
+  cudaFree(hd->d_val);
+  cudaFree(hd->d_spbuf);
+  if (hd->spA) cusparseDestroySpMat(hd->spA);
+  if (hd->sp) cusparseDestroy(hd->sp);
+  if (hd->side) cudaStreamDestroy(hd->side);
+  if (hd->ev_fork) cudaEventDestroy(hd->ev_fork);
+  if (hd->ev_join) cudaEventDestroy(hd->ev_join);
+  delete hd;
+}
+
+int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
+  if (!pb) return fail(CUTFEM_EINVAL, "null problem");
+  const int p = pb->degree;
+  if (p < 1 || p > 8) return fail(CUTFEM_EINVAL, "degree must be in 1..8");
+  if (!(pb->h > 0)) return fail(CUTFEM_EINVAL, "h must be > 0");
+  for (int i = 0; i < 3; ++i)
+    if (pb->n_cells[i] < 1) return fail(CUTFEM_EINVAL, "n_cells must be >= 1");
+  if (pb->n_active < 0 || (pb->n_active > 0 && (!pb->active_ijk || !pb->is_cut)))
+    return fail(CUTFEM_EINVAL, "active arrays");
+  if (!pb->gp_gamma) return fail(CUTFEM_EINVAL, "gp_gamma is NULL");
+  const int n = p + 1;
+  const int64_t na = pb->n_active;
+  const int64_t nx = pb->n_cells[0], ny = pb->n_cells[1], nz = pb->n_cells[2];
+  if ((double)na * n * n * n > 9.0e18) return fail(CUTFEM_EINVAL, "too many DoFs");
+  hd->device = device;
+  hd->degree = p;
+  hd->n = n;
+  hd->h = pb->h;
+  hd->n_active = na;
+  hd->mask = pb->term_mask ? pb->term_mask : CUTFEM_TERM_ALL;
+  CU(cudaSetDevice(device));
+  // grid -> block map
+  std::vector<int32_t> grid((size_t)(nx * ny * nz), -1);
+  std::vector<int64_t> cut_ord(na, -1);
+  int64_t nc = 0;
+  for (int64_t b = 0; b < na; ++b) {
+    const int32_t i = pb->active_ijk[3 * b], j = pb->active_ijk[3 * b + 1], k = pb->active_ijk[3 * b + 2];
+    if (i < 0 || j < 0 || k < 0 || i >= nx || j >= ny || k >= nz)
+      return fail(CUTFEM_EINVAL, "active_ijk out of range");
+    int32_t &g = grid[(size_t)((i * ny + j) * nz + k)];
+    if (g >= 0) return fail(CUTFEM_EINVAL, "duplicate active cell");
+    g = (int32_t)b;
+    if (pb->is_cut[b]) cut_ord[b] = nc++;
+  }
+  hd->color.resize(na);
+  for (int64_t b = 0; b < na; ++b)
+    hd->color[b] = (uint8_t)((pb->active_ijk[3 * b] + 2 * pb->active_ijk[3 * b + 1] + 3 * pb->active_ijk[3 * b + 2]) % 7);
+  hd->n_cut = nc;
+  hd->n_uncut = na - nc;
+  if (nc > 0 && (!pb->vol_ptr || !pb->srf_ptr)) return fail(CUTFEM_EINVAL, "vol_ptr/srf_ptr NULL");
+  const int64_t nvol = nc ? pb->vol_ptr[nc] : 0, nsrf = nc ? pb->srf_ptr[nc] : 0;
+  if (nc && (pb->vol_ptr[0] != 0 || pb->srf_ptr[0] != 0)) return fail(CUTFEM_EINVAL, "ptr[0] != 0");
+  for (int64_t c = 0; c < nc; ++c)
+    if (pb->vol_ptr[c + 1] < pb->vol_ptr[c] || pb->srf_ptr[c + 1] < pb->srf_ptr[c])
+      return fail(CUTFEM_EINVAL, "ptr not monotone");
+  if ((nvol && !pb->vol_pts) || (nsrf && !pb->srf_pts)) return fail(CUTFEM_EINVAL, "points NULL");
+  const double tol = 1e-12;
+  for (int64_t q = 0; q < nvol; ++q) {
+    const double *x = pb->vol_pts + 4 * q;
+    for (int d = 0; d < 3; ++d)
+      if (!(x[d] >= -tol && x[d] <= 1 + tol)) return fail(CUTFEM_EINVAL, "volume point outside [0,1]^3");
+    if (!(x[3] >= 0)) return fail(CUTFEM_EINVAL, "negative volume weight");
+  }
+  for (int64_t q = 0; q < nsrf; ++q) {
+    const double *x = pb->srf_pts + 7 * q;
+    for (int d = 0; d < 3; ++d)
+      if (!(x[d] >= -tol && x[d] <= 1 + tol)) return fail(CUTFEM_EINVAL, "surface point outside [0,1]^3");
+    const double nn = std::sqrt(x[3] * x[3] + x[4] * x[4] + x[5] * x[5]);
+    if (!(std::fabs(nn - 1) <= 1e-10)) return fail(CUTFEM_EINVAL, "surface normal not unit");
+    if (!(x[6] >= 0)) return fail(CUTFEM_EINVAL, "negative surface weight");
+  }
+  // listed faces
+  const int64_t nsf = pb->n_sfaces;
+  if (nsf < 0 || (nsf > 0 && (!pb->sf_cells || !pb->sf_axis || !pb->sf_ptr)))
+    return fail(CUTFEM_EINVAL, "sf arrays");
+  const int64_t nfp = nsf ? pb->sf_ptr[nsf] : 0;
+  if (nsf && pb->sf_ptr[0] != 0) return fail(CUTFEM_EINVAL, "sf_ptr[0] != 0");
+  if (nfp && !pb->sf_pts) return fail(CUTFEM_EINVAL, "sf_pts NULL");
+  for (int64_t q = 0; q < nfp; ++q) {
+    const double *x = pb->sf_pts + 3 * q;
+    if (!(x[0] >= -tol && x[0] <= 1 + tol && x[1] >= -tol && x[1] <= 1 + tol))
+      return fail(CUTFEM_EINVAL, "face point outside [0,1]^2");
+    if (!(x[2] >= 0)) return fail(CUTFEM_EINVAL, "negative face weight");
+  }
+  // sf index per (cell, face)
+  std::vector<int32_t> sfid((size_t)na * 6, -1);
+  int64_t n_fcut = 0, n_fempty = 0;
+  for (int64_t f = 0; f < nsf; ++f) {
+    const int32_t m = pb->sf_cells[2 * f], pl = pb->sf_cells[2 * f + 1];
+    const int d = pb->sf_axis[f];
+    if (d > 2 || m < 0 || pl < 0 || m >= na || pl >= na) return fail(CUTFEM_EINVAL, "bad listed face");
+    if (pb->sf_ptr[f + 1] < pb->sf_ptr[f]) return fail(CUTFEM_EINVAL, "sf_ptr not monotone");
+    for (int t = 0; t < 3; ++t) {
+      const int32_t want = pb->active_ijk[3 * m + t] + (t == d ? 1 : 0);
+      if (pb->active_ijk[3 * pl + t] != want) return fail(CUTFEM_EINVAL, "listed face cells not adjacent");
+    }
+    if (!pb->is_cut[m] || !pb->is_cut[pl])
+      return fail(CUTFEM_EINVAL, "listed face touches an uncut cell (its faces are inside Ω)");
+    if (sfid[m * 6 + 2 * d + 1] >= 0) return fail(CUTFEM_EINVAL, "duplicate listed face");
+    sfid[m * 6 + 2 * d + 1] = (int32_t)f;
+    sfid[pl * 6 + 2 * d] = (int32_t)f;
+    if (pb->sf_ptr[f + 1] > pb->sf_ptr[f]) ++n_fcut; else ++n_fempty;
+  }
+  // descriptors
+  std::vector<UDesc> ud;
+  std::vector<CDesc> cd;
+  std::vector<int64_t> ccost;
+  ud.reserve(na - nc);
+  cd.reserve(nc);
+  int64_t n_struct = 0, n_gp = 0;
+  for (int64_t b = 0; b < na; ++b) {
+    const int32_t ijk[3] = {pb->active_ijk[3 * b], pb->active_ijk[3 * b + 1], pb->active_ijk[3 * b + 2]};
+    int32_t nb[6];
+    for (int f = 0; f < 6; ++f) {
+      int32_t q[3] = {ijk[0], ijk[1], ijk[2]};
+      const int d = f >> 1;
+      q[d] += (f & 1) ? 1 : -1;
+      const int64_t lim = pb->n_cells[d];
+      nb[f] = (q[d] < 0 || q[d] >= lim) ? -1 : grid[(size_t)((q[0] * ny + q[1]) * nz + q[2])];
+    }
+    const bool cut = pb->is_cut[b] != 0;
+    if (!cut) {
+      UDesc u;
+      std::memset(&u, 0, sizeof(u));
+      u.blk = (int32_t)b;
+      for (int f = 0; f < 6; ++f) {
+        u.nb[f] = nb[f];
+        if (nb[f] >= 0 && pb->is_cut[nb[f]]) u.flags |= 1u << f;
+      }
+      ud.push_back(u);
+    } else {
+      CDesc c;
+      std::memset(&c, 0, sizeof(c));
+      c.blk = (int32_t)b;
+      c.cut = (int32_t)cut_ord[b];
+      int64_t cost = (pb->vol_ptr[c.cut + 1] - pb->vol_ptr[c.cut]) + (pb->srf_ptr[c.cut + 1] - pb->srf_ptr[c.cut]);
+      for (int f = 0; f < 6; ++f) {
+        c.nb[f] = nb[f];
+        c.sf[f] = -1;
+        if (nb[f] < 0) continue;
+        c.flags |= 1u << f;  // ghost penalty: this cell is cut
+        const int32_t s = sfid[b * 6 + f];
+        if (s < 0) {
+          c.flags |= 1u << (6 + f);
+        } else if (pb->sf_ptr[s + 1] > pb->sf_ptr[s]) {
+          c.flags |= 1u << (12 + f);
+          c.sf[f] = s;
+          cost += (pb->sf_ptr[s + 1] - pb->sf_ptr[s]) / 2;
+        }
+      }
+      cd.push_back(c);
+      ccost.push_back(cost);
+    }
+    // count every interior face once, from its minus side (hi face f = 2d+1)
+    for (int d = 0; d < 3; ++d) {
+      const int32_t q = nb[2 * d + 1];
+      if (q < 0) continue;
+      if (cut || pb->is_cut[q]) ++n_gp;
+      if (sfid[b * 6 + 2 * d + 1] < 0) ++n_struct;
+    }
+  }
+  // heaviest cut cells first (LPT order for the block scheduler)
+  {
+    std::vector<int64_t> order(cd.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int64_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return ccost[a] > ccost[b]; });
+    std::vector<CDesc> s(cd.size());
+    for (size_t i = 0; i < order.size(); ++i) s[i] = cd[order[i]];
+    cd.swap(s);
+  }
+  int rc;
+  if ((rc = upload(hd, &hd->d_udesc, ud.data(), ud.size()))) return rc;
+  if ((rc = upload(hd, &hd->d_cdesc, cd.data(), cd.size()))) return rc;
+  if ((rc = upload(hd, &hd->d_vol, pb->vol_pts, (size_t)(4 * nvol)))) return rc;
+  if ((rc = upload(hd, &hd->d_srf, pb->srf_pts, (size_t)(7 * nsrf)))) return rc;
+  if ((rc = upload(hd, &hd->d_sfp, pb->sf_pts, (size_t)(3 * nfp)))) return rc;
+  if ((rc = upload(hd, &hd->d_volptr, pb->vol_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
+  if ((rc = upload(hd, &hd->d_srfptr, pb->srf_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
+  if ((rc = upload(hd, &hd->d_sfptr, pb->sf_ptr, (size_t)(nsf ? nsf + 1 : 0)))) return rc;
+  if ((rc = upload_tables(p))) return rc;
+  if ((rc = dispatch_attrs(n))) return rc;
+  build_facetab(p, pb->h, pb->gp_gamma, hd->ft);
+  hd->kp.h = pb->h;
+  hd->kp.sigma = pb->sipg_gamma / pb->h;
+  hd->kp.tau = pb->nitsche_tau / pb->h;
+  hd->kp.mask = hd->mask;
+  hd->kp.n_cells = 0;
+  CU(cudaStreamCreateWithFlags(&hd->side, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&hd->ev_fork, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&hd->ev_join, cudaEventDisableTiming));
+  cutfem_stats_t &s = hd->stats;
+  std::memset(&s, 0, sizeof(s));
+  s.n_active = na;
+  s.n_uncut = na - nc;
+  s.n_cut = nc;
+  s.n_vol_pts = nvol;
+  s.n_srf_pts = nsrf;
+  s.n_face_pts = nfp;
+  s.n_faces_struct = n_struct;
+  s.n_faces_cut = n_fcut;
+  s.n_faces_empty = n_fempty;
+  s.n_faces_gp = n_gp;
+  s.n_dofs = na * n * n * n;
+  s.degree = p;
+  s.device = device;
+  s.launches_per_apply = (nc > 0) + (na - nc > 0);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *cutfem_last_error(void) { return g_err.c_str(); }
+
+int cutfem_setup(const cutfem_problem *pb, int device, cutfem_handle **out) {
+  if (!out) return fail(CUTFEM_EINVAL, "out is NULL");
+  *out = nullptr;
+  cutfem_handle *hd = new (std::nothrow) cutfem_handle();
+  if (!hd) return fail(CUTFEM_ENOMEM, "host allocation");
+  int rc = setup_impl(pb, device, hd);
+  if (rc) {
+    free_handle(hd);
+    return rc;
+  }
+  hd->stats.dev_bytes = hd->dev_bytes;
+  *out = hd;
+  return 0;
+}
+
+int cutfem_apply(cutfem_handle *hd, const double *u_dev, double *v_dev, void *cuda_stream) {
+  if (!hd) return fail(CUTFEM_EINVAL, "null handle");
+  if (hd->n_active > 0 && (!u_dev || !v_dev)) return fail(CUTFEM_EINVAL, "null vector");
+  if (u_dev == v_dev && hd->n_active > 0) return fail(CUTFEM_EINVAL, "u and v must not alias");
+  if (((uintptr_t)u_dev | (uintptr_t)v_dev) & 7) return fail(CUTFEM_EINVAL, "vectors must be 8-byte aligned");
+  CU(cudaSetDevice(hd->device));
+  return dispatch_apply(hd, u_dev, v_dev, (cudaStream_t)cuda_stream);
+}
+
+int cutfem_apply_host(cutfem_handle *hd, const double *u_host, double *v_host, void *cuda_stream) {
+  if (!hd) return fail(CUTFEM_EINVAL, "null handle");
+  CU(cudaSetDevice(hd->device));
+  const size_t bytes = sizeof(double) * (size_t)hd->stats.n_dofs;
+  if (!hd->d_u) {
+    CU(cudaMalloc(&hd->d_u, std::max<size_t>(bytes, 8)));
+    CU(cudaMalloc(&hd->d_v, std::max<size_t>(bytes, 8)));
+    hd->dev_bytes += 2 * (int64_t)bytes;
+  }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  CU(cudaMemcpyAsync(hd->d_u, u_host, bytes, cudaMemcpyHostToDevice, st));
+  int rc = dispatch_apply(hd, hd->d_u, hd->d_v, st);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(v_host, hd->d_v, bytes, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int cutfem_stats(const cutfem_handle *hd, cutfem_stats_t *out) {
+  if (!hd || !out) return fail(CUTFEM_EINVAL, "null");
+  *out = hd->stats;
+  out->dev_bytes = hd->dev_bytes;
+  return 0;
+}
+
+int cutfem_destroy(cutfem_handle *hd) {
+  if (!hd) return 0;
+  cudaSetDevice(hd->device);
+  cudaDeviceSynchronize();
+  free_handle(hd);
+  return 0;
+}
+
+}  // extern "C"
+
+#include "csr.inl"

@@ -1,0 +1,713 @@
+// sm_100a FP64 kernels of the DG-CutFEM operator apply (included by cutfem.cu).
+//
+// Two element-centric kernels; every v block is written exactly once by the
+// kernel that owns its cell, so no atomics are needed (BASELINE north_star:
+// "Face contributions use warp-level primitives or element-centric loops so
+// that no atomics land on the hot path").  Each cell also evaluates its own
+// side of the six faces (SIPG, ghost penalty, cut-face SIPG), reading the
+// neighbour blocks from L2.
+//
+//   k_uncut<N>: structured cells (Alg. 1 "inside" branch): a warp
+//     holds 32/N^2 cells, one lane per 1-D line; sum factorisation with the
+//     even-odd decomposition of every n x n line operator (S, K_c, S^T, M).
+//   k_cut<N>:   unstructured cells (Alg. 1 "intersected" branch):
+//     one CTA per cut cell, one thread per quadrature point for the per-point
+//     tensor evaluation (eq:unstructured_cell), then a DoF-parallel
+//     reduction over points for the integration; faces with the face-normal
+//     reduction + in-face per-point evaluation (eq:unstructured_face P:491-496).
+#pragma once
+#include <cstdint>
+
+#define CUTFEM_NMAX 9
+
+// Even-odd factors of a centro-symmetric n x n matrix M (M[i][j] = M[n-1-i][n-1-j]):
+//   E[i][j] = (M[i][j] + M[i][n-1-j]) / 2 (j < H), E[i][H] = M[i][H] (n odd), i < HC
+//   O[i][j] = (M[i][j] - M[i][n-1-j]) / 2, i, j < H
+// out_i = E_i + O_i, out_{n-1-i} = E_i - O_i: n^2/2 + 2n flops instead of n^2 FMAs.
+struct EO {
+  double E[25];
+  double O[16];
+};
+
+struct RefTab {
+  EO S;   // GLL values -> Gauss values
+  EO St;  // transpose (integration back to GLL)
+  EO Kc;  // D_g^T W D_g on the Gauss collocation points
+  EO M;   // GLL mass
+  double x[CUTFEM_NMAX];     // GLL nodes
+  double cinv[CUTFEM_NMAX];  // 1 / prod_{m != a} (x_a - x_m)
+  double gw[CUTFEM_NMAX];    // Gauss weights
+  double d0[CUTFEM_NMAX];    // l_a'(0)
+  double d1[CUTFEM_NMAX];    // l_a'(1)
+};
+
+__constant__ RefTab c_ref[8];  // index N - 2
+
+// Handle-specific ghost-penalty line operators (h and gp_gamma folded in):
+//   Goo[s][m][a] = h sum_j g_j e_j[m] e_j[a], Gon[s][m][a] = h sum_j g_j e_j[m] o_j[a]
+// with e_j = l^(j)(own face), o_j = l^(j)(neighbour face); s = 0 own cell is the
+// minus side (face at xi_d = 1), s = 1 own cell is the plus side.
+struct FaceTab {
+  double Goo[2][CUTFEM_NMAX * CUTFEM_NMAX];
+  double Gon[2][CUTFEM_NMAX * CUTFEM_NMAX];
+};
+
+struct KParams {
+  double h;      // cell edge
+  double sigma;  // SIPG penalty gamma / h
+  double tau;    // Nitsche penalty tau_D / h
+  uint32_t mask; // CUTFEM_TERM_* bits
+  int32_t n_cells;
+};
+
+// per uncut cell: block id, 6 face neighbours (-1: none / inactive), GP bits
+struct __align__(16) UDesc {
+  int32_t blk;
+  int32_t nb[6];
+  uint32_t flags;  // bit f: ghost penalty on face f (neighbour cut)
+};
+
+// per cut cell
+struct __align__(16) CDesc {
+  int32_t blk;
+  int32_t nb[6];
+  uint32_t flags;  // bit f: GP; bit 6+f: structured SIPG; bit 12+f: cut-face SIPG (points)
+  int32_t sf[6];   // face-point list index for cut faces, else -1
+  int32_t cut;     // ordinal in vol_ptr / srf_ptr
+  int32_t pad;
+};
+
+#define TERM_CELL 1u
+#define TERM_SIPG 2u
+#define TERM_NITSCHE 4u
+#define TERM_GP 8u
+
+template <int N>
+__device__ __forceinline__ void eo_mv(const EO &m, const double (&in)[N], double (&out)[N]) {
+  constexpr int H = N / 2, HC = (N + 1) / 2;
+  double e[HC], o[H];
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    e[j] = in[j] + in[N - 1 - j];
+    o[j] = in[j] - in[N - 1 - j];
+  }
+  if (N & 1) e[H] = in[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    double E = 0.0, O = 0.0;
+#pragma unroll
+    for (int j = 0; j < HC; ++j) E = fma(m.E[i * HC + j], e[j], E);
+#pragma unroll
+    for (int j = 0; j < H; ++j) O = fma(m.O[i * H + j], o[j], O);
+    out[i] = E + O;
+    out[N - 1 - i] = E - O;
+  }
+  if (N & 1) {
+    double E = 0.0;
+#pragma unroll
+    for (int j = 0; j < HC; ++j) E = fma(m.E[H * HC + j], e[j], E);
+    out[H] = E;
+  }
+}
+
+// Padded cell block in shared memory: index (c*N + b)*P + a, P = N+1, so that
+// the lines of all three directions are bank-conflict free.
+template <int N>
+struct Blk {
+  static constexpr int P = N + 1;
+  static constexpr int NN = N * N;
+  static constexpr int N3 = N * N * N;
+  static constexpr int SZ = N * N * P;
+  __device__ static __forceinline__ int pad(int l) { return (l / N) * P + (l % N); }
+  // line t (t = t0 + N*t1, t0 along the lower in-face axis) in direction d
+  __device__ static __forceinline__ void line(int d, int t, int &base, int &stride) {
+    const int t0 = t % N, t1 = t / N;
+    if (d == 0) {
+      base = (t1 * N + t0) * P;
+      stride = 1;
+    } else if (d == 1) {
+      base = t1 * N * P + t0;
+      stride = P;
+    } else {
+      base = t1 * P + t0;
+      stride = N * P;
+    }
+  }
+};
+
+// MODE 0: dst = M src; MODE 1: dst += s * M src; MODE 2: dst = s * M src
+template <int N, int MODE>
+__device__ __forceinline__ void sweep_line(const double *src, double *dst, int base, int stride,
+                                           const EO &m, double s) {
+  double in[N], out[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) in[k] = src[base + k * stride];
+  eo_mv<N>(m, in, out);
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    if (MODE == 0) dst[base + k * stride] = out[k];
+    else if (MODE == 1) dst[base + k * stride] = fma(s, out[k], dst[base + k * stride]);
+    else dst[base + k * stride] = s * out[k];
+  }
+}
+
+// 1-D Lagrange basis values and derivatives at t (product form with prefix /
+// suffix products; "evaluate the actual polynomial basis by 1D evaluations").
+template <int N>
+__device__ __forceinline__ void basis_vd(const RefTab &R, double t, double (&v)[N], double (&dv)[N]) {
+  double d[N], pre[N], dpre[N];
+#pragma unroll
+  for (int m = 0; m < N; ++m) d[m] = t - R.x[m];
+  double p = 1.0, dp = 0.0;
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    pre[a] = p;
+    dpre[a] = dp;
+    dp = fma(dp, d[a], p);
+    p *= d[a];
+  }
+  double s = 1.0, ds = 0.0;
+#pragma unroll
+  for (int a = N - 1; a >= 0; --a) {
+    v[a] = R.cinv[a] * pre[a] * s;
+    dv[a] = R.cinv[a] * fma(dpre[a], s, pre[a] * ds);
+    ds = fma(ds, d[a], s);
+    s *= d[a];
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void basis_v(const RefTab &R, double t, double (&v)[N]) {
+  double d[N], pre[N];
+#pragma unroll
+  for (int m = 0; m < N; ++m) d[m] = t - R.x[m];
+  double p = 1.0;
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+    pre[a] = p;
+    p *= d[a];
+  }
+  double s = 1.0;
+#pragma unroll
+  for (int a = N - 1; a >= 0; --a) {
+    v[a] = R.cinv[a] * pre[a] * s;
+    s *= d[a];
+  }
+}
+
+// ============================================================ uncut cells
+template <int N>
+struct UncutCfg {
+  static constexpr int NN = N * N;
+  static constexpr int LPS = NN <= 32 ? NN : 32;  // lanes per cell slot
+  static constexpr int CPW = NN <= 32 ? 32 / NN : 1;  // cells per warp
+  static constexpr int WARPS = 4;
+  static constexpr int SLOT = 4 * Blk<N>::SZ + 2 * NN;  // U, Q/T, R, NB, FA, FB
+  static constexpr int SMEM = WARPS * CPW * SLOT * 8;
+};
+
+template <int N>
+__global__ void __launch_bounds__(128) k_uncut(const double *__restrict__ u, double *__restrict__ v,
+                                               const UDesc *__restrict__ desc, int ncell, KParams kp,
+                                               FaceTab ft) {
+  using B = Blk<N>;
+  using C = UncutCfg<N>;
+  constexpr int NN = B::NN, N3 = B::N3, SZ = B::SZ, LPS = C::LPS;
+  const RefTab &R = c_ref[N - 2];
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = lane / LPS, t0 = lane % LPS;
+  const int cell = (blockIdx.x * C::WARPS + warp) * C::CPW + slot;
+  const bool valid = slot < C::CPW && cell < ncell;
+  double *base = smem + (warp * C::CPW + (slot < C::CPW ? slot : 0)) * C::SLOT;
+  double *U = base, *Q = base + SZ, *Rb = base + 2 * SZ, *NB = base + 3 * SZ;
+  double *FA = base + 4 * SZ, *FB = FA + NN;
+  double *T = Q;
+
+  UDesc dsc;
+  if (valid) dsc = desc[cell];
+  else dsc.blk = -1;
+  if (valid) {
+    const double *ub = u + (size_t)dsc.blk * N3;
+    for (int l = t0; l < N3; l += LPS) U[B::pad(l)] = __ldg(ub + l);
+  }
+  __syncwarp();
+  const double h = kp.h;
+  if (kp.mask & TERM_CELL) {
+    // E: GLL -> Gauss values (S in x, y, z)
+    if (valid)
+      for (int t = t0; t < NN; t += LPS) {
+        int b0, st;
+        B::line(0, t, b0, st);
+        sweep_line<N, 0>(U, Q, b0, st, R.S, 1.0);
+      }
+    __syncwarp();
+#pragma unroll
+    for (int d = 1; d < 3; ++d) {
+      if (valid)
+        for (int t = t0; t < NN; t += LPS) {
+          int b0, st;
+          B::line(d, t, b0, st);
+          sweep_line<N, 0>(Q, Q, b0, st, R.S, 1.0);
+        }
+      __syncwarp();
+    }
+    // B: per direction collocation derivative, quadrature weight h*w*w*w and
+    // transposed derivative folded into K_c = D^T W D (Cartesian metric)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (valid)
+        for (int t = t0; t < NN; t += LPS) {
+          int b0, st;
+          B::line(d, t, b0, st);
+          const double s = h * R.gw[t % N] * R.gw[t / N];
+          if (d == 0) sweep_line<N, 2>(Q, Rb, b0, st, R.Kc, s);
+          else sweep_line<N, 1>(Q, Rb, b0, st, R.Kc, s);
+        }
+      __syncwarp();
+    }
+    // I: Gauss -> GLL (S^T in x, y, z)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (valid)
+        for (int t = t0; t < NN; t += LPS) {
+          int b0, st;
+          B::line(d, t, b0, st);
+          sweep_line<N, 0>(Rb, Rb, b0, st, R.St, 1.0);
+        }
+      __syncwarp();
+    }
+  } else {
+    if (valid)
+      for (int l = t0; l < SZ; l += LPS) Rb[l] = 0.0;
+    __syncwarp();
+  }
+
+  // ---- faces (element-centric, own side only)
+  const double h2 = h * h;
+  for (int f = 0; f < 6; ++f) {
+    const int nbk = valid ? dsc.nb[f] : -1;
+    const bool gp = nbk >= 0 && ((dsc.flags >> f) & 1u) && (kp.mask & TERM_GP);
+    const bool sipg = nbk >= 0 && (kp.mask & TERM_SIPG);
+    const bool doit = gp || sipg;
+    if (doit) {
+      const double *nbp = u + (size_t)nbk * N3;
+      for (int l = t0; l < N3; l += LPS) NB[B::pad(l)] = __ldg(nbp + l);
+    }
+    __syncwarp();
+    const int dd = f >> 1, side = f & 1;
+    const int fo = side ? N - 1 : 0, fn = side ? 0 : N - 1;
+    const double sg = side ? 1.0 : -1.0;
+    const double *dow = side ? R.d1 : R.d0;
+    const double *dnb = side ? R.d0 : R.d1;
+    const double *Goo = ft.Goo[side ? 0 : 1];
+    const double *Gon = ft.Gon[side ? 0 : 1];
+    if (doit)
+      for (int t = t0; t < NN; t += LPS) {
+        int b0, st;
+        B::line(dd, t, b0, st);
+        double uo[N], un[N];
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          uo[m] = U[b0 + m * st];
+          un[m] = NB[b0 + m * st];
+        }
+        const double J0 = uo[fo] - un[fn];
+        double A = 0.0;
+#pragma unroll
+        for (int m = 0; m < N; ++m) A = fma(dow[m], uo[m], fma(dnb[m], un[m], A));
+        const double F1 = sipg ? h2 * (kp.sigma * J0 - sg * A / (2.0 * h)) : 0.0;
+        const double F2 = sipg ? -0.5 * h * sg * J0 : 0.0;
+        if (gp) {
+#pragma unroll
+          for (int m = 0; m < N; ++m) {
+            double F = 0.0;
+#pragma unroll
+            for (int a = 0; a < N; ++a) F = fma(Goo[m * N + a], uo[a], fma(-Gon[m * N + a], un[a], F));
+            F = fma(dow[m], F2, F);
+            if (m == fo) F += F1;
+            T[b0 + m * st] = F;
+          }
+        } else {
+          FA[t] = F1;
+          FB[t] = F2;
+        }
+      }
+    __syncwarp();
+    // in-face mass M (x) M (reference; h^2 already folded into F)
+    const int e1 = (dd == 0) ? 1 : 0, e2 = (dd == 2) ? 1 : 2;
+    if (gp) {
+      for (int t = t0; t < NN; t += LPS) {
+        int b0, st;
+        B::line(e1, t, b0, st);
+        sweep_line<N, 0>(T, T, b0, st, R.M, 1.0);
+      }
+    } else if (doit) {
+      for (int k = t0; k < 2 * N; k += LPS) {
+        double *F = (k < N) ? FA : FB;
+        sweep_line<N, 0>(F, F, (k % N) * N, 1, R.M, 1.0);
+      }
+    }
+    __syncwarp();
+    if (gp) {
+      for (int t = t0; t < NN; t += LPS) {
+        int b0, st;
+        B::line(e2, t, b0, st);
+        sweep_line<N, 0>(T, T, b0, st, R.M, 1.0);
+      }
+    } else if (doit) {
+      for (int k = t0; k < 2 * N; k += LPS) {
+        double *F = (k < N) ? FA : FB;
+        sweep_line<N, 0>(F, F, k % N, N, R.M, 1.0);
+      }
+    }
+    __syncwarp();
+    if (doit)
+      for (int t = t0; t < NN; t += LPS) {
+        int b0, st;
+        B::line(dd, t, b0, st);
+        if (gp) {
+#pragma unroll
+          for (int m = 0; m < N; ++m) Rb[b0 + m * st] += T[b0 + m * st];
+        } else {
+          const double fa = FA[t], fb = FB[t];
+#pragma unroll
+          for (int m = 0; m < N; ++m) Rb[b0 + m * st] = fma(dow[m], fb, Rb[b0 + m * st]);
+          Rb[b0 + fo * st] += fa;
+        }
+      }
+    __syncwarp();
+  }
+  if (valid) {
+    double *vb = v + (size_t)dsc.blk * N3;
+    for (int l = t0; l < N3; l += LPS) vb[l] = Rb[B::pad(l)];
+  }
+}
+
+// ============================================================== cut cells
+template <int N>
+struct CutCfg {
+  static constexpr int THREADS = 128;
+  static constexpr int NN = N * N, N3 = N * N * N;
+  static constexpr int ROW0 = 2 * NN + 2 * N;
+  static constexpr int ROW = (ROW0 % 2 == 0) ? ROW0 + 1 : ROW0;  // odd stride: no bank conflicts
+  static constexpr int CHUNK = N <= 4 ? 128 : (N <= 6 ? 64 : 32);
+  static constexpr int FROW = 2 * N + 3;  // cut-face point row: l(s), l(t), c1, c2 (+pad)
+  static constexpr int KPT = (N3 + THREADS - 1) / THREADS;
+  // U, NB, T, R (padded blocks) + JA, JB, FC1, FC2 (NN each) + point rows
+  static constexpr int SMEM_D = 4 * Blk<N>::SZ + 4 * NN + CHUNK * ROW;
+  static constexpr int SMEM = SMEM_D * 8;
+};
+
+// E-phase for one point: returns (value, reference gradient)
+template <int N>
+__device__ __forceinline__ void eval_point(const double *U, const double (&vx)[N], const double (&dvx)[N],
+                                           const double (&vy)[N], const double (&dvy)[N],
+                                           const double (&vz)[N], const double (&dvz)[N], double &u0,
+                                           double &ux, double &uy, double &uz) {
+  constexpr int P = N + 1;
+  u0 = ux = uy = uz = 0.0;
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    double t00 = 0.0, t10 = 0.0, t01 = 0.0;
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double s0 = 0.0, s1 = 0.0;
+      const double *row = U + (c * N + b) * P;
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        const double uu = row[a];
+        s0 = fma(vx[a], uu, s0);
+        s1 = fma(dvx[a], uu, s1);
+      }
+      t00 = fma(vy[b], s0, t00);
+      t10 = fma(dvy[b], s0, t10);
+      t01 = fma(vy[b], s1, t01);
+    }
+    u0 = fma(vz[c], t00, u0);
+    uz = fma(dvz[c], t00, uz);
+    uy = fma(vz[c], t10, uy);
+    ux = fma(vz[c], t01, ux);
+  }
+}
+
+template <int N, bool SURF>
+__device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int64_t pb, int64_t pe,
+                                             const double *U, double *PS, double (&acc)[CutCfg<N>::KPT],
+                                             const KParams &kp, const RefTab &R) {
+  using C = CutCfg<N>;
+  constexpr int NN = C::NN, N3 = C::N3, ROW = C::ROW;
+  const int tid = threadIdx.x;
+  const double h = kp.h, ih = 1.0 / h, ih2 = ih * ih;
+  for (int64_t c0 = pb; c0 < pe; c0 += C::CHUNK) {
+    if (tid < C::CHUNK) {
+      const int64_t q = c0 + tid;
+      double xi = 0.5, eta = 0.5, zeta = 0.5, W = 0.0, nx = 0.0, ny = 0.0, nz = 0.0;
+      if (q < pe) {
+        if (SURF) {
+          const double *p = pts + 7 * q;
+          xi = __ldg(p);
+          eta = __ldg(p + 1);
+          zeta = __ldg(p + 2);
+          nx = __ldg(p + 3);
+          ny = __ldg(p + 4);
+          nz = __ldg(p + 5);
+          W = __ldg(p + 6);
+        } else {
+          const double2 a = __ldg(reinterpret_cast<const double2 *>(pts + 4 * q));
+          const double2 b = __ldg(reinterpret_cast<const double2 *>(pts + 4 * q) + 1);
+          xi = a.x;
+          eta = a.y;
+          zeta = b.x;
+          W = b.y;
+        }
+      }
+      double vx[N], dvx[N], vy[N], dvy[N], vz[N], dvz[N];
+      basis_vd<N>(R, xi, vx, dvx);
+      basis_vd<N>(R, eta, vy, dvy);
+      basis_vd<N>(R, zeta, vz, dvz);
+      double u0, ux, uy, uz;
+      eval_point<N>(U, vx, dvx, vy, dvy, vz, dvz, u0, ux, uy, uz);
+      // B: quadrature-point operation
+      double c0v, c1, c2, c3;
+      if (SURF) {
+        const double un = (nx * ux + ny * uy + nz * uz) * ih;  // physical normal derivative
+        c0v = W * (kp.tau * u0 - un);
+        const double g = -W * u0 * ih;
+        c1 = g * nx;
+        c2 = g * ny;
+        c3 = g * nz;
+      } else {
+        c0v = 0.0;
+        const double s = W * ih2;
+        c1 = s * ux;
+        c2 = s * uy;
+        c3 = s * uz;
+      }
+      // I (z and y stages per point); the x stage is the reduction below
+      double T0[N], T1[N], T2[N];
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        T0[c] = fma(c0v, vz[c], c3 * dvz[c]);
+        T1[c] = c2 * vz[c];
+        T2[c] = c1 * vz[c];
+      }
+      double *row = PS + tid * ROW;
+#pragma unroll
+      for (int c = 0; c < N; ++c)
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+          row[b + N * c] = fma(vy[b], T0[c], dvy[b] * T1[c]);
+          row[NN + b + N * c] = vy[b] * T2[c];
+        }
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        row[2 * NN + a] = vx[a];
+        row[2 * NN + N + a] = dvx[a];
+      }
+    }
+    __syncthreads();
+    const int cnt = (int)((pe - c0) < C::CHUNK ? (pe - c0) : C::CHUNK);
+#pragma unroll
+    for (int k = 0; k < C::KPT; ++k) {
+      const int l = tid + k * C::THREADS;
+      if (l < N3) {
+        const int a = l % N, bc = l / N;
+        double s = acc[k];
+        for (int qq = 0; qq < cnt; ++qq) {
+          const double *row = PS + qq * ROW;
+          s = fma(row[2 * NN + a], row[bc], s);
+          s = fma(row[2 * NN + N + a], row[NN + bc], s);
+        }
+        acc[k] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, double *__restrict__ v,
+                                             const CDesc *__restrict__ desc, int ncut,
+                                             const double *__restrict__ vol_pts,
+                                             const int64_t *__restrict__ vol_ptr,
+                                             const double *__restrict__ srf_pts,
+                                             const int64_t *__restrict__ srf_ptr,
+                                             const double *__restrict__ sf_pts,
+                                             const int64_t *__restrict__ sf_ptr, KParams kp, FaceTab ft) {
+  using B = Blk<N>;
+  using C = CutCfg<N>;
+  constexpr int NN = B::NN, N3 = B::N3, SZ = B::SZ, TH = C::THREADS;
+  const RefTab &R = c_ref[N - 2];
+  extern __shared__ double smem[];
+  double *U = smem, *NB = smem + SZ, *T = smem + 2 * SZ, *Rb = smem + 3 * SZ;
+  double *JA = smem + 4 * SZ, *JB = JA + NN, *FC1 = JB + NN, *FC2 = FC1 + NN;
+  double *PS = FC2 + NN;
+  const int tid = threadIdx.x;
+  const CDesc dsc = desc[blockIdx.x];
+  {
+    const double *ub = u + (size_t)dsc.blk * N3;
+    for (int l = tid; l < N3; l += TH) U[B::pad(l)] = __ldg(ub + l);
+  }
+  __syncthreads();
+  double acc[C::KPT];
+#pragma unroll
+  for (int k = 0; k < C::KPT; ++k) acc[k] = 0.0;
+  if (kp.mask & TERM_CELL)
+    point_chunks<N, false>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], U, PS, acc, kp, R);
+  if (kp.mask & TERM_NITSCHE)
+    point_chunks<N, true>(srf_pts, srf_ptr[dsc.cut], srf_ptr[dsc.cut + 1], U, PS, acc, kp, R);
+#pragma unroll
+  for (int k = 0; k < C::KPT; ++k) {
+    const int l = tid + k * TH;
+    if (l < N3) Rb[B::pad(l)] = acc[k];
+  }
+  __syncthreads();
+
+  const double h = kp.h, h2 = h * h;
+  for (int f = 0; f < 6; ++f) {
+    const int nbk = dsc.nb[f];
+    if (nbk < 0) continue;
+    const bool gp = ((dsc.flags >> f) & 1u) && (kp.mask & TERM_GP);
+    const bool ss = ((dsc.flags >> (6 + f)) & 1u) && (kp.mask & TERM_SIPG);
+    const bool sc = ((dsc.flags >> (12 + f)) & 1u) && (kp.mask & TERM_SIPG);
+    if (!(gp || ss || sc)) continue;
+    {
+      const double *nbp = u + (size_t)nbk * N3;
+      for (int l = tid; l < N3; l += TH) NB[B::pad(l)] = __ldg(nbp + l);
+    }
+    __syncthreads();
+    const int dd = f >> 1, side = f & 1;
+    const int fo = side ? N - 1 : 0, fn = side ? 0 : N - 1;
+    const double sg = side ? 1.0 : -1.0;
+    const double *dow = side ? R.d1 : R.d0;
+    const double *dnb = side ? R.d0 : R.d1;
+    const double *Goo = ft.Goo[side ? 0 : 1];
+    const double *Gon = ft.Gon[side ? 0 : 1];
+    const bool structured = gp || ss;
+    for (int t = tid; t < NN; t += TH) {
+      int b0, st;
+      B::line(dd, t, b0, st);
+      double uo[N], un[N];
+#pragma unroll
+      for (int m = 0; m < N; ++m) {
+        uo[m] = U[b0 + m * st];
+        un[m] = NB[b0 + m * st];
+      }
+      const double J0 = uo[fo] - un[fn];
+      double A = 0.0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) A = fma(dow[m], uo[m], fma(dnb[m], un[m], A));
+      JA[t] = J0;
+      JB[t] = A;
+      FC1[t] = 0.0;
+      FC2[t] = 0.0;
+      if (structured) {
+        const double F1 = ss ? h2 * (kp.sigma * J0 - sg * A / (2.0 * h)) : 0.0;
+        const double F2 = ss ? -0.5 * h * sg * J0 : 0.0;
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          double F = 0.0;
+          if (gp) {
+#pragma unroll
+            for (int a = 0; a < N; ++a) F = fma(Goo[m * N + a], uo[a], fma(-Gon[m * N + a], un[a], F));
+          }
+          F = fma(dow[m], F2, F);
+          if (m == fo) F += F1;
+          T[b0 + m * st] = F;
+        }
+      }
+    }
+    __syncthreads();
+    if (structured) {
+      const int e1 = (dd == 0) ? 1 : 0, e2 = (dd == 2) ? 1 : 2;
+      for (int t = tid; t < NN; t += TH) {
+        int b0, st;
+        B::line(e1, t, b0, st);
+        sweep_line<N, 0>(T, T, b0, st, R.M, 1.0);
+      }
+      __syncthreads();
+      for (int t = tid; t < NN; t += TH) {
+        int b0, st;
+        B::line(e2, t, b0, st);
+        sweep_line<N, 0>(T, T, b0, st, R.M, 1.0);
+      }
+      __syncthreads();
+    }
+    if (sc) {
+      // unstructured in-face quadrature (eq:unstructured_face P:491-496)
+      const int64_t pb = sf_ptr[dsc.sf[f]], pe = sf_ptr[dsc.sf[f] + 1];
+      constexpr int FR = C::FROW;
+      constexpr int FCH = (C::CHUNK * C::ROW) / FR < TH ? (C::CHUNK * C::ROW) / FR : TH;
+      double f1 = 0.0, f2 = 0.0;
+      for (int64_t c0 = pb; c0 < pe; c0 += FCH) {
+        if (tid < FCH) {
+          const int64_t q = c0 + tid;
+          double s = 0.5, tt = 0.5, W = 0.0;
+          if (q < pe) {
+            s = __ldg(sf_pts + 3 * q);
+            tt = __ldg(sf_pts + 3 * q + 1);
+            W = __ldg(sf_pts + 3 * q + 2);
+          }
+          double ls[N], lt[N];
+          basis_v<N>(R, s, ls);
+          basis_v<N>(R, tt, lt);
+          double J0 = 0.0, A = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+              r0 = fma(ls[i], JA[i + N * j], r0);
+              r1 = fma(ls[i], JB[i + N * j], r1);
+            }
+            J0 = fma(lt[j], r0, J0);
+            A = fma(lt[j], r1, A);
+          }
+          double *row = PS + tid * FR;
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            row[i] = ls[i];
+            row[N + i] = lt[i];
+          }
+          row[2 * N] = W * (kp.sigma * J0 - sg * A / (2.0 * h));
+          row[2 * N + 1] = -W * sg * J0 / (2.0 * h);
+        }
+        __syncthreads();
+        const int cnt = (int)((pe - c0) < FCH ? (pe - c0) : FCH);
+        if (tid < NN) {
+          const int i = tid % N, j = tid / N;
+          for (int qq = 0; qq < cnt; ++qq) {
+            const double *row = PS + qq * FR;
+            const double psi = row[i] * row[N + j];
+            f1 = fma(psi, row[2 * N], f1);
+            f2 = fma(psi, row[2 * N + 1], f2);
+          }
+        }
+        __syncthreads();
+      }
+      if (tid < NN) {
+        FC1[tid] = f1;
+        FC2[tid] = f2;
+      }
+      __syncthreads();
+    }
+    for (int t = tid; t < NN; t += TH) {
+      int b0, st;
+      B::line(dd, t, b0, st);
+      if (structured) {
+#pragma unroll
+        for (int m = 0; m < N; ++m) Rb[b0 + m * st] += T[b0 + m * st];
+      }
+      if (sc) {
+        const double fa = FC1[t], fb = FC2[t];
+#pragma unroll
+        for (int m = 0; m < N; ++m) Rb[b0 + m * st] = fma(dow[m], fb, Rb[b0 + m * st]);
+        Rb[b0 + fo * st] += fa;
+      }
+    }
+    __syncthreads();
+  }
+  double *vb = v + (size_t)dsc.blk * N3;
+  for (int l = tid; l < N3; l += TH) vb[l] = Rb[B::pad(l)];
+}
