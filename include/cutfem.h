@@ -109,6 +109,13 @@ int cutfem_setup(const cutfem_problem *pb, int device, cutfem_handle **out);
  * no host synchronisation.  One apply in flight per handle. */
 int cutfem_apply(cutfem_handle *hd, const double *u_dev, double *v_dev, void *cuda_stream);
 
+/* Launch only one of the two kernels of cutfem_apply on `cuda_stream`:
+ * which = 0 the structured kernel (uncut cells and their faces), which = 1 the
+ * unstructured kernel (cut cells, interface, cut faces).  Only the v blocks
+ * owned by that kernel are written.  For per-kernel timing / roofline
+ * attribution; cutfem_apply = both, concurrently. */
+int cutfem_apply_kernel(cutfem_handle *hd, int which, const double *u_dev, double *v_dev, void *cuda_stream);
+
 /* Same operator with HOST buffers: copies u host->device, applies, copies
  * v device->host, synchronises the stream (the end-to-end path). */
 int cutfem_apply_host(cutfem_handle *hd, const double *u_host, double *v_host, void *cuda_stream);

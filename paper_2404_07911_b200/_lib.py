@@ -66,7 +66,7 @@ class Stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
-EXPORTS = ["cutfem_setup", "cutfem_apply", "cutfem_apply_host", "cutfem_csr_assemble",
+EXPORTS = ["cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_host", "cutfem_csr_assemble",
            "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_nnz", "cutfem_csr_download",
            "cutfem_stats", "cutfem_last_error", "cutfem_destroy"]
 
@@ -86,6 +86,7 @@ def load(path: str | None = None):
     L.cutfem_setup.argtypes = [ctypes.POINTER(_Problem), i32, ctypes.POINTER(vp)]
     L.cutfem_apply.argtypes = [vp, vp, vp, vp]
     L.cutfem_apply_host.argtypes = [vp, vp, vp, vp]
+    L.cutfem_apply_kernel.argtypes = [vp, ctypes.c_int, vp, vp, vp]
     L.cutfem_csr_assemble.argtypes = [vp, ctypes.POINTER(i64)]
     L.cutfem_csr_setup.argtypes = [vp, i64, vp, vp, vp]
     L.cutfem_csr_apply.argtypes = [vp, vp, vp, vp]
@@ -95,7 +96,7 @@ def load(path: str | None = None):
     L.cutfem_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     L.cutfem_last_error.restype = ctypes.c_char_p
     L.cutfem_destroy.argtypes = [vp]
-    for name in ("cutfem_setup", "cutfem_apply", "cutfem_apply_host", "cutfem_csr_assemble",
+    for name in ("cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_host", "cutfem_csr_assemble",
                  "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_download", "cutfem_stats",
                  "cutfem_destroy"):
         getattr(L, name).restype = i32
@@ -180,6 +181,12 @@ class CutFEM:
         assert u.numel() == self.n_dofs and v.numel() == self.n_dofs
         assert u.is_contiguous() and v.is_contiguous()
         _check(self._L.cutfem_apply(self._h, u.data_ptr(), v.data_ptr(), _stream_ptr(stream)))
+        return v
+
+    def apply_kernel(self, which: int, u, v, stream=None):
+        """Launch only the structured (0) or unstructured (1) kernel (timing attribution)."""
+        _check(self._L.cutfem_apply_kernel(self._h, int(which), u.data_ptr(), v.data_ptr(),
+                                           _stream_ptr(stream)))
         return v
 
     def apply_host(self, u: np.ndarray, v: np.ndarray | None = None, stream=0) -> np.ndarray:

@@ -138,13 +138,19 @@ void build_facetab(int p, double h, const double *gpg, FaceTab &ft) {
   }
 }
 
+// which: bit0 structured (uncut) kernel, bit1 unstructured (cut) kernel.  With
+// both, the cut kernel runs on the forked side stream, concurrently.
 template <int N>
-int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st) {
-  const int64_t nu = hd->n_uncut, nc = hd->n_cut;
+int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which = 3) {
+  const int64_t nu = (which & 1) ? hd->n_uncut : 0, nc = (which & 2) ? hd->n_cut : 0;
+  const bool fork = nc > 0 && nu > 0;
+  cudaStream_t cs = fork ? hd->side : st;
   if (nc > 0) {
-    CU(cudaEventRecord(hd->ev_fork, st));
-    CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
-    k_cut<N><<<(unsigned)nc, CutCfg<N>::THREADS, CutCfg<N>::SMEM, hd->side>>>(
+    if (fork) {
+      CU(cudaEventRecord(hd->ev_fork, st));
+      CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
+    }
+    k_cut<N><<<(unsigned)nc, CutCfg<N>::THREADS, CutCfg<N>::SMEM, cs>>>(
         u, v, hd->d_cdesc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp,
         hd->d_sfptr, hd->kp, hd->ft);
     CU(cudaGetLastError());
@@ -156,7 +162,7 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st) {
     k_uncut<N><<<grid, 32 * C::WARPS, C::SMEM, st>>>(u, v, hd->d_udesc, (int)nu, hd->kp, hd->ft);
     CU(cudaGetLastError());
   }
-  if (nc > 0) {
+  if (fork) {
     CU(cudaEventRecord(hd->ev_join, hd->side));
     CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
   }
@@ -170,16 +176,16 @@ int set_attrs() {
   return 0;
 }
 
-int dispatch_apply(cutfem_handle *hd, const double *u, double *v, cudaStream_t st) {
+int dispatch_apply(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which = 3) {
   switch (hd->n) {
-    case 2: return launch<2>(hd, u, v, st);
-    case 3: return launch<3>(hd, u, v, st);
-    case 4: return launch<4>(hd, u, v, st);
-    case 5: return launch<5>(hd, u, v, st);
-    case 6: return launch<6>(hd, u, v, st);
-    case 7: return launch<7>(hd, u, v, st);
-    case 8: return launch<8>(hd, u, v, st);
-    case 9: return launch<9>(hd, u, v, st);
+    case 2: return launch<2>(hd, u, v, st, which);
+    case 3: return launch<3>(hd, u, v, st, which);
+    case 4: return launch<4>(hd, u, v, st, which);
+    case 5: return launch<5>(hd, u, v, st, which);
+    case 6: return launch<6>(hd, u, v, st, which);
+    case 7: return launch<7>(hd, u, v, st, which);
+    case 8: return launch<8>(hd, u, v, st, which);
+    case 9: return launch<9>(hd, u, v, st, which);
   }
   return fail(CUTFEM_EUNSUPPORTED, "degree");
 }
@@ -449,6 +455,14 @@ int cutfem_apply(cutfem_handle *hd, const double *u_dev, double *v_dev, void *cu
   if (((uintptr_t)u_dev | (uintptr_t)v_dev) & 7) return fail(CUTFEM_EINVAL, "vectors must be 8-byte aligned");
   CU(cudaSetDevice(hd->device));
   return dispatch_apply(hd, u_dev, v_dev, (cudaStream_t)cuda_stream);
+}
+
+int cutfem_apply_kernel(cutfem_handle *hd, int which, const double *u_dev, double *v_dev, void *cuda_stream) {
+  if (!hd) return fail(CUTFEM_EINVAL, "null handle");
+  if (which != 0 && which != 1) return fail(CUTFEM_EINVAL, "which must be 0 (structured) or 1 (unstructured)");
+  if (u_dev == v_dev && hd->n_active > 0) return fail(CUTFEM_EINVAL, "u and v must not alias");
+  CU(cudaSetDevice(hd->device));
+  return dispatch_apply(hd, u_dev, v_dev, (cudaStream_t)cuda_stream, which == 0 ? 1 : 2);
 }
 
 int cutfem_apply_host(cutfem_handle *hd, const double *u_host, double *v_host, void *cuda_stream) {
