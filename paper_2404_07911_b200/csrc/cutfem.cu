@@ -150,16 +150,32 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
       CU(cudaEventRecord(hd->ev_fork, st));
       CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
     }
-    k_cut<N><<<(unsigned)nc, CutCfg<N>::THREADS, CutCfg<N>::SMEM, cs>>>(
-        u, v, hd->d_cdesc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp,
-        hd->d_sfptr, hd->kp, hd->ft);
+    if (N <= 4) {
+      using CW = CutWCfg<(N <= 4 ? N : 4)>;
+      const unsigned grid = (unsigned)((nc + CW::WARPS - 1) / CW::WARPS);
+      k_cutw<(N <= 4 ? N : 4)><<<grid, 32 * CW::WARPS, CW::SMEM, cs>>>(
+          u, v, hd->d_cdesc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp,
+          hd->d_sfptr, hd->kp, hd->ft);
+    } else {
+      k_cut<N><<<(unsigned)nc, CutCfg<N>::THREADS, CutCfg<N>::SMEM, cs>>>(
+          u, v, hd->d_cdesc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp,
+          hd->d_sfptr, hd->kp, hd->ft);
+    }
     CU(cudaGetLastError());
   }
   if (nu > 0) {
-    using C = UncutCfg<N>;
-    const int per_block = C::WARPS * C::CPW;
-    const unsigned grid = (unsigned)((nu + per_block - 1) / per_block);
-    k_uncut<N><<<grid, 32 * C::WARPS, C::SMEM, st>>>(u, v, hd->d_udesc, (int)nu, hd->kp, hd->ft);
+    if (N <= 5) {
+      using C = Uncut2Cfg<(N <= 5 ? N : 5)>;
+      const int per_block = C::WARPS * C::CPW;
+      const unsigned grid = (unsigned)((nu + per_block - 1) / per_block);
+      k_uncut2<(N <= 5 ? N : 5)><<<grid, 32 * C::WARPS, C::SMEM, st>>>(u, v, hd->d_udesc, (int)nu, hd->kp,
+                                                                       hd->ft);
+    } else {
+      using C = UncutCfg<N>;
+      const int per_block = C::WARPS * C::CPW;
+      const unsigned grid = (unsigned)((nu + per_block - 1) / per_block);
+      k_uncut<N><<<grid, 32 * C::WARPS, C::SMEM, st>>>(u, v, hd->d_udesc, (int)nu, hd->kp, hd->ft);
+    }
     CU(cudaGetLastError());
   }
   if (fork) {
@@ -172,7 +188,13 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
 template <int N>
 int set_attrs() {
   CU(cudaFuncSetAttribute(k_cut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutCfg<N>::SMEM));
+  if (N <= 4)
+    CU(cudaFuncSetAttribute(k_cutw<(N <= 4 ? N : 4)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            CutWCfg<(N <= 4 ? N : 4)>::SMEM));
   CU(cudaFuncSetAttribute(k_uncut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncutCfg<N>::SMEM));
+  if (N <= 5)
+    CU(cudaFuncSetAttribute(k_uncut2<(N <= 5 ? N : 5)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            Uncut2Cfg<(N <= 5 ? N : 5)>::SMEM));
   return 0;
 }
 
@@ -353,6 +375,10 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
       std::memset(&c, 0, sizeof(c));
       c.blk = (int32_t)b;
       c.cut = (int32_t)cut_ord[b];
+      c.vb = pb->vol_ptr[c.cut];
+      c.sb = pb->srf_ptr[c.cut];
+      c.nv = (int32_t)(pb->vol_ptr[c.cut + 1] - pb->vol_ptr[c.cut]);
+      c.ns = (int32_t)(pb->srf_ptr[c.cut + 1] - pb->srf_ptr[c.cut]);
       int64_t cost = (pb->vol_ptr[c.cut + 1] - pb->vol_ptr[c.cut]) + (pb->srf_ptr[c.cut + 1] - pb->srf_ptr[c.cut]);
       for (int f = 0; f < 6; ++f) {
         c.nb[f] = nb[f];

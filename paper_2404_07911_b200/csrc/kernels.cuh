@@ -75,6 +75,8 @@ struct __align__(16) CDesc {
   int32_t sf[6];   // face-point list index for cut faces, else -1
   int32_t cut;     // ordinal in vol_ptr / srf_ptr
   int32_t pad;
+  int64_t vb, sb;  // first volume / interface point
+  int32_t nv, ns;  // volume / interface point counts
 };
 
 #define TERM_CELL 1u
@@ -110,27 +112,42 @@ __device__ __forceinline__ void eo_mv(const EO &m, const double (&in)[N], double
   }
 }
 
-// Padded cell block in shared memory: index (c*N + b)*P + a, P = N+1, so that
-// the lines of all three directions are bank-conflict free.
+// Padded cell block in shared memory: index c*PS + b*P + a.  (P, PS) per N
+// minimise 64-bit bank conflicts of the 1-D lines in all three directions
+// (searched offline: worst case 2-way for N >= 4, conflict-free for N <= 3).
+template <int N>
+struct BlkPad {
+  static constexpr int P = (N == 2 || N == 3 || N == 5 || N == 7) ? N : N + 1;
+  static constexpr int PS = N == 2 ? 4 : (N == 3 ? 12 : (N == 5 ? 25 : (N == 7 ? 52 : N * (N + 1))));
+};
 template <int N>
 struct Blk {
-  static constexpr int P = N + 1;
+  static constexpr int P = BlkPad<N>::P;
+  static constexpr int PS = BlkPad<N>::PS;
   static constexpr int NN = N * N;
   static constexpr int N3 = N * N * N;
-  static constexpr int SZ = N * N * P;
-  __device__ static __forceinline__ int pad(int l) { return (l / N) * P + (l % N); }
+  static constexpr int SZ = N * PS;
+  __device__ static __forceinline__ int pad(int l) { return (l / NN) * PS + ((l / N) % N) * P + (l % N); }
+  __device__ static __forceinline__ int at(int a, int b, int c) { return c * PS + b * P + a; }
+  template <int D>
+  __host__ __device__ static constexpr int lstride() { return D == 0 ? 1 : (D == 1 ? P : PS); }
+  template <int D>
+  __device__ static __forceinline__ int lbase(int t) {
+    const int t0 = t % N, t1 = t / N;
+    return D == 0 ? t1 * PS + t0 * P : (D == 1 ? t1 * PS + t0 : t1 * P + t0);
+  }
   // line t (t = t0 + N*t1, t0 along the lower in-face axis) in direction d
   __device__ static __forceinline__ void line(int d, int t, int &base, int &stride) {
     const int t0 = t % N, t1 = t / N;
     if (d == 0) {
-      base = (t1 * N + t0) * P;
+      base = t1 * PS + t0 * P;
       stride = 1;
     } else if (d == 1) {
-      base = t1 * N * P + t0;
+      base = t1 * PS + t0;
       stride = P;
     } else {
       base = t1 * P + t0;
-      stride = N * P;
+      stride = PS;
     }
   }
 };
@@ -405,7 +422,7 @@ __device__ __forceinline__ void eval_point(const double *U, const double (&vx)[N
                                            const double (&vy)[N], const double (&dvy)[N],
                                            const double (&vz)[N], const double (&dvz)[N], double &u0,
                                            double &ux, double &uy, double &uz) {
-  constexpr int P = N + 1;
+  constexpr int P = Blk<N>::P, PS = Blk<N>::PS;
   u0 = ux = uy = uz = 0.0;
 #pragma unroll
   for (int c = 0; c < N; ++c) {
@@ -413,7 +430,7 @@ __device__ __forceinline__ void eval_point(const double *U, const double (&vx)[N
 #pragma unroll
     for (int b = 0; b < N; ++b) {
       double s0 = 0.0, s1 = 0.0;
-      const double *row = U + (c * N + b) * P;
+      const double *row = U + c * PS + b * P;
 #pragma unroll
       for (int a = 0; a < N; ++a) {
         const double uu = row[a];
@@ -711,3 +728,58 @@ __global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, doubl
   double *vb = v + (size_t)dsc.blk * N3;
   for (int l = tid; l < N3; l += TH) vb[l] = Rb[B::pad(l)];
 }
+
+// ======================================================= cut cells, p <= 3
+// One WARP per cut cell; lanes = quadrature points (the paper's vectorisation
+// over points, "combining the operations of several quadrature points of
+// an entity into the SIMD lanes").  Each lane accumulates the integration into
+// all n^3 <= 64 DoFs in registers (so the reduction over points never touches
+// shared memory); one butterfly reduce-scatter over the warp at the end.  Volume
+// and interface points form one stream (no partially filled round per kind).
+// The cell block and its six neighbour blocks are fetched with cp.async at
+// kernel entry, overlapping the point work.
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K)); }
+
+// Warp reduce-scatter of L per-lane partial sums (L a power of two <= 64).
+// Afterwards value j of lane l is the warp sum of entry idx(l, j) =
+// (l >> (5 - S)) * (L >> S) + j with S = min(log2 L, 5).
+template <int L, int O, int LEN>
+__device__ __forceinline__ void bfly_round(double (&a)[L], int lane) {
+  if constexpr (O >= 1) {
+    if constexpr (LEN > 1) {
+      constexpr int h = LEN / 2;
+      const bool up = (lane & O) != 0;
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        const double send = up ? a[i] : a[i + h];
+        const double keep = up ? a[i + h] : a[i];
+        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+      }
+      bfly_round<L, O / 2, h>(a, lane);
+    } else {
+      a[0] += __shfl_xor_sync(0xffffffffu, a[0], O);
+      bfly_round<L, O / 2, 1>(a, lane);
+    }
+  }
+}
+template <int L>
+__device__ __forceinline__ void butterfly(double (&a)[L], int lane) {
+  bfly_round<L, 16, L>(a, lane);
+}
+template <int L>
+struct BF {
+  static constexpr int S = (L >= 32) ? 5 : (L == 16 ? 4 : (L == 8 ? 3 : (L == 4 ? 2 : (L == 2 ? 1 : 0))));
+  static constexpr int LF = L >> S;  // values left per lane
+  __device__ static __forceinline__ int idx(int lane, int j) { return (lane >> (5 - S)) * LF + j; }
+  // lanes holding a duplicate of the same entry (full-reduce rounds) write only once
+  __device__ static __forceinline__ bool writer(int lane) { return (lane & ((1 << (5 - S)) - 1)) == 0; }
+};
+
+#include "kernels_fast.cuh"
