@@ -418,8 +418,17 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
   if ((rc = upload(hd, &hd->d_udesc, ud.data(), ud.size()))) return rc;
   if ((rc = upload(hd, &hd->d_cdesc, cd.data(), cd.size()))) return rc;
   if ((rc = upload(hd, &hd->d_vol, pb->vol_pts, (size_t)(4 * nvol)))) return rc;
-  if ((rc = upload(hd, &hd->d_srf, pb->srf_pts, (size_t)(7 * nsrf)))) return rc;
-  if ((rc = upload(hd, &hd->d_sfp, pb->sf_pts, (size_t)(3 * nfp)))) return rc;
+  {
+    // repack interface points to 64-byte rows and face points to 32-byte rows so
+    // that every point list is a 16-byte aligned contiguous bulk-copy source
+    std::vector<double> s8((size_t)8 * nsrf, 0.0), f4((size_t)4 * nfp, 0.0);
+    for (int64_t q = 0; q < nsrf; ++q)
+      for (int k = 0; k < 7; ++k) s8[8 * q + k] = pb->srf_pts[7 * q + k];
+    for (int64_t q = 0; q < nfp; ++q)
+      for (int k = 0; k < 3; ++k) f4[4 * q + k] = pb->sf_pts[3 * q + k];
+    if ((rc = upload(hd, &hd->d_srf, s8.data(), s8.size()))) return rc;
+    if ((rc = upload(hd, &hd->d_sfp, f4.data(), f4.size()))) return rc;
+  }
   if ((rc = upload(hd, &hd->d_volptr, pb->vol_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_srfptr, pb->srf_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_sfptr, pb->sf_ptr, (size_t)(nsf ? nsf + 1 : 0)))) return rc;
@@ -429,6 +438,11 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
   hd->kp.h = pb->h;
   hd->kp.sigma = pb->sipg_gamma / pb->h;
   hd->kp.tau = pb->nitsche_tau / pb->h;
+  hd->kp.ih = 1.0 / pb->h;
+  hd->kp.ih2 = 1.0 / (pb->h * pb->h);
+  hd->kp.i2h = 0.5 / pb->h;
+  hd->kp.h2sig = pb->h * pb->h * hd->kp.sigma;
+  hd->kp.hh = 0.5 * pb->h;
   hd->kp.mask = hd->mask;
   hd->kp.n_cells = 0;
   CU(cudaStreamCreateWithFlags(&hd->side, cudaStreamNonBlocking));

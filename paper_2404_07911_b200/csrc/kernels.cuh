@@ -17,6 +17,7 @@
 //     reduction + in-face per-point evaluation (eq:unstructured_face P:491-496).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #define CUTFEM_NMAX 9
 
@@ -56,6 +57,11 @@ struct KParams {
   double h;      // cell edge
   double sigma;  // SIPG penalty gamma / h
   double tau;    // Nitsche penalty tau_D / h
+  double ih;     // 1 / h
+  double ih2;    // 1 / h^2
+  double i2h;    // 1 / (2 h)
+  double h2sig;  // h^2 sigma
+  double hh;     // h / 2
   uint32_t mask; // CUTFEM_TERM_* bits
   int32_t n_cells;
 };
@@ -151,6 +157,48 @@ struct Blk {
     }
   }
 };
+
+// Unpadded block (the global layout): destination of bulk (TMA) copies.
+template <int N>
+struct BlkU {
+  static constexpr int P = N, PS = N * N, NN = N * N, N3 = N * N * N, SZ = N3;
+  __device__ static __forceinline__ int at(int a, int b, int c) { return c * PS + b * P + a; }
+  template <int D>
+  __host__ __device__ static constexpr int lstride() { return D == 0 ? 1 : (D == 1 ? P : PS); }
+  template <int D>
+  __device__ static __forceinline__ int lbase(int t) {
+    const int t0 = t % N, t1 = t / N;
+    return D == 0 ? t1 * PS + t0 * P : (D == 1 ? t1 * PS + t0 : t1 * P + t0);
+  }
+};
+
+// ---- mbarrier + cp.async.bulk (TMA bulk copy, SASS UBLKCP) helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// generic-proxy accesses before this fence are ordered before later async-proxy (bulk) writes
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // MODE 0: dst = M src; MODE 1: dst += s * M src; MODE 2: dst = s * M src
 template <int N, int MODE>
@@ -448,6 +496,37 @@ __device__ __forceinline__ void eval_point(const double *U, const double (&vx)[N
   }
 }
 
+// same, with the block in layout L (padded or unpadded)
+template <int N, class L>
+__device__ __forceinline__ void eval_point_l(const double *U, const double (&vx)[N], const double (&dvx)[N],
+                                             const double (&vy)[N], const double (&dvy)[N],
+                                             const double (&vz)[N], const double (&dvz)[N], double &u0,
+                                             double &ux, double &uy, double &uz) {
+  u0 = ux = uy = uz = 0.0;
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    double t00 = 0.0, t10 = 0.0, t01 = 0.0;
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double s0 = 0.0, s1 = 0.0;
+      const double *row = U + c * L::PS + b * L::P;
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        const double uu = row[a];
+        s0 = fma(vx[a], uu, s0);
+        s1 = fma(dvx[a], uu, s1);
+      }
+      t00 = fma(vy[b], s0, t00);
+      t10 = fma(dvy[b], s0, t10);
+      t01 = fma(vy[b], s1, t01);
+    }
+    u0 = fma(vz[c], t00, u0);
+    uz = fma(dvz[c], t00, uz);
+    uy = fma(vz[c], t10, uy);
+    ux = fma(vz[c], t01, ux);
+  }
+}
+
 template <int N, bool SURF>
 __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int64_t pb, int64_t pe,
                                              const double *U, double *PS, double (&acc)[CutCfg<N>::KPT],
@@ -462,7 +541,7 @@ __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int
       double xi = 0.5, eta = 0.5, zeta = 0.5, W = 0.0, nx = 0.0, ny = 0.0, nz = 0.0;
       if (q < pe) {
         if (SURF) {
-          const double *p = pts + 7 * q;
+          const double *p = pts + 8 * q;
           xi = __ldg(p);
           eta = __ldg(p + 1);
           zeta = __ldg(p + 2);
@@ -662,9 +741,9 @@ __global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, doubl
           const int64_t q = c0 + tid;
           double s = 0.5, tt = 0.5, W = 0.0;
           if (q < pe) {
-            s = __ldg(sf_pts + 3 * q);
-            tt = __ldg(sf_pts + 3 * q + 1);
-            W = __ldg(sf_pts + 3 * q + 2);
+            s = __ldg(sf_pts + 4 * q);
+            tt = __ldg(sf_pts + 4 * q + 1);
+            W = __ldg(sf_pts + 4 * q + 2);
           }
           double ls[N], lt[N];
           basis_v<N>(R, s, ls);
