@@ -78,7 +78,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or _SO
+    p = path or os.environ.get("CUTFEM_LIB") or _SO
     if not os.path.exists(p):
         raise RuntimeError(f"libcutfem.so not built ({p}); run __graft_entry__.build()")
     L = ctypes.CDLL(p)

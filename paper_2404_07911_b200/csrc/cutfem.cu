@@ -46,6 +46,9 @@ struct cutfem_handle {
   int n = 2;
   double h = 1;
   int64_t n_active = 0, n_uncut = 0, n_cut = 0;
+  int64_t n_plain = 0;     // uncut cells whose six neighbours are active and uncut (first in d_udesc)
+  int sm_count = 148;
+  int occ_plain = 1, occ_gen = 1;  // resident CTAs per SM of the persistent structured kernels
   uint32_t mask = CUTFEM_TERM_ALL;
   KParams kp;
   FaceTab ft;
@@ -165,11 +168,26 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
   }
   if (nu > 0) {
     if (N <= 5) {
-      using C = Uncut2Cfg<(N <= 5 ? N : 5)>;
+      constexpr int NC = (N <= 5 ? N : 5);
+      using C = Uncut3Cfg<NC>;
       const int per_block = C::WARPS * C::CPW;
-      const unsigned grid = (unsigned)((nu + per_block - 1) / per_block);
-      k_uncut2<(N <= 5 ? N : 5)><<<grid, 32 * C::WARPS, C::SMEM, st>>>(u, v, hd->d_udesc, (int)nu, hd->kp,
-                                                                       hd->ft);
+      const int64_t np = hd->n_plain, ng = nu - np;
+      const bool plain_ok = (hd->kp.mask & TERM_SIPG) != 0;
+      auto grid_for = [&](int64_t n, int occ) {
+        const int64_t need = (n + per_block - 1) / per_block;
+        return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)occ * hd->sm_count));
+      };
+      if (plain_ok) {
+        if (np > 0)
+          k_uncut3<NC, true><<<grid_for(np, hd->occ_plain), 32 * C::WARPS, C::SMEM, st>>>(
+              u, v, hd->d_udesc, (int)np, hd->kp, hd->ft);
+        if (ng > 0)
+          k_uncut3<NC, false><<<grid_for(ng, hd->occ_gen), 32 * C::WARPS, C::SMEM, st>>>(
+              u, v, hd->d_udesc + np, (int)ng, hd->kp, hd->ft);
+      } else {
+        k_uncut3<NC, false><<<grid_for(nu, hd->occ_gen), 32 * C::WARPS, C::SMEM, st>>>(u, v, hd->d_udesc,
+                                                                                          (int)nu, hd->kp, hd->ft);
+      }
     } else {
       using C = UncutCfg<N>;
       const int per_block = C::WARPS * C::CPW;
@@ -186,15 +204,29 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
 }
 
 template <int N>
+int query_occ(cutfem_handle *hd) {
+  if (N <= 5) {
+    constexpr int NC = (N <= 5 ? N : 5);
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_plain, k_uncut3<NC, true>, 128, Uncut3Cfg<NC>::SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_gen, k_uncut3<NC, false>, 128, Uncut3Cfg<NC>::SMEM));
+    hd->occ_plain = std::max(1, hd->occ_plain);
+    hd->occ_gen = std::max(1, hd->occ_gen);
+  }
+  return 0;
+}
+
+template <int N>
 int set_attrs() {
   CU(cudaFuncSetAttribute(k_cut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutCfg<N>::SMEM));
   if (N <= 4)
     CU(cudaFuncSetAttribute(k_cutw<(N <= 4 ? N : 4)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             CutWCfg<(N <= 4 ? N : 4)>::SMEM));
   CU(cudaFuncSetAttribute(k_uncut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncutCfg<N>::SMEM));
-  if (N <= 5)
-    CU(cudaFuncSetAttribute(k_uncut2<(N <= 5 ? N : 5)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            Uncut2Cfg<(N <= 5 ? N : 5)>::SMEM));
+  if (N <= 5) {
+    constexpr int NC = (N <= 5 ? N : 5);
+    CU(cudaFuncSetAttribute(k_uncut3<NC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Uncut3Cfg<NC>::SMEM));
+    CU(cudaFuncSetAttribute(k_uncut3<NC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Uncut3Cfg<NC>::SMEM));
+  }
   return 0;
 }
 
@@ -210,6 +242,16 @@ int dispatch_apply(cutfem_handle *hd, const double *u, double *v, cudaStream_t s
     case 9: return launch<9>(hd, u, v, st, which);
   }
   return fail(CUTFEM_EUNSUPPORTED, "degree");
+}
+
+int dispatch_occ(cutfem_handle *hd) {
+  switch (hd->n) {
+    case 2: return query_occ<2>(hd);
+    case 3: return query_occ<3>(hd);
+    case 4: return query_occ<4>(hd);
+    case 5: return query_occ<5>(hd);
+    default: return 0;
+  }
 }
 
 int dispatch_attrs(int n) {
@@ -405,6 +447,19 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
       if (sfid[b * 6 + 2 * d + 1] < 0) ++n_struct;
     }
   }
+  // uncut: "plain" cells (six active uncut neighbours) first
+  {
+    std::vector<UDesc> plain, gen;
+    for (auto &x : ud) {
+      bool pl = true;
+      for (int f = 0; f < 6; ++f)
+        if (x.nb[f] < 0 || pb->is_cut[x.nb[f]]) pl = false;
+      (pl ? plain : gen).push_back(x);
+    }
+    hd->n_plain = (int64_t)plain.size();
+    ud = plain;
+    ud.insert(ud.end(), gen.begin(), gen.end());
+  }
   // heaviest cut cells first (LPT order for the block scheduler)
   {
     std::vector<int64_t> order(cd.size());
@@ -434,6 +489,12 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
   if ((rc = upload(hd, &hd->d_sfptr, pb->sf_ptr, (size_t)(nsf ? nsf + 1 : 0)))) return rc;
   if ((rc = upload_tables(p))) return rc;
   if ((rc = dispatch_attrs(n))) return rc;
+  {
+    int dev = device, smc = 148;
+    cudaDeviceGetAttribute(&smc, cudaDevAttrMultiProcessorCount, dev);
+    hd->sm_count = smc;
+  }
+  if ((rc = dispatch_occ(hd))) return rc;
   build_facetab(p, pb->h, pb->gp_gamma, hd->ft);
   hd->kp.h = pb->h;
   hd->kp.sigma = pb->sipg_gamma / pb->h;
@@ -463,7 +524,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
   s.n_dofs = na * n * n * n;
   s.degree = p;
   s.device = device;
-  s.launches_per_apply = (nc > 0) + (na - nc > 0);
+  s.launches_per_apply = (nc > 0) + (hd->n_plain > 0) + (na - nc - hd->n_plain > 0);
   return 0;
 }
 

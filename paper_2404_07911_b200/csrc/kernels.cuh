@@ -20,6 +20,9 @@
 #include <type_traits>
 
 #define CUTFEM_NMAX 9
+#ifndef CUTFEM_USE_BULK
+#define CUTFEM_USE_BULK 1
+#endif
 
 // Even-odd factors of a centro-symmetric n x n matrix M (M[i][j] = M[n-1-i][n-1-j]):
 //   E[i][j] = (M[i][j] + M[i][n-1-j]) / 2 (j < H), E[i][H] = M[i][H] (n odd), i < HC

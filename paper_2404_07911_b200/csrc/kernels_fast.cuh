@@ -153,7 +153,7 @@ __device__ __forceinline__ void face_accumulate(double *Rb, const double *NB, in
 // ======================================================= structured cells
 template <int N>
 struct Uncut2Cfg {
-  static constexpr bool BULK = (N % 2) == 0;   // blocks are 16-byte multiples
+  static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;   // blocks are 16-byte multiples
   using LN = typename std::conditional<BULK, BlkU<N>, Blk<N>>::type;  // U / NB layout
   static constexpr int NN = N * N, N3 = N * N * N;
   static constexpr int LPS = NN;               // N <= 5: one lane per line
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(128) k_uncut2(const double *__restrict__ u, do
 // ============================================================ cut cells
 template <int N>
 struct CutWCfg {
-  static constexpr bool BULK = (N % 2) == 0;
+  static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
   using LN = typename std::conditional<BULK, BlkU<N>, Blk<N>>::type;
   static constexpr int WARPS = 4;
   static constexpr int NN = N * N, N3 = N * N * N;
@@ -635,3 +635,4 @@ __global__ void __launch_bounds__(128) k_cutw(const double *__restrict__ u, doub
   double *vbk = v + (size_t)dsc.blk * N3;
   for (int l = lane; l < N3; l += 32) vbk[l] = Rb[B::pad(l)];
 }
+#include "kernels_uncut3.cuh"

@@ -14,6 +14,15 @@ P = cutgen.config(cfg, degree=deg)
 u = torch.from_numpy(P.seeded_u(0)).cuda()
 v = torch.empty_like(u)
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+flush2 = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+MODE = os.environ.get("FLUSH", "write")
+
+
+def do_flush():
+    if MODE in ("write", "writeread"):
+        flush.zero_()
+    if MODE == "writeread":
+        flush2.sum()
 
 
 def t(fn, K=20):
@@ -21,7 +30,7 @@ def t(fn, K=20):
         fn()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     for a, b in ev:
-        flush.zero_()
+        do_flush()
         a.record()
         fn()
         b.record()
@@ -29,7 +38,7 @@ def t(fn, K=20):
     return float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
 
 
-res = {"cfg": cfg, "n_dofs": P.n_dofs}
+res = {"cfg": cfg, "n_dofs": P.n_dofs, "flush": MODE}
 for mask, name in ((15, "all"), (1, "cell"), (2, "sipg"), (4, "nitsche"), (8, "gp"), (0x10 | 0, "none")):
     m = mask if mask != 0x10 else 0x10
     try:
