@@ -89,8 +89,7 @@ __global__ void __launch_bounds__(128) k_uncut3(const double *__restrict__ u, do
     }
   };
   // issue the loads of `cell` into buffer set `st` (lane t == 0 of the slot)
-  auto issue = [&](int cell, int st) {
-    const UDesc d = desc[cell];
+  auto issue = [&](const UDesc &d, int st) {
     *reinterpret_cast<UDesc *>(base + C::OFF_D + 4 * st) = d;
     uint32_t act, gpm;
     masks(d, act, gpm);
@@ -130,8 +129,8 @@ __global__ void __launch_bounds__(128) k_uncut3(const double *__restrict__ u, do
     }
     __syncwarp(mask);
     if (t == 0) {
-      issue(s0, 0);
-      if (s0 + S < ncell) issue(s0 + S, 1);
+      issue(desc[s0], 0);
+      if (s0 + S < ncell) issue(desc[s0 + S], 1);
     }
     __syncwarp(mask);  // the staged descriptors are visible to the slot
   } else {
@@ -149,6 +148,8 @@ __global__ void __launch_bounds__(128) k_uncut3(const double *__restrict__ u, do
     uint32_t act, gpm;
     act = 0x3fu;
     gpm = 0u;
+    UDesc dn;  // descriptor of cell + 2S (lane 0), prefetched a full iteration ahead
+    if (C::BULK && t == 0 && cell + 2 * S < ncell) dn = desc[cell + 2 * S];
     if constexpr (C::BULK) {
       mbar_wait(bar + 2 * st, par);
     } else {
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(128) k_uncut3(const double *__restrict__ u, do
       if constexpr (C::BULK) {
         if (t == 0) {
           fence_proxy_async();
-          issue(cell + 2 * S, st);
+          issue(dn, st);
         }
       } else {
         issue_lanes(cell + 2 * S, st);
