@@ -49,6 +49,7 @@ struct cutfem_handle {
   int64_t n_plain = 0;     // uncut cells whose six neighbours are active and uncut (first in d_udesc)
   int sm_count = 148;
   int occ_plain = 1, occ_gen = 1;  // resident CTAs per SM of the persistent structured kernels
+  int occ_cut = 1;                 // ... and of the persistent unstructured kernel
   uint32_t mask = CUTFEM_TERM_ALL;
   KParams kp;
   FaceTab ft;
@@ -205,6 +206,11 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
 
 template <int N>
 int query_occ(cutfem_handle *hd) {
+  if (N <= 4) {
+    constexpr int NC = (N <= 4 ? N : 4);
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_cut, k_cutw<NC>, 128, CutWCfg<NC>::SMEM));
+    hd->occ_cut = std::max(1, hd->occ_cut);
+  }
   if (N <= 5) {
     constexpr int NC = (N <= 5 ? N : 5);
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_plain, k_uncut3<NC, true>, 128, Uncut3Cfg<NC>::SMEM));
