@@ -95,6 +95,7 @@ typedef struct {
   int64_t dev_bytes;         /* device memory held by the handle                  */
   int32_t launches_per_apply;
   int32_t reserved;
+  int64_t n_ext_dofs;        /* u length incl. ghost blocks (distributed handles) */
 } cutfem_stats_t;
 
 /* Build device tables for `pb` on CUDA device `device`.  Validation failures
@@ -134,6 +135,41 @@ int cutfem_csr_apply(cutfem_handle *hd, const double *u_dev, double *v_dev, void
 /* Copy the device CSR to host arrays sized by cutfem_csr_nnz (for tests). */
 int64_t cutfem_csr_nnz(const cutfem_handle *hd);
 int cutfem_csr_download(const cutfem_handle *hd, int64_t *row_ptr, int32_t *col, double *val);
+
+/* ---------------------------------------------------------------- x-slabs
+ * the mesh is split into contiguous x-slabs of cell planes
+ * (requires x-slowest block order, as cutgen emits); each rank owns the active
+ * cells of its planes [x_begin, x_end) and reads one ghost plane from each
+ * neighbour.  Work balance follows PAPER §3.5 with weight 1 for uncut
+ * and w_cut for cut cells. */
+typedef struct {
+  cutfem_problem pb;       /* local problem: owned blocks (global order), then the
+                              ghost blocks of plane x_begin-1, then of plane x_end */
+  int64_t n_own;           /* owned blocks = global blocks [global_begin, +n_own) */
+  int64_t n_ghost_lo, n_ghost_hi;
+  int64_t global_begin;
+  int64_t plane_lo, plane_hi; /* owned blocks in the first / last owned plane (halo sends) */
+  void *storage;           /* library-owned; release with cutfem_local_free */
+} cutfem_local;
+
+/* Host only (no GPU): split planes 0..n_cells[0] into nparts weighted slabs;
+ * x_split has nparts+1 entries (x_split[0] = 0, x_split[nparts] = n_cells[0]). */
+int cutfem_partition_x(const cutfem_problem *pb, int nparts, double w_cut, int32_t *x_split);
+/* Host only: the local problem of slab [x_begin, x_end) (for tests / inspection). */
+int cutfem_local_build(const cutfem_problem *global_pb, int32_t x_begin, int32_t x_end, cutfem_local *out);
+void cutfem_local_free(cutfem_local *loc);
+/* NCCL unique id (ncclUniqueId, 128 bytes) for cutfem_setup_dist; created on one
+ * rank and broadcast by the caller (torch.distributed). */
+int cutfem_nccl_unique_id(void *out, int64_t size);
+/* Distributed handle for slab [x_begin, x_end) of the GLOBAL problem pb.  Its
+ * cutfem_apply takes u_dev with room for n_own + n_ghost_lo + n_ghost_hi blocks
+ * (owned values first; the ghost tail is filled by the NCCL halo exchange inside
+ * the apply) and writes the n_own owned blocks of v_dev.  nranks == 1 needs no
+ * id.  The exchange runs on an internal stream, overlapped with the slab-interior
+ * cells; the slab-boundary cells run after it. */
+int cutfem_setup_dist(const cutfem_problem *global_pb, int32_t x_begin, int32_t x_end, int rank, int nranks,
+                      const void *nccl_id, int device, cutfem_handle **out);
+int cutfem_dist_info(const cutfem_handle *hd, int64_t *n_own_blocks, int64_t *n_ghost_lo, int64_t *n_ghost_hi);
 
 int cutfem_stats(const cutfem_handle *hd, cutfem_stats_t *out);
 const char *cutfem_last_error(void);

@@ -28,13 +28,24 @@ def _sources():
     return [os.path.join(_SRC_DIR, f) for f in sorted(os.listdir(_SRC_DIR))] + [_HDR]
 
 
+def _nccl_dir() -> str:
+    """NCCL shipped with torch (nvidia-nccl wheel): headers + libnccl.so.2."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is not None and spec.submodule_search_locations:
+        return list(spec.submodule_search_locations)[0]
+    raise RuntimeError("NCCL (nvidia.nccl) not found")
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile libcutfem.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
     stale = force or not os.path.exists(_SO) or any(
         os.path.getmtime(s) > os.path.getmtime(_SO) for s in _sources())
     if stale:
-        cmd = ["nvcc", *NVCC_FLAGS, "-I", os.path.join(_ROOT, "include"), "-o", _SO,
-               os.path.join(_SRC_DIR, "cutfem.cu"), "-lcusparse"]
+        nccl = _nccl_dir()
+        cmd = ["nvcc", *NVCC_FLAGS, "-I", os.path.join(_ROOT, "include"), "-I", os.path.join(nccl, "include"),
+               "-o", _SO, os.path.join(_SRC_DIR, "cutfem.cu"), "-lcusparse", "-L", os.path.join(nccl, "lib"),
+               "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)
@@ -60,7 +71,8 @@ class Stats(ctypes.Structure):
         "n_active", "n_uncut", "n_cut", "n_vol_pts", "n_srf_pts", "n_face_pts", "n_faces_struct",
         "n_faces_cut", "n_faces_empty", "n_faces_gp", "n_dofs")] + [
         ("degree", ctypes.c_int32), ("device", ctypes.c_int32), ("dev_bytes", ctypes.c_int64),
-        ("launches_per_apply", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+        ("launches_per_apply", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("n_ext_dofs", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -68,7 +80,15 @@ class Stats(ctypes.Structure):
 
 EXPORTS = ["cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_host", "cutfem_csr_assemble",
            "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_nnz", "cutfem_csr_download",
-           "cutfem_stats", "cutfem_last_error", "cutfem_destroy"]
+           "cutfem_stats", "cutfem_last_error", "cutfem_destroy", "cutfem_partition_x",
+           "cutfem_local_build", "cutfem_local_free", "cutfem_nccl_unique_id", "cutfem_setup_dist",
+           "cutfem_dist_info"]
+
+
+class _Local(ctypes.Structure):
+    _fields_ = [("pb", _Problem), ("n_own", ctypes.c_int64), ("n_ghost_lo", ctypes.c_int64),
+                ("n_ghost_hi", ctypes.c_int64), ("global_begin", ctypes.c_int64),
+                ("plane_lo", ctypes.c_int64), ("plane_hi", ctypes.c_int64), ("storage", ctypes.c_void_p)]
 
 _lib = None
 
@@ -96,9 +116,19 @@ def load(path: str | None = None):
     L.cutfem_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     L.cutfem_last_error.restype = ctypes.c_char_p
     L.cutfem_destroy.argtypes = [vp]
+    L.cutfem_partition_x.argtypes = [ctypes.POINTER(_Problem), ctypes.c_int, ctypes.c_double, vp]
+    L.cutfem_local_build.argtypes = [ctypes.POINTER(_Problem), ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.POINTER(_Local)]
+    L.cutfem_local_free.argtypes = [ctypes.POINTER(_Local)]
+    L.cutfem_local_free.restype = None
+    L.cutfem_nccl_unique_id.argtypes = [vp, i64]
+    L.cutfem_setup_dist.argtypes = [ctypes.POINTER(_Problem), ctypes.c_int32, ctypes.c_int32, i32, i32, vp, i32,
+                                    ctypes.POINTER(vp)]
+    L.cutfem_dist_info.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     for name in ("cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_host", "cutfem_csr_assemble",
                  "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_download", "cutfem_stats",
-                 "cutfem_destroy"):
+                 "cutfem_destroy", "cutfem_partition_x", "cutfem_local_build", "cutfem_nccl_unique_id",
+                 "cutfem_setup_dist", "cutfem_dist_info"):
         getattr(L, name).restype = i32
     if path is None:
         _lib = L
@@ -123,49 +153,126 @@ def _stream_ptr(stream):
     return stream.cuda_stream
 
 
+def _marshal(prob, term_mask=TERM_ALL):
+    """Problem fields -> _Problem (with the numpy arrays kept alive in `keep`)."""
+    keep = {
+        "ijk": np.ascontiguousarray(prob.active_ijk, dtype=np.int32),
+        "cut": np.ascontiguousarray(prob.is_cut, dtype=np.uint8),
+        "vp": np.ascontiguousarray(prob.vol_ptr, dtype=np.int64),
+        "vx": np.ascontiguousarray(prob.vol_pts, dtype=np.float64),
+        "sp": np.ascontiguousarray(prob.srf_ptr, dtype=np.int64),
+        "sx": np.ascontiguousarray(prob.srf_pts, dtype=np.float64),
+        "fc": np.ascontiguousarray(prob.sf_cells, dtype=np.int32),
+        "fa": np.ascontiguousarray(prob.sf_axis, dtype=np.uint8),
+        "fp": np.ascontiguousarray(prob.sf_ptr, dtype=np.int64),
+        "fx": np.ascontiguousarray(prob.sf_pts, dtype=np.float64),
+        "gp": np.ascontiguousarray(prob.gp_gamma, dtype=np.float64),
+    }
+    pb = _Problem()
+    for i in range(3):
+        pb.n_cells[i] = int(prob.n_cells[i])
+        pb.lower[i] = float(prob.lower[i])
+    pb.h = float(prob.h)
+    pb.degree = int(prob.degree)
+    pb.n_active = keep["ijk"].shape[0]
+    pb.active_ijk, pb.is_cut = _ptr(keep["ijk"]), _ptr(keep["cut"])
+    pb.vol_ptr, pb.vol_pts = _ptr(keep["vp"]), _ptr(keep["vx"])
+    pb.srf_ptr, pb.srf_pts = _ptr(keep["sp"]), _ptr(keep["sx"])
+    pb.n_sfaces = keep["fc"].shape[0]
+    pb.sf_cells, pb.sf_axis = _ptr(keep["fc"]), _ptr(keep["fa"])
+    pb.sf_ptr, pb.sf_pts = _ptr(keep["fp"]), _ptr(keep["fx"])
+    pb.sipg_gamma, pb.nitsche_tau = float(prob.sipg_gamma), float(prob.nitsche_tau)
+    pb.gp_gamma = _ptr(keep["gp"])
+    pb.term_mask = int(term_mask)
+    return pb, keep
+
+
+def _arr(ptr, n, ctype, dtype, shape):
+    if n == 0 or not ptr:
+        return np.zeros(shape, dtype=dtype)
+    return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctype)), shape=(n,)).astype(dtype).reshape(shape)
+
+
+def partition_x(prob, nparts: int, w_cut: float = 7.0):
+    """Weighted x-slab split (host only): list of nparts+1 plane indices."""
+    L = load()
+    pb, keep = _marshal(prob)
+    out = np.zeros(nparts + 1, dtype=np.int32)
+    _check(L.cutfem_partition_x(ctypes.byref(pb), int(nparts), float(w_cut), out.ctypes.data))
+    return [int(x) for x in out]
+
+
+class LocalProblem:
+    """Local problem of one x-slab (host only), built by the C library: owned blocks
+    then the ghost planes.  Field names match cutgen.Problem."""
+
+    def __init__(self, prob, x_begin: int, x_end: int):
+        L = load()
+        pb, keep = _marshal(prob)
+        loc = _Local()
+        _check(L.cutfem_local_build(ctypes.byref(pb), int(x_begin), int(x_end), ctypes.byref(loc)))
+        try:
+            q = loc.pb
+            na, n_sf = int(q.n_active), int(q.n_sfaces)
+            self.active_ijk = _arr(q.active_ijk, 3 * na, ctypes.c_int32, np.int32, (na, 3))
+            self.is_cut = _arr(q.is_cut, na, ctypes.c_uint8, np.uint8, (na,))
+            nc = int(self.is_cut.sum())
+            self.vol_ptr = _arr(q.vol_ptr, nc + 1, ctypes.c_int64, np.int64, (nc + 1,))
+            self.srf_ptr = _arr(q.srf_ptr, nc + 1, ctypes.c_int64, np.int64, (nc + 1,))
+            self.vol_pts = _arr(q.vol_pts, 4 * int(self.vol_ptr[-1]), ctypes.c_double, np.float64, (-1, 4))
+            self.srf_pts = _arr(q.srf_pts, 7 * int(self.srf_ptr[-1]), ctypes.c_double, np.float64, (-1, 7))
+            self.sf_cells = _arr(q.sf_cells, 2 * n_sf, ctypes.c_int32, np.int32, (n_sf, 2))
+            self.sf_axis = _arr(q.sf_axis, n_sf, ctypes.c_uint8, np.uint8, (n_sf,))
+            self.sf_ptr = _arr(q.sf_ptr, n_sf + 1, ctypes.c_int64, np.int64, (n_sf + 1,))
+            self.sf_pts = _arr(q.sf_pts, 3 * int(self.sf_ptr[-1]), ctypes.c_double, np.float64, (-1, 3))
+            self.n_own, self.n_ghost_lo, self.n_ghost_hi = int(loc.n_own), int(loc.n_ghost_lo), int(loc.n_ghost_hi)
+            self.global_begin, self.plane_lo, self.plane_hi = int(loc.global_begin), int(loc.plane_lo), int(loc.plane_hi)
+        finally:
+            L.cutfem_local_free(ctypes.byref(loc))
+        for k in ("n_cells", "lower", "h", "degree", "sipg_gamma", "nitsche_tau", "gp_gamma", "level_set"):
+            setattr(self, k, getattr(prob, k))
+        self.vol_pts = self.vol_pts.reshape(-1, 4)
+        self.srf_pts = self.srf_pts.reshape(-1, 7)
+        self.sf_pts = self.sf_pts.reshape(-1, 3)
+
+    @property
+    def n_active(self):
+        return int(self.active_ijk.shape[0])
+
+    @property
+    def n_dofs(self):
+        return self.n_active * (self.degree + 1) ** 3
+
+
+def nccl_unique_id() -> bytes:
+    L = load()
+    buf = ctypes.create_string_buffer(128)
+    _check(L.cutfem_nccl_unique_id(buf, 128))
+    return bytes(buf.raw)
+
+
 class CutFEM:
     """Handle for v = A u on one GPU.  ``prob`` is a cutgen.Problem (or anything
     with the same fields).  Device vectors are torch.float64 CUDA tensors."""
 
-    def __init__(self, prob, device: int = 0, term_mask: int = TERM_ALL):
+    def __init__(self, prob, device: int = 0, term_mask: int = TERM_ALL, _dist=None):
         L = load()
-        self._keep = keep = {
-            "ijk": np.ascontiguousarray(prob.active_ijk, dtype=np.int32),
-            "cut": np.ascontiguousarray(prob.is_cut, dtype=np.uint8),
-            "vp": np.ascontiguousarray(prob.vol_ptr, dtype=np.int64),
-            "vx": np.ascontiguousarray(prob.vol_pts, dtype=np.float64),
-            "sp": np.ascontiguousarray(prob.srf_ptr, dtype=np.int64),
-            "sx": np.ascontiguousarray(prob.srf_pts, dtype=np.float64),
-            "fc": np.ascontiguousarray(prob.sf_cells, dtype=np.int32),
-            "fa": np.ascontiguousarray(prob.sf_axis, dtype=np.uint8),
-            "fp": np.ascontiguousarray(prob.sf_ptr, dtype=np.int64),
-            "fx": np.ascontiguousarray(prob.sf_pts, dtype=np.float64),
-            "gp": np.ascontiguousarray(prob.gp_gamma, dtype=np.float64),
-        }
-        pb = _Problem()
-        for i in range(3):
-            pb.n_cells[i] = int(prob.n_cells[i])
-            pb.lower[i] = float(prob.lower[i])
-        pb.h = float(prob.h)
-        pb.degree = int(prob.degree)
-        pb.n_active = keep["ijk"].shape[0]
-        pb.active_ijk, pb.is_cut = _ptr(keep["ijk"]), _ptr(keep["cut"])
-        pb.vol_ptr, pb.vol_pts = _ptr(keep["vp"]), _ptr(keep["vx"])
-        pb.srf_ptr, pb.srf_pts = _ptr(keep["sp"]), _ptr(keep["sx"])
-        pb.n_sfaces = keep["fc"].shape[0]
-        pb.sf_cells, pb.sf_axis = _ptr(keep["fc"]), _ptr(keep["fa"])
-        pb.sf_ptr, pb.sf_pts = _ptr(keep["fp"]), _ptr(keep["fx"])
-        pb.sipg_gamma, pb.nitsche_tau = float(prob.sipg_gamma), float(prob.nitsche_tau)
-        pb.gp_gamma = _ptr(keep["gp"])
-        pb.term_mask = int(term_mask)
+        pb, keep = _marshal(prob, term_mask)
         h = ctypes.c_void_p()
-        _check(L.cutfem_setup(ctypes.byref(pb), int(device), ctypes.byref(h)))
+        if _dist is None:
+            _check(L.cutfem_setup(ctypes.byref(pb), int(device), ctypes.byref(h)))
+        else:
+            x0, x1, rank, nranks, nid = _dist
+            idb = ctypes.create_string_buffer(nid, 128) if nid is not None else None
+            _check(L.cutfem_setup_dist(ctypes.byref(pb), int(x0), int(x1), int(rank), int(nranks), idb,
+                                       int(device), ctypes.byref(h)))
         self._h = h
         self._L = L
         self.device = device
         self.degree = int(prob.degree)
-        self.n_dofs = int(keep["ijk"].shape[0]) * (self.degree + 1) ** 3
-        del self._keep  # setup deep-copied everything
+        st = self.stats()
+        self.n_dofs = int(st["n_dofs"])          # v length (owned blocks)
+        self.n_ext_dofs = int(st["n_ext_dofs"])  # u length (owned + ghost blocks)
 
     def stats(self) -> dict:
         s = Stats()
@@ -176,9 +283,9 @@ class CutFEM:
         """v = A u on the device (torch float64 CUDA tensors), stream-ordered."""
         import torch
         if v is None:
-            v = torch.empty_like(u)
+            v = torch.empty(self.n_dofs, dtype=u.dtype, device=u.device)
         assert u.dtype == torch.float64 and v.dtype == torch.float64 and u.is_cuda and v.is_cuda
-        assert u.numel() == self.n_dofs and v.numel() == self.n_dofs
+        assert u.numel() == self.n_ext_dofs and v.numel() == self.n_dofs
         assert u.is_contiguous() and v.is_contiguous()
         _check(self._L.cutfem_apply(self._h, u.data_ptr(), v.data_ptr(), _stream_ptr(stream)))
         return v
@@ -236,3 +343,16 @@ class CutFEM:
             self.close()
         except Exception:
             pass
+
+
+class CutFEMDist(CutFEM):
+    """One rank's x-slab [x_begin, x_end) of the global problem.  apply(u_ext, v):
+    u_ext holds n_ext_dofs values (owned blocks first; the ghost tail is filled by
+    the NCCL halo exchange inside the apply), v receives the n_dofs owned values."""
+
+    def __init__(self, prob, x_begin, x_end, rank=0, nranks=1, nccl_id=None, device=0, term_mask=TERM_ALL):
+        super().__init__(prob, device=device, term_mask=term_mask,
+                         _dist=(x_begin, x_end, rank, nranks, nccl_id))
+        n_own, g_lo, g_hi = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(self._L.cutfem_dist_info(self._h, ctypes.byref(n_own), ctypes.byref(g_lo), ctypes.byref(g_hi)))
+        self.n_own_blocks, self.n_ghost_lo, self.n_ghost_hi = n_own.value, g_lo.value, g_hi.value

@@ -143,6 +143,7 @@ int cutfem_csr_setup(cutfem_handle *hd, int64_t n_rows, const int64_t *row_ptr, 
 
 int cutfem_csr_assemble(cutfem_handle *hd, int64_t *nnz_out) {
   if (!hd) return fail(CUTFEM_EINVAL, "null handle");
+  if (hd->dist || hd->n_own != hd->n_active) return fail(CUTFEM_EUNSUPPORTED, "CSR assembly needs a single-GPU handle");
   CU(cudaSetDevice(hd->device));
   csr_free(hd);
   // The handle's descriptors live on the device; rebuild the block graph from them.

@@ -9,6 +9,7 @@
 // blocks), joined by an event — no host synchronisation.
 #include <cuda_runtime.h>
 #include <cusparse.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -47,6 +48,17 @@ struct cutfem_handle {
   double h = 1;
   int64_t n_active = 0, n_uncut = 0, n_cut = 0;
   int64_t n_plain = 0;     // uncut cells whose six neighbours are active and uncut (first in d_udesc)
+  int64_t n_own = 0;       // computed blocks (= n_active unless distributed; ghosts follow)
+  // descriptor ranges per part (0 all, 1 interior, 2 slab boundary): plain, general, cut
+  int64_t r_off[3][3] = {{0}}, r_cnt[3][3] = {{0}};
+  // distributed (x-slab) state
+  int rank = 0, nranks = 1;
+  bool dist = false;
+  int64_t ghost_lo = 0, ghost_hi = 0;      // ghost blocks after the owned ones
+  int64_t plane_lo = 0, plane_hi = 0;      // owned blocks of the first / last owned plane
+  void *comm = nullptr;                    // ncclComm_t
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_comm = nullptr, ev_comm_fork = nullptr;
   int sm_count = 148;
   int occ_plain = 1, occ_gen = 1;  // resident CTAs per SM of the persistent structured kernels
   int occ_cut = 1;                 // ... and of the persistent unstructured kernel
@@ -142,11 +154,16 @@ void build_facetab(int p, double h, const double *gpg, FaceTab &ft) {
   }
 }
 
-// which: bit0 structured (uncut) kernel, bit1 unstructured (cut) kernel.  With
-// both, the cut kernel runs on the forked side stream, concurrently.
+// which: bit0 structured (uncut) kernels, bit1 unstructured (cut) kernel; part:
+// 0 all owned cells, 1 slab-interior cells, 2 slab-boundary cells.  With both
+// kinds, the cut kernel runs on the forked side stream, concurrently.
 template <int N>
-int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which = 3) {
-  const int64_t nu = (which & 1) ? hd->n_uncut : 0, nc = (which & 2) ? hd->n_cut : 0;
+int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which = 3, int part = 0) {
+  const int64_t np = (which & 1) ? hd->r_cnt[part][0] : 0, ng = (which & 1) ? hd->r_cnt[part][1] : 0;
+  const int64_t nc = (which & 2) ? hd->r_cnt[part][2] : 0;
+  const UDesc *dp = hd->d_udesc + hd->r_off[part][0], *dg = hd->d_udesc + hd->r_off[part][1];
+  const CDesc *dc = hd->d_cdesc + hd->r_off[part][2];
+  const int64_t nu = np + ng;
   const bool fork = nc > 0 && nu > 0;
   cudaStream_t cs = fork ? hd->side : st;
   if (nc > 0) {
@@ -158,12 +175,12 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
       using CW = CutWCfg<(N <= 4 ? N : 4)>;
       const unsigned grid = (unsigned)((nc + CW::WARPS - 1) / CW::WARPS);
       k_cutw<(N <= 4 ? N : 4)><<<grid, 32 * CW::WARPS, CW::SMEM, cs>>>(
-          u, v, hd->d_cdesc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp,
-          hd->d_sfptr, hd->kp, hd->ft);
+          u, v, dc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp, hd->d_sfptr, hd->kp,
+          hd->ft);
     } else {
       k_cut<N><<<(unsigned)nc, CutCfg<N>::THREADS, CutCfg<N>::SMEM, cs>>>(
-          u, v, hd->d_cdesc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp,
-          hd->d_sfptr, hd->kp, hd->ft);
+          u, v, dc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp, hd->d_sfptr, hd->kp,
+          hd->ft);
     }
     CU(cudaGetLastError());
   }
@@ -172,28 +189,32 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
       constexpr int NC = (N <= 5 ? N : 5);
       using C = Uncut3Cfg<NC>;
       const int per_block = C::WARPS * C::CPW;
-      const int64_t np = hd->n_plain, ng = nu - np;
       const bool plain_ok = (hd->kp.mask & TERM_SIPG) != 0;
       auto grid_for = [&](int64_t n, int occ) {
         const int64_t need = (n + per_block - 1) / per_block;
         return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)occ * hd->sm_count));
       };
-      if (plain_ok) {
-        if (np > 0)
-          k_uncut3<NC, true><<<grid_for(np, hd->occ_plain), 32 * C::WARPS, C::SMEM, st>>>(
-              u, v, hd->d_udesc, (int)np, hd->kp, hd->ft);
-        if (ng > 0)
-          k_uncut3<NC, false><<<grid_for(ng, hd->occ_gen), 32 * C::WARPS, C::SMEM, st>>>(
-              u, v, hd->d_udesc + np, (int)ng, hd->kp, hd->ft);
-      } else {
-        k_uncut3<NC, false><<<grid_for(nu, hd->occ_gen), 32 * C::WARPS, C::SMEM, st>>>(u, v, hd->d_udesc,
-                                                                                          (int)nu, hd->kp, hd->ft);
+      // plain cells run the branch-free path (needs SIPG on); the rest the general one
+      if (np > 0) {
+        if (plain_ok)
+          k_uncut3<NC, true><<<grid_for(np, hd->occ_plain), 32 * C::WARPS, C::SMEM, st>>>(u, v, dp, (int)np,
+                                                                                            hd->kp, hd->ft);
+        else
+          k_uncut3<NC, false><<<grid_for(np, hd->occ_gen), 32 * C::WARPS, C::SMEM, st>>>(u, v, dp, (int)np,
+                                                                                            hd->kp, hd->ft);
       }
+      if (ng > 0)
+        k_uncut3<NC, false><<<grid_for(ng, hd->occ_gen), 32 * C::WARPS, C::SMEM, st>>>(u, v, dg, (int)ng, hd->kp,
+                                                                                          hd->ft);
     } else {
       using C = UncutCfg<N>;
       const int per_block = C::WARPS * C::CPW;
-      const unsigned grid = (unsigned)((nu + per_block - 1) / per_block);
-      k_uncut<N><<<grid, 32 * C::WARPS, C::SMEM, st>>>(u, v, hd->d_udesc, (int)nu, hd->kp, hd->ft);
+      if (np > 0)
+        k_uncut<N><<<(unsigned)((np + per_block - 1) / per_block), 32 * C::WARPS, C::SMEM, st>>>(u, v, dp, (int)np,
+                                                                                               hd->kp, hd->ft);
+      if (ng > 0)
+        k_uncut<N><<<(unsigned)((ng + per_block - 1) / per_block), 32 * C::WARPS, C::SMEM, st>>>(u, v, dg, (int)ng,
+                                                                                               hd->kp, hd->ft);
     }
     CU(cudaGetLastError());
   }
@@ -236,16 +257,16 @@ int set_attrs() {
   return 0;
 }
 
-int dispatch_apply(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which = 3) {
+int dispatch_part(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which, int part) {
   switch (hd->n) {
-    case 2: return launch<2>(hd, u, v, st, which);
-    case 3: return launch<3>(hd, u, v, st, which);
-    case 4: return launch<4>(hd, u, v, st, which);
-    case 5: return launch<5>(hd, u, v, st, which);
-    case 6: return launch<6>(hd, u, v, st, which);
-    case 7: return launch<7>(hd, u, v, st, which);
-    case 8: return launch<8>(hd, u, v, st, which);
-    case 9: return launch<9>(hd, u, v, st, which);
+    case 2: return launch<2>(hd, u, v, st, which, part);
+    case 3: return launch<3>(hd, u, v, st, which, part);
+    case 4: return launch<4>(hd, u, v, st, which, part);
+    case 5: return launch<5>(hd, u, v, st, which, part);
+    case 6: return launch<6>(hd, u, v, st, which, part);
+    case 7: return launch<7>(hd, u, v, st, which, part);
+    case 8: return launch<8>(hd, u, v, st, which, part);
+    case 9: return launch<9>(hd, u, v, st, which, part);
   }
   return fail(CUTFEM_EUNSUPPORTED, "degree");
 }
@@ -258,6 +279,19 @@ int dispatch_occ(cutfem_handle *hd) {
     case 5: return query_occ<5>(hd);
     default: return 0;
   }
+}
+
+int halo_exchange(cutfem_handle *hd, const double *u_ext, cudaStream_t st);  // dist.inl
+
+int dispatch_apply(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which = 3) {
+  if (!hd->dist) return dispatch_part(hd, u, v, st, which, 0);
+  // x-slab: the halo exchange runs on the comm stream while the slab-interior
+  // cells compute; the boundary cells follow once the ghost blocks have landed
+  int rc = halo_exchange(hd, u, st);
+  if (rc) return rc;
+  if ((rc = dispatch_part(hd, u, v, st, which, 1))) return rc;
+  if (hd->ev_comm) CU(cudaStreamWaitEvent(st, hd->ev_comm, 0));
+  return dispatch_part(hd, u, v, st, which, 2);
 }
 
 int dispatch_attrs(int n) {
@@ -293,12 +327,16 @@ void free_handle(cutfem_handle *hd) {
   if (hd->spA) cusparseDestroySpMat(hd->spA);
   if (hd->sp) cusparseDestroy(hd->sp);
   if (hd->side) cudaStreamDestroy(hd->side);
+  if (hd->comm) ncclCommDestroy((ncclComm_t)hd->comm);
+  if (hd->comm_stream) cudaStreamDestroy(hd->comm_stream);
+  if (hd->ev_comm) cudaEventDestroy(hd->ev_comm);
+  if (hd->ev_comm_fork) cudaEventDestroy(hd->ev_comm_fork);
   if (hd->ev_fork) cudaEventDestroy(hd->ev_fork);
   if (hd->ev_join) cudaEventDestroy(hd->ev_join);
   delete hd;
 }
 
-int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
+int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t n_compute = -1) {
   if (!pb) return fail(CUTFEM_EINVAL, "null problem");
   const int p = pb->degree;
   if (p < 1 || p > 8) return fail(CUTFEM_EINVAL, "degree must be in 1..8");
@@ -395,10 +433,13 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
   std::vector<UDesc> ud;
   std::vector<CDesc> cd;
   std::vector<int64_t> ccost;
+  if (n_compute < 0) n_compute = na;
+  hd->n_own = n_compute;
   ud.reserve(na - nc);
   cd.reserve(nc);
+  std::vector<uint8_t> ubnd, cbnd;  // slab-boundary flag (a neighbour is a ghost block)
   int64_t n_struct = 0, n_gp = 0;
-  for (int64_t b = 0; b < na; ++b) {
+  for (int64_t b = 0; b < n_compute; ++b) {
     const int32_t ijk[3] = {pb->active_ijk[3 * b], pb->active_ijk[3 * b + 1], pb->active_ijk[3 * b + 2]};
     int32_t nb[6];
     for (int f = 0; f < 6; ++f) {
@@ -409,7 +450,11 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
       nb[f] = (q[d] < 0 || q[d] >= lim) ? -1 : grid[(size_t)((q[0] * ny + q[1]) * nz + q[2])];
     }
     const bool cut = pb->is_cut[b] != 0;
+    bool bnd = false;
+    for (int f = 0; f < 6; ++f)
+      if (nb[f] >= n_compute) bnd = true;
     if (!cut) {
+      ubnd.push_back(bnd ? 1 : 0);
       UDesc u;
       std::memset(&u, 0, sizeof(u));
       u.blk = (int32_t)b;
@@ -443,7 +488,8 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
         }
       }
       cd.push_back(c);
-      ccost.push_back(cost);
+      ccost.push_back(cost + (bnd ? (int64_t)1 << 40 : 0));  // boundary cells sort last (key), heavy first
+      cbnd.push_back(bnd ? 1 : 0);
     }
     // count every interior face once, from its minus side (hi face f = 2d+1)
     for (int d = 0; d < 3; ++d) {
@@ -453,28 +499,55 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
       if (sfid[b * 6 + 2 * d + 1] < 0) ++n_struct;
     }
   }
-  // uncut: "plain" cells (six active uncut neighbours) first
+  // uncut order: [plain interior | plain boundary | general interior | general boundary];
+  // plain = six active uncut neighbours
   {
-    std::vector<UDesc> plain, gen;
-    for (auto &x : ud) {
+    std::vector<UDesc> cls[2][2];
+    for (size_t i = 0; i < ud.size(); ++i) {
+      const UDesc &x = ud[i];
       bool pl = true;
       for (int f = 0; f < 6; ++f)
         if (x.nb[f] < 0 || pb->is_cut[x.nb[f]]) pl = false;
-      (pl ? plain : gen).push_back(x);
+      cls[pl ? 0 : 1][ubnd[i]].push_back(x);
     }
-    hd->n_plain = (int64_t)plain.size();
-    ud = plain;
-    ud.insert(ud.end(), gen.begin(), gen.end());
+    ud.clear();
+    int64_t off = 0;
+    for (int k = 0; k < 2; ++k) {
+      hd->r_off[1][k] = off;
+      hd->r_cnt[1][k] = (int64_t)cls[k][0].size();
+      hd->r_off[2][k] = off + (int64_t)cls[k][0].size();
+      hd->r_cnt[2][k] = (int64_t)cls[k][1].size();
+      hd->r_off[0][k] = off;
+      hd->r_cnt[0][k] = (int64_t)(cls[k][0].size() + cls[k][1].size());
+      for (int bd = 0; bd < 2; ++bd) ud.insert(ud.end(), cls[k][bd].begin(), cls[k][bd].end());
+      off += hd->r_cnt[0][k];
+    }
+    hd->n_plain = hd->r_cnt[0][0];
   }
-  // heaviest cut cells first (LPT order for the block scheduler)
+  // cut order: [interior | boundary], each heaviest first (LPT order for the block scheduler)
   {
     std::vector<int64_t> order(cd.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int64_t)i;
-    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return ccost[a] > ccost[b]; });
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      if (cbnd[a] != cbnd[b]) return cbnd[a] < cbnd[b];
+      return ccost[a] > ccost[b];
+    });
     std::vector<CDesc> s(cd.size());
-    for (size_t i = 0; i < order.size(); ++i) s[i] = cd[order[i]];
+    int64_t nci = 0;
+    for (size_t i = 0; i < order.size(); ++i) {
+      s[i] = cd[order[i]];
+      if (!cbnd[order[i]]) ++nci;
+    }
     cd.swap(s);
+    hd->r_off[0][2] = 0;
+    hd->r_cnt[0][2] = (int64_t)cd.size();
+    hd->r_off[1][2] = 0;
+    hd->r_cnt[1][2] = nci;
+    hd->r_off[2][2] = nci;
+    hd->r_cnt[2][2] = (int64_t)cd.size() - nci;
   }
+  hd->n_uncut = (int64_t)ud.size();
+  hd->n_cut = (int64_t)cd.size();
   int rc;
   if ((rc = upload(hd, &hd->d_udesc, ud.data(), ud.size()))) return rc;
   if ((rc = upload(hd, &hd->d_cdesc, cd.data(), cd.size()))) return rc;
@@ -517,9 +590,9 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
   CU(cudaEventCreateWithFlags(&hd->ev_join, cudaEventDisableTiming));
   cutfem_stats_t &s = hd->stats;
   std::memset(&s, 0, sizeof(s));
-  s.n_active = na;
-  s.n_uncut = na - nc;
-  s.n_cut = nc;
+  s.n_active = hd->n_own;
+  s.n_uncut = hd->n_uncut;
+  s.n_cut = hd->n_cut;
   s.n_vol_pts = nvol;
   s.n_srf_pts = nsrf;
   s.n_face_pts = nfp;
@@ -527,10 +600,11 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd) {
   s.n_faces_cut = n_fcut;
   s.n_faces_empty = n_fempty;
   s.n_faces_gp = n_gp;
-  s.n_dofs = na * n * n * n;
+  s.n_dofs = hd->n_own * n * n * n;
+  s.n_ext_dofs = na * n * n * n;
   s.degree = p;
   s.device = device;
-  s.launches_per_apply = (nc > 0) + (hd->n_plain > 0) + (na - nc - hd->n_plain > 0);
+  s.launches_per_apply = (hd->n_cut > 0) + (hd->n_plain > 0) + (hd->n_uncut - hd->n_plain > 0);
   return 0;
 }
 
@@ -608,3 +682,4 @@ int cutfem_destroy(cutfem_handle *hd) {
 }  // extern "C"
 
 #include "csr.inl"
+#include "dist.inl"
