@@ -10,8 +10,9 @@ stream; max over ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun (N > 1) every rank runs one replica of the workload on its own
-GPU (weak scaling).
+Under torchrun (N > 1) the same global workload is split into N x-slabs, one per
+GPU, with the NCCL halo exchange inside every apply (strong scaling; DESIGN.md
+"Multi-GPU").
 """
 from __future__ import annotations
 
@@ -182,10 +183,27 @@ def run_ours(args, P, cfg, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    op = cf.CutFEM(P, device=local_rank)
+    nd = (P.degree + 1) ** 3
+    ug = P.seeded_u(0)
+    if world == 1:
+        op = cf.CutFEM(P, device=local_rank)
+        g0, n_own = 0, P.n_active
+        u = torch.from_numpy(ug).to(dev)
+        xs = [0, P.n_cells[0]]
+    else:
+        # x-slab partition (weights 1 / w_cut), one slab per rank, NCCL halo inside the apply
+        xs = cf.partition_x(P, world, args.w_cut)
+        nid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            nid.copy_(torch.frombuffer(bytearray(cf.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(nid, 0)
+        op = cf.CutFEMDist(P, xs[rank], xs[rank + 1], rank, world, bytes(nid.cpu().numpy()), device=local_rank)
+        L = cf.LocalProblem(P, xs[rank], xs[rank + 1])
+        g0, n_own = L.global_begin, L.n_own
+        u = torch.zeros(op.n_ext_dofs, dtype=torch.float64, device=dev)
+        u[:n_own * nd] = torch.from_numpy(ug[g0 * nd:(g0 + n_own) * nd]).to(dev)
     st = op.stats()
-    u = torch.from_numpy(P.seeded_u(0)).to(dev)
-    v = torch.empty_like(u)
+    v = torch.empty(op.n_dofs, dtype=torch.float64, device=dev)
     props = torch.cuda.get_device_properties(dev)
     l2 = int(getattr(props, "L2_cache_size", 128 << 20) or (128 << 20))
     flush = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device=dev)
@@ -223,7 +241,7 @@ def run_ours(args, P, cfg, rank, world, local_rank):
         t = torch.tensor([ms_step], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
-    value = world * P.n_dofs / (ms_step * 1e-3)
+    value = P.n_dofs / (ms_step * 1e-3)  # whole-job throughput: the global operator per step
 
     # per-kernel timing (attribution) on the same stream
     k_ms = {}
@@ -238,7 +256,7 @@ def run_ours(args, P, cfg, rank, world, local_rank):
     peaks = load_peaks()
     bw = float(peaks.get("hbm_gbs", 6543.7)) * 1e9
     fp64 = costmodel.fp64_peak_tflops() * 1e12
-    kname = {"structured": f"k_uncut<{P.degree + 1}>", "unstructured": f"k_cut<{P.degree + 1}>"}
+    kname = {"structured": f"k_uncut3<{P.degree + 1}>", "unstructured": f"k_cutw<{P.degree + 1}>"}
     dom = max(k_ms, key=k_ms.get)
     F_dom = work["F_uncut"] if dom == "structured" else work["F_cut"]
     B_dom = work["B_uncut"] if dom == "structured" else work["B_cut"]
@@ -250,33 +268,54 @@ def run_ours(args, P, cfg, rank, world, local_rank):
                 "kernel_ms": k_ms[dom], "flops_per_launch": F_dom, "alg_bytes_per_launch": B_dom,
                 "peak_kind": "derived FP64: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (measured DFMA probe 34.1)",
                 "apply": {"F_alg": work["F_total"], "B_alg": work["B_total"],
-                          "flop_per_dof": work["F_total"] / P.n_dofs, "byte_per_dof": work["B_total"] / P.n_dofs,
+                          "flop_per_dof": work["F_total"] / max(op.n_dofs, 1),
+                          "byte_per_dof": work["B_total"] / max(op.n_dofs, 1),
                           "t_roof_ms": t_roof * 1e3, "frac": t_roof / (ms_step * 1e-3),
                           "hbm_gbs": bw / 1e9, "fp64_tflops": fp64 / 1e12},
-                "per_kernel_ms": k_ms}
+                "per_kernel_ms": k_ms, "scope": "rank 0" if world > 1 else "whole problem"}
 
-    # end to end through the C ABI with pinned host buffers
-    uh = torch.from_numpy(P.seeded_u(0)).pin_memory()
-    vh = torch.empty_like(uh).pin_memory()
-    uhn, vhn = uh.numpy(), vh.numpy()
+    # end to end through the public API with pinned host buffers
+    uh = torch.from_numpy(ug[g0 * nd:(g0 + n_own) * nd].copy()).pin_memory()
+    vh = torch.empty(op.n_dofs, dtype=torch.float64).pin_memory()
+    if world == 1:
+        uhn, vhn = uh.numpy(), vh.numpy()
+        e2e_fn = lambda: op.apply_host(uhn, vhn)  # noqa: E731
+    else:
+        def e2e_fn():
+            u[:n_own * nd].copy_(uh, non_blocking=True)
+            op.apply(u, v)
+            vh.copy_(v, non_blocking=True)
+            torch.cuda.synchronize(dev)
     for _ in range(2):
-        op.apply_host(uhn, vhn)
+        e2e_fn()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        op.apply_host(uhn, vhn)
+        e2e_fn()
     e2e_s = (time.perf_counter() - t0) / args.steps
-    e2e = {"value": world * P.n_dofs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * P.n_dofs,
-           "d2h_bytes_per_step": 8 * P.n_dofs, "ms_per_step": e2e_s * 1e3}
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": P.n_dofs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * op.n_dofs,
+           "d2h_bytes_per_step": 8 * op.n_dofs, "ms_per_step": e2e_s * 1e3,
+           "bytes_scope": "per rank" if world > 1 else "whole problem"}
     vd = op.apply(u, v)
     torch.cuda.synchronize(dev)
-    assert np.array_equal(vd.cpu().numpy(), vhn), "host path and device path disagree"
+    if world == 1:
+        assert np.array_equal(vd.cpu().numpy(), vh.numpy()), "host path and device path disagree"
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {**workload_desc(P, cfg), "parallelism": f"replicas{world}" if world > 1 else "single"},
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {**workload_desc(P, cfg),
+                       "parallelism": f"xslab{world}" if world > 1 else "single",
+                       "x_split": xs},
             "clocks": clk.summary(), "e2e": e2e,
-            "gpu_launches": args.steps * int(st["launches_per_apply"]), "roofline": roofline}
+            "gpu_launches": args.steps * int(st["launches_per_apply"]) * (2 if world > 1 else 1),
+            "roofline": roofline}
 
     if not args.no_csr and world == 1:
         try:
@@ -317,6 +356,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=3.0)
+    ap.add_argument("--w-cut", type=float, default=7.0, help="slab-balance weight of a cut cell (uncut = 1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
