@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -65,6 +66,13 @@ struct cutfem_handle {
   uint32_t mask = CUTFEM_TERM_ALL;
   KParams kp;
   FaceTab ft;
+  // thread-per-cell structured kernel (N <= 4): warp-tiles per part (0 all, 1 interior, 2 boundary)
+  // tile sets: [0] uncut cells, volume + SIPG (v = ...); [1] ghost-penalty cells
+  // (cut cells and their uncut neighbours) + the cut cells' structured SIPG (v += ...)
+  void *d_tiles = nullptr;
+  int64_t t_off[2][3] = {{0}}, t_cnt[2][3] = {{0}};
+  int occ_tile[2] = {1, 1};
+  std::vector<char> ttab;  // TileTab<N> bytes
   UDesc *d_udesc = nullptr;
   CDesc *d_cdesc = nullptr;
   double *d_vol = nullptr, *d_srf = nullptr, *d_sfp = nullptr;
@@ -154,11 +162,327 @@ void build_facetab(int p, double h, const double *gpg, FaceTab &ft) {
   }
 }
 
+// ---- k_tile: per-handle line operators (long double, then rounded)
+template <int N>
+void build_tiletab(double h, double sipg_gamma, const double *gpg, TileTab<N> &tt) {
+  typedef long double ld;
+  const int p = N - 1, n = N;
+  cutfem_tables::Ref r = cutfem_tables::build(p);
+  std::vector<ld> K1(n * n, 0), Mi(n * n, 0), A(n * n);
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b < n; ++b) {
+      ld k = 0;
+      for (int q = 0; q < n; ++q)
+        k += r.w[q] * cutfem_tables::dlag(r.x, a, r.g[q]) * cutfem_tables::dlag(r.x, b, r.g[q]);
+      K1[a * n + b] = k;
+    }
+  // M^{-1} by Gauss-Jordan (M is SPD, well conditioned for n <= 9)
+  for (int i = 0; i < n * n; ++i) A[i] = r.M[i];
+  for (int i = 0; i < n; ++i) Mi[i * n + i] = 1;
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int i = c + 1; i < n; ++i)
+      if (std::fabs((double)A[i * n + c]) > std::fabs((double)A[piv * n + c])) piv = i;
+    for (int j = 0; j < n; ++j) {
+      std::swap(A[c * n + j], A[piv * n + j]);
+      std::swap(Mi[c * n + j], Mi[piv * n + j]);
+    }
+    const ld d = A[c * n + c];
+    for (int j = 0; j < n; ++j) {
+      A[c * n + j] /= d;
+      Mi[c * n + j] /= d;
+    }
+    for (int i = 0; i < n; ++i) {
+      if (i == c) continue;
+      const ld f = A[i * n + c];
+      for (int j = 0; j < n; ++j) {
+        A[i * n + j] -= f * A[c * n + j];
+        Mi[i * n + j] -= f * Mi[c * n + j];
+      }
+    }
+  }
+  auto tr = [&](int j, int s, int a) { return r.tr[(j * 2 + s) * n + a]; };  // l_a^(j)(s)
+  std::memset(&tt, 0, sizeof(tt));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      ld x = 0;
+      for (int k = 0; k < n; ++k) x += Mi[i * n + k] * K1[k * n + j];
+      tt.L[i * n + j] = (double)(h * x);
+      tt.M[i * n + j] = (double)r.M[i * n + j];
+    }
+  // lo face (own cell is the plus side, own face node 0); the hi face uses the
+  // mirrored entries (see TileTab)
+  const ld h2sig = (ld)h * sipg_gamma, hs = (ld)h / 2;
+  for (int m = 0; m < n; ++m) {
+    ld be = 0;
+    for (int k = 0; k < n; ++k) be += Mi[m * n + k] * tr(1, 0, k);
+    const ld al = Mi[m * n + 0];
+    tt.cJ[m] = (double)(al * h2sig + be * hs);
+    tt.cA[m] = (double)(al * hs);
+    tt.d0[m] = (double)tr(1, 0, m);
+  }
+  // ghost penalty (lo face, own coordinate 0, neighbour 1):
+  //   Goo[m][a] = h sum_j g_j l_m^(j)(0) l_a^(j)(0), Gon[m][a] = h sum_j g_j l_m^(j)(0) l_a^(j)(1)
+  std::vector<ld> Goo(n * n, 0), Gon(n * n, 0);
+  for (int m = 0; m < n; ++m)
+    for (int a = 0; a < n; ++a)
+      for (int j = 0; j <= p; ++j) {
+        Goo[m * n + a] += (ld)h * gpg[j] * tr(j, 0, m) * tr(j, 0, a);
+        Gon[m * n + a] += (ld)h * gpg[j] * tr(j, 0, m) * tr(j, 1, a);
+      }
+  for (int m = 0; m < n; ++m)
+    for (int a = 0; a < n; ++a) {
+      ld go = 0, gn = 0;
+      for (int k = 0; k < n; ++k) {
+        go += Mi[m * n + k] * Goo[k * n + a];
+        gn += Mi[m * n + k] * Gon[k * n + a];
+      }
+      tt.Goo[m * n + a] = (double)go;
+      tt.Gon[m * n + a] = (double)(-gn);
+    }
+}
+
+// ---- k_tile*: one cell of a tile set: block, face neighbours, face masks
+struct TCell {
+  int32_t blk;
+  int32_t nb[6];
+  uint32_t gp, sipg;  // faces (bits 0..5) with ghost penalty / SIPG in this pass
+  bool vol;
+};
+
+// Group cells into warp-tiles of <= 32 cells (bricks of the background grid,
+// partial bricks merged in brick order) and number the slots: own cells first
+// (slot = cell index), then the face-neighbour halo of the faces with work, face
+// by face (so that the lanes of one face read consecutive slots).
+template <int N>
+void build_tiles(const std::vector<TCell> &cells, const cutfem_problem *pb, std::vector<char> &out) {
+  using C = TileCfg<N>;
+  using R = TileRec<C::SMAX>;
+  auto used = [&](const TCell &c, int f) { return c.nb[f] >= 0 && (((c.gp | c.sipg) >> f) & 1u); };
+  std::vector<std::pair<int64_t, int64_t>> key(cells.size());
+  for (size_t c = 0; c < cells.size(); ++c) {
+    const int32_t *q = pb->active_ijk + 3 * (size_t)cells[c].blk;
+    const int64_t bk = ((int64_t)(q[0] / C::BX) << 42) | ((int64_t)(q[1] / C::BY) << 21) | (int64_t)(q[2] / C::BZ);
+    const int64_t in = ((int64_t)q[0] << 42) | ((int64_t)q[1] << 21) | (int64_t)q[2];
+    key[c] = {bk, in};
+  }
+  std::vector<size_t> ord(cells.size());
+  for (size_t c = 0; c < ord.size(); ++c) ord[c] = c;
+  std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return key[a] < key[b]; });
+  std::vector<R> tiles;
+  std::vector<size_t> cur;
+  std::unordered_map<int32_t, int> set;
+  auto blocks_of = [&](const std::vector<size_t> &cs, std::unordered_map<int32_t, int> &m) {
+    for (size_t c : cs) {
+      m.emplace(cells[c].blk, 0);
+      for (int f = 0; f < 6; ++f)
+        if (used(cells[c], f)) m.emplace(cells[c].nb[f], 0);
+    }
+  };
+  auto flush = [&]() {
+    if (cur.empty()) return;
+    R t;
+    std::memset(&t, 0, sizeof(t));
+    std::unordered_map<int32_t, int> slot;
+    int ns = 0;
+    for (size_t c : cur) {
+      slot[cells[c].blk] = ns;
+      t.blk[ns++] = cells[c].blk;
+    }
+    for (int f = 0; f < 6; ++f)
+      for (size_t c : cur) {
+        if (!used(cells[c], f)) continue;
+        const int32_t nb = cells[c].nb[f];
+        if (!slot.count(nb)) {
+          slot[nb] = ns;
+          t.blk[ns++] = nb;
+        }
+      }
+    t.nslot = ns;
+    t.ncell = (int32_t)cur.size();
+    for (size_t l = 0; l < cur.size(); ++l) {
+      const TCell &d = cells[cur[l]];
+      uint32_t sl[6];
+      for (int f = 0; f < 6; ++f) sl[f] = used(d, f) ? (uint32_t)slot[d.nb[f]] : 0xffu;
+      const uint32_t gp = d.gp & 0x3fu, sp = d.sipg & 0x3fu;
+      t.lane_nb[l][0] = sl[0] | (sl[1] << 8) | (sl[2] << 16) | (sl[3] << 24);
+      t.lane_nb[l][1] = sl[4] | (sl[5] << 8) | (gp << 16) | (sp << 24) | ((d.vol ? 1u : 0u) << 30);
+    }
+    for (int l = (int)cur.size(); l < 32; ++l) {
+      t.lane_nb[l][0] = 0xffffffffu;
+      t.lane_nb[l][1] = 0x0000ffffu;
+    }
+    tiles.push_back(t);
+    cur.clear();
+    set.clear();
+  };
+  size_t i = 0;
+  while (i < ord.size()) {
+    size_t j = i;
+    while (j < ord.size() && key[ord[j]].first == key[ord[i]].first) ++j;
+    std::vector<size_t> g(ord.begin() + i, ord.begin() + j);
+    std::unordered_map<int32_t, int> trial = set;
+    blocks_of(g, trial);
+    if (cur.size() + g.size() > 32 || (int)trial.size() > C::SMAX) {
+      flush();
+      trial.clear();
+      blocks_of(g, trial);
+    }
+    cur.insert(cur.end(), g.begin(), g.end());
+    set.swap(trial);
+    i = j;
+  }
+  flush();
+  out.resize(tiles.size() * sizeof(R));
+  if (!tiles.empty()) std::memcpy(out.data(), tiles.data(), out.size());
+}
+
+template <int N>
+int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<UDesc> &ud,
+                const std::vector<CDesc> &cd) {
+  using C = TileCfg<N>;
+  // per part (1 interior, 2 slab boundary): K1 = uncut cells, K2 = GP cells
+  std::vector<TCell> set[2][2];
+  for (int pt = 1; pt <= 2; ++pt) {
+    for (int k = 0; k < 2; ++k)
+      for (int64_t i = hd->r_off[pt][k]; i < hd->r_off[pt][k] + hd->r_cnt[pt][k]; ++i) {
+        const UDesc &d = ud[i];
+        TCell c;
+        c.blk = d.blk;
+        uint32_t nbm = 0;
+        for (int f = 0; f < 6; ++f) {
+          c.nb[f] = d.nb[f];
+          if (d.nb[f] >= 0) nbm |= 1u << f;
+        }
+        c.gp = 0;
+        c.sipg = nbm;  // faces of an uncut cell are inside the domain: full SIPG
+        c.vol = true;
+        set[0][pt - 1].push_back(c);
+        if (d.flags & nbm & 0x3fu) {
+          c.gp = d.flags & nbm & 0x3fu;
+          c.sipg = 0;
+          c.vol = false;
+          set[1][pt - 1].push_back(c);
+        }
+      }
+    for (int64_t i = hd->r_off[pt][2]; i < hd->r_off[pt][2] + hd->r_cnt[pt][2]; ++i) {
+      const CDesc &d = cd[i];
+      TCell c;
+      c.blk = d.blk;
+      uint32_t nbm = 0;
+      for (int f = 0; f < 6; ++f) {
+        c.nb[f] = d.nb[f];
+        if (d.nb[f] >= 0) nbm |= 1u << f;
+      }
+      c.gp = d.flags & nbm & 0x3fu;
+      c.sipg = (d.flags >> 6) & nbm & 0x3fu;  // structured (full, uncut) faces of the cut cell
+      c.vol = false;
+      if (c.gp | c.sipg) set[1][pt - 1].push_back(c);
+    }
+  }
+  const int64_t rs = (int64_t)sizeof(TileRec<C::SMAX>);
+  std::vector<char> all;
+  for (int k = 0; k < 2; ++k) {
+    std::vector<char> b0, b1;
+    build_tiles<N>(set[k][0], pb, b0);
+    build_tiles<N>(set[k][1], pb, b1);
+    hd->t_off[k][0] = hd->t_off[k][1] = (int64_t)all.size() / rs;
+    hd->t_cnt[k][1] = (int64_t)b0.size() / rs;
+    hd->t_off[k][2] = hd->t_off[k][1] + hd->t_cnt[k][1];
+    hd->t_cnt[k][2] = (int64_t)b1.size() / rs;
+    hd->t_cnt[k][0] = hd->t_cnt[k][1] + hd->t_cnt[k][2];
+    all.insert(all.end(), b0.begin(), b0.end());
+    all.insert(all.end(), b1.begin(), b1.end());
+  }
+  int rc = upload(hd, reinterpret_cast<char **>(&hd->d_tiles), all.data(), all.size());
+  if (rc) return rc;
+  hd->ttab.resize(sizeof(TileTab<N>));
+  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
+  if constexpr (N == 4) {
+    using C2 = Tile2Cfg<N>;
+    CU(cudaFuncSetAttribute(k_tile2<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
+    CU(cudaFuncSetAttribute(k_tile2<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_tile2<N, 0>, C2::THREADS, C2::SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_tile2<N, 1>, C2::THREADS, C2::SMEM));
+  } else {
+    CU(cudaFuncSetAttribute(k_tile<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    CU(cudaFuncSetAttribute(k_tile<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_tile<N, 0>, 32, C::SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_tile<N, 1>, 32, C::SMEM));
+  }
+  CU(cudaFuncSetAttribute(k_cutw<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutWCfg<N>::SMEM));
+  for (int k = 0; k < 2; ++k) hd->occ_tile[k] = std::max(1, hd->occ_tile[k]);
+  return 0;
+}
+
+int dispatch_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<UDesc> &ud,
+                   const std::vector<CDesc> &cd) {
+  switch (hd->n) {
+    case 2: return setup_tiles<2>(hd, pb, ud, cd);
+    case 3: return setup_tiles<3>(hd, pb, ud, cd);
+    case 4: return setup_tiles<4>(hd, pb, ud, cd);
+  }
+  return 0;
+}
+
+// N <= 4: the cut kernel (points + cut faces, v = ...) on the side stream
+// concurrently with K1 (uncut cells, v = ...); then K2 (ghost penalty and the
+// cut cells' structured SIPG, v += ...) once both have written.
+template <int N>
+int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which, int part) {
+  constexpr int NT = (N <= 4 ? N : 4);
+  using C = TileCfg<NT>;
+  const int64_t nc = (which & 2) ? hd->r_cnt[part][2] : 0;
+  const int64_t n1 = (which & 1) ? hd->t_cnt[0][part] : 0, n2 = (which & 1) ? hd->t_cnt[1][part] : 0;
+  const bool fork = nc > 0 && n1 > 0;
+  if (nc > 0) {
+    if (fork) {
+      CU(cudaEventRecord(hd->ev_fork, st));
+      CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
+    }
+    using CW = CutWCfg<NT>;
+    const unsigned grid = (unsigned)((nc + CW::WARPS - 1) / CW::WARPS);
+    k_cutw<NT, false><<<grid, 32 * CW::WARPS, CW::SMEM, fork ? hd->side : st>>>(
+        u, v, hd->d_cdesc + hd->r_off[part][2], (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp,
+        hd->d_sfptr, hd->kp, hd->ft);
+    CU(cudaGetLastError());
+  }
+  const TileTab<NT> &tt = *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data());
+  const auto *tl = reinterpret_cast<const TileRec<C::SMAX> *>(hd->d_tiles);
+  auto grid_of = [&](int64_t nt, int k) {
+    return (unsigned)std::min<int64_t>(nt, (int64_t)hd->occ_tile[k] * hd->sm_count);
+  };
+  if (n1 > 0) {
+    const auto *t1 = tl + hd->t_off[0][part];
+    if constexpr (NT == 4)
+      k_tile2<NT, 0><<<grid_of(n1, 0), Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, t1, (int)n1, tt,
+                                                                                        hd->kp.mask);
+    else
+      k_tile<NT, 0><<<grid_of(n1, 0), 32, C::SMEM, st>>>(u, v, t1, (int)n1, tt, hd->kp.mask);
+    CU(cudaGetLastError());
+  }
+  if (fork) {
+    CU(cudaEventRecord(hd->ev_join, hd->side));
+    CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
+  }
+  if (n2 > 0 && (hd->kp.mask & (TERM_GP | TERM_SIPG))) {
+    const auto *t2 = tl + hd->t_off[1][part];
+    if constexpr (NT == 4)
+      k_tile2<NT, 1><<<grid_of(n2, 1), Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, t2, (int)n2, tt,
+                                                                                        hd->kp.mask);
+    else
+      k_tile<NT, 1><<<grid_of(n2, 1), 32, C::SMEM, st>>>(u, v, t2, (int)n2, tt, hd->kp.mask);
+    CU(cudaGetLastError());
+  }
+  return 0;
+}
+
 // which: bit0 structured (uncut) kernels, bit1 unstructured (cut) kernel; part:
 // 0 all owned cells, 1 slab-interior cells, 2 slab-boundary cells.  With both
 // kinds, the cut kernel runs on the forked side stream, concurrently.
 template <int N>
 int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which = 3, int part = 0) {
+  if (N <= 4 && hd->d_tiles) return launch_tiles<N>(hd, u, v, st, which, part);
   const int64_t np = (which & 1) ? hd->r_cnt[part][0] : 0, ng = (which & 1) ? hd->r_cnt[part][1] : 0;
   const int64_t nc = (which & 2) ? hd->r_cnt[part][2] : 0;
   const UDesc *dp = hd->d_udesc + hd->r_off[part][0], *dg = hd->d_udesc + hd->r_off[part][1];
@@ -311,6 +635,7 @@ int dispatch_attrs(int n) {
 void free_handle(cutfem_handle *hd) {
   if (!hd) return;
   cudaFree(hd->d_udesc);
+  cudaFree(hd->d_tiles);
   cudaFree(hd->d_cdesc);
   cudaFree(hd->d_vol);
   cudaFree(hd->d_srf);
@@ -566,6 +891,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   if ((rc = upload(hd, &hd->d_volptr, pb->vol_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_srfptr, pb->srf_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_sfptr, pb->sf_ptr, (size_t)(nsf ? nsf + 1 : 0)))) return rc;
+  if (!std::getenv("CUTFEM_NO_TILE") && (rc = dispatch_tiles(hd, pb, ud, cd))) return rc;
   if ((rc = upload_tables(p))) return rc;
   if ((rc = dispatch_attrs(n))) return rc;
   {
@@ -604,7 +930,8 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   s.n_ext_dofs = na * n * n * n;
   s.degree = p;
   s.device = device;
-  s.launches_per_apply = (hd->n_cut > 0) + (hd->n_plain > 0) + (hd->n_uncut - hd->n_plain > 0);
+  s.launches_per_apply = hd->d_tiles ? (hd->n_cut > 0) + (hd->t_cnt[0][0] > 0) + (hd->t_cnt[1][0] > 0)
+                                     : (hd->n_cut > 0) + (hd->n_plain > 0) + (hd->n_uncut - hd->n_plain > 0);
   return 0;
 }
 

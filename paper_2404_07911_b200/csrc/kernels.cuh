@@ -865,3 +865,4 @@ struct BF {
 };
 
 #include "kernels_fast.cuh"
+#include "kernels_tile.cuh"

@@ -358,7 +358,10 @@ __device__ __forceinline__ void warp_reduce_smem(const double (&a)[L], double *R
   }
 }
 
-template <int N>
+// STRUCT = false: the structured faces of the cut cell (full-face SIPG next to
+// uncut cells, ghost penalty) are left to k_tile*<MODE 1>, which adds them
+// afterwards; this kernel then does the points and the cut faces only.
+template <int N, bool STRUCT = true>
 __global__ void __launch_bounds__(128) k_cutw(const double *__restrict__ u, double *__restrict__ v,
                                               const CDesc *__restrict__ desc, int ncut,
                                               const double *__restrict__ vol_pts,
@@ -387,8 +390,8 @@ __global__ void __launch_bounds__(128) k_cutw(const double *__restrict__ u, doub
 #pragma unroll
   for (int f = 0; f < 6; ++f)
     if (dsc.nb[f] >= 0) nbm |= 1u << f;
-  const uint32_t gpm = gp_on ? (dsc.flags & 0x3fu & nbm) : 0u;
-  const uint32_t ssm = sipg_on ? ((dsc.flags >> 6) & 0x3fu & nbm) : 0u;
+  const uint32_t gpm = (STRUCT && gp_on) ? (dsc.flags & 0x3fu & nbm) : 0u;
+  const uint32_t ssm = (STRUCT && sipg_on) ? ((dsc.flags >> 6) & 0x3fu & nbm) : 0u;
   const uint32_t scm = sipg_on ? ((dsc.flags >> 12) & 0x3fu & nbm) : 0u;
   const uint32_t act = gpm | ssm | scm, stm = gpm | ssm;
 

@@ -1,0 +1,691 @@
+// k_tile<N> (N = p+1 <= 4): structured (uncut) cells, ONE THREAD PER CELL with
+// the whole cell block held in registers (included by kernels.cuh).
+//
+// Why: the line-per-lane kernels sweep every 1-D line through shared memory,
+// i.e. one shared-memory access per FMA; the FP64 pipe needs ~4 FMAs per
+// 8-byte shared access to stay busy (64 DFMA vs 16 doubles per clock per SM),
+// so they saturate shared memory at ~25% of the FP64 peak.  Here the sum
+// factorisation runs entirely on registers; shared memory only supplies the
+// own block once and each neighbour block once per face.
+//
+// Arithmetic (exactly the structured terms of Alg. 1, on a
+// Cartesian cell; the (p+1)-point Gauss rule integrates every product below
+// exactly, so this is algebraically identical to quadrature):
+//   volume     h K1 (x) M (x) M + M (x) h K1 (x) M + M (x) M (x) h K1
+//   SIPG face  h^2 (M (x) M)_in-face  (x)  rank-2 1-D trace operator
+//   face GP    h^2 (M (x) M)_in-face  (x)  G_oo / G_on line operators   (BASELINE configs[0])
+// Every term is (M (x) M (x) M) applied to a sum of 1-D line operators along
+// one axis each, premultiplied by M^{-1} on that axis:
+//   v = (M (x) M (x) M) w,  w = sum_d [ (M^{-1} h K1)_d u + face terms_d ],
+// so a cell costs 3 "line-operator" sweeps + the face traces + 3 mass sweeps
+// (6 n^4 FMAs + O(n^3) per face), all with warp-uniform coefficients from the
+// kernel parameter block (constant-bank operands).
+//
+// Data movement: a warp owns a tile of <= 32 uncut cells (a 2x4x4 brick of the
+// background grid, partial bricks merged; built on the host).  All blocks the
+// tile touches (its cells, then the face-neighbour halo) are copied by TMA bulk
+// copies (cp.async.bulk + mbarrier complete_tx, SASS UBLKCP) into padded
+// shared-memory slots (stride chosen so 16-byte per-lane reads of 32 different
+// slots are bank-conflict free), the result is written back into the cell's
+// own slot and stored by a bulk shared->global copy.  Each v block is written
+// once, no atomics.  Odd n (blocks not 16-byte multiples) uses coalesced
+// LDG/STS staging instead of bulk copies.
+#pragma once
+#ifndef T2MINB
+#define T2MINB 1
+#endif
+#ifndef T1MINB
+#define T1MINB 1
+#endif
+
+template <int N>
+struct TileCfg {
+  static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
+  static constexpr int N3 = N * N * N;
+  static constexpr int ST = N == 2 ? 10 : (N == 3 ? 27 : 66);  // slot stride (doubles)
+  static constexpr int SMAX = N == 4 ? 100 : 128;             // slots per tile
+  static constexpr int SMEM = 16 + SMAX * ST * 8;
+  static constexpr int BX = 2, BY = 4, BZ = 4;  // brick of the background grid
+};
+
+// One warp-tile.  lane_nb[l] = {slot of faces 0..3 (bytes), slot of faces 4,5
+// (bytes 0,1) | ghost-penalty face bits << 16}; slot 255 = no neighbour.  Lane l
+// computes the cell in slot l (l < ncell).
+template <int SMAX>
+struct __align__(16) TileRec {
+  int32_t nslot, ncell, pad0, pad1;
+  uint32_t lane_nb[32][2];
+  int32_t blk[SMAX];
+};
+
+// Per-handle line operators (h, penalties folded), all warp-uniform.  Only the
+// lo-face (s = 0) variants are stored: every 1-D operator here is
+// centro-symmetric (GLL nodes and Gauss points are symmetric about 1/2), so the
+// hi face uses the reversed entries:  l'_a(1) = -l'_{n-1-a}(0),
+// cJ_hi[m] = cJ_lo[n-1-m], cA_hi[m] = -cA_lo[n-1-m], G_hi[m][a] = G_lo[n-1-m][n-1-a],
+// and L, M satisfy X[i][j] = X[n-1-i][n-1-j].  Reading only the canonical half
+// keeps ~20 distinct constants live next to the 64-double accumulator.
+template <int N>
+struct TileTab {
+  double L[N * N];    // M^{-1} h K1: volume term along one axis
+  double M[N * N];    // GLL mass M1
+  double d0[N];       // l'_a(0)
+  double cJ[N];       // SIPG (lo face): w_line += cJ [u] + cA (d u_own + d u_nb)
+  double cA[N];
+  double Goo[N * N];  // ghost penalty (lo face), own line:        M^{-1} G_oo
+  double Gon[N * N];  // ghost penalty (lo face), neighbour line: -M^{-1} G_on
+};
+
+// canonical index of a centro-symmetric n x n matrix entry
+template <int N>
+__device__ __forceinline__ constexpr int csym(int k) {
+  return k < N * N - 1 - k ? k : N * N - 1 - k;
+}
+
+// position m along axis D of line t (t = t0 + N t1 over the two other axes, ascending)
+template <int N, int D>
+__device__ __forceinline__ constexpr int lix(int t, int m) {
+  return D == 0 ? (m + N * (t % N) + N * N * (t / N))
+                : (D == 1 ? ((t % N) + N * m + N * N * (t / N)) : ((t % N) + N * (t / N) + N * N * m));
+}
+
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
+// SIPG contribution of face (D, S) to line t from the own line uo[] and the
+// neighbour's line un[]; en = 1 (face present) or 0 (no face: un is a dummy).
+template <int N, int D, int S, int W>
+__device__ __forceinline__ void sipg_line(double (&w)[W], int t, const double (&uo)[N], const double (&un)[N],
+                                          double en, const TileTab<N> &tt) {
+  double A0 = 0.0, A1 = 0.0;
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    if (S == 0) {  // own l'(0), neighbour l'(1) = -l'_{n-1-m}(0)
+      A0 = fma(tt.d0[m], uo[m], A0);
+      A1 = fma(-tt.d0[N - 1 - m], un[m], A1);
+    } else {       // own l'(1), neighbour l'(0)
+      A0 = fma(-tt.d0[N - 1 - m], uo[m], A0);
+      A1 = fma(tt.d0[m], un[m], A1);
+    }
+  }
+  const double J = en * (S ? (uo[N - 1] - un[0]) : (uo[0] - un[N - 1]));
+  const double A = en * (A0 + A1);
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    double &r = w[lix<N, D>(t, m)];
+    if (S == 0) r = fma(tt.cJ[m], J, fma(tt.cA[m], A, r));
+    else r = fma(tt.cJ[N - 1 - m], J, fma(-tt.cA[N - 1 - m], A, r));
+  }
+}
+
+// ghost penalty of face S on a line: rows [R0, R1) of the line operator, output
+// row m written to w[wi(m)]
+template <int N, int S, int R0, int R1, class WI, int W>
+__device__ __forceinline__ void gp_rows(double (&w)[W], WI wi, const double (&uo)[N], const double (&un)[N],
+                                        double eg, const TileTab<N> &tt) {
+#pragma unroll
+  for (int m = R0; m < R1; ++m) {
+    double r = 0.0;
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      const int k = S ? (N - 1 - m) * N + (N - 1 - a) : m * N + a;
+      r = fma(tt.Goo[k], uo[a], fma(tt.Gon[k], un[a], r));
+    }
+    w[wi(m)] = fma(eg, r, w[wi(m)]);
+  }
+}
+
+// Load line t along D of the block at B (shared memory), 16-byte words where
+// the line is contiguous (D = 0, even N).
+template <int N, int D>
+__device__ __forceinline__ void ld_line(const double *B, int t, double (&a)[N]) {
+  if constexpr ((N % 2) == 0 && D == 0) {
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) {
+      const double2 x = *reinterpret_cast<const double2 *>(B + lix<N, 0>(t, 2 * k));
+      a[2 * k] = x.x;
+      a[2 * k + 1] = x.y;
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < N; ++m) a[m] = B[lix<N, D>(t, m)];
+  }
+}
+// Lines t and t+1 (t0 even, D != 0, even N) share 16-byte words.
+template <int N, int D>
+__device__ __forceinline__ void ld_pair(const double *B, int t, double (&a)[N], double (&b)[N]) {
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    const double2 x = *reinterpret_cast<const double2 *>(B + lix<N, D>(t, m));
+    a[m] = x.x;
+    b[m] = x.y;
+  }
+}
+
+template <int N, int D, int W>
+__device__ __forceinline__ void vol_line(double (&w)[W], int t, const double (&uo)[N], double ev,
+                                         const TileTab<N> &tt) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double r = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) r = fma(tt.L[csym<N>(i * N + j)], uo[j], r);
+    w[lix<N, D>(t, i)] = fma(ev, r, w[lix<N, D>(t, i)]);
+  }
+}
+
+// Axis D: volume line operator and SIPG on both faces for every line (branch
+// free: a missing face reads a dummy line and is scaled by 0), then the
+// ghost-penalty faces of this axis (rare: only next to cut cells).
+template <int N, int D>
+__device__ __forceinline__ void axis_all(double (&w)[N * N * N], const double *Us, const double *Nl, const double *Nh,
+                                         double ev, double el, double eh, const TileTab<N> &tt) {
+  constexpr int NN = N * N;
+  if constexpr ((N % 2) == 0 && D != 0) {
+#pragma unroll
+    for (int t = 0; t < NN; t += 2) {
+      double u0[N], u1[N], a0[N], a1[N];
+      ld_pair<N, D>(Us, t, u0, u1);
+      vol_line<N, D>(w, t, u0, ev, tt);
+      vol_line<N, D>(w, t + 1, u1, ev, tt);
+      ld_pair<N, D>(Nl, t, a0, a1);
+      sipg_line<N, D, 0>(w, t, u0, a0, el, tt);
+      sipg_line<N, D, 0>(w, t + 1, u1, a1, el, tt);
+      ld_pair<N, D>(Nh, t, a0, a1);
+      sipg_line<N, D, 1>(w, t, u0, a0, eh, tt);
+      sipg_line<N, D, 1>(w, t + 1, u1, a1, eh, tt);
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < NN; ++t) {
+      double u0[N], a0[N];
+      ld_line<N, D>(Us, t, u0);
+      vol_line<N, D>(w, t, u0, ev, tt);
+      ld_line<N, D>(Nl, t, a0);
+      sipg_line<N, D, 0>(w, t, u0, a0, el, tt);
+      ld_line<N, D>(Nh, t, a0);
+      sipg_line<N, D, 1>(w, t, u0, a0, eh, tt);
+    }
+  }
+}
+
+// MODE 0 / 1 as for k_tile2 below (volume + SIPG, v = ... / ghost penalty +
+// structured SIPG of cut cells, v += ...).
+template <int N, int MODE>
+__global__ void __launch_bounds__(32, T1MINB) k_tile(const double *__restrict__ u, double *__restrict__ v,
+                                                     const TileRec<TileCfg<N>::SMAX> *__restrict__ tiles,
+                                                     int ntiles, TileTab<N> tt, uint32_t mask) {
+  using C = TileCfg<N>;
+  constexpr int NN = N * N, N3 = NN * N, ST = C::ST;
+  extern __shared__ __align__(16) double smem[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  double *S = smem + 2;
+  const int lane = threadIdx.x;
+  const bool cell_on = (mask & TERM_CELL) != 0, sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
+  if (C::BULK && lane == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  uint32_t it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const TileRec<C::SMAX> *T = tiles + tile;
+    const int nslot = T->nslot, ncell = T->ncell;
+    const uint2 ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[lane][0]);
+    const int myblk = lane < ncell ? T->blk[lane] : 0;
+    const bool on = lane < ncell;
+    // ---- stage the tile's blocks (own cells first, then the halo)
+    if constexpr (C::BULK) {
+      bulk_wait_read0();     // previous tile's v stores have left shared memory
+      fence_proxy_async();   // ... and so have this lane's generic reads
+      __syncwarp();
+      if (lane == 0) mbar_expect_tx(bar, (uint32_t)(nslot * N3 * 8));
+      __syncwarp();
+      for (int s = lane; s < nslot; s += 32) bulk_g2s(S + s * ST, u + (size_t)T->blk[s] * N3, N3 * 8, bar);
+      mbar_wait(bar, it & 1);
+    } else {
+      __syncwarp();
+      for (int s0 = 0; s0 < nslot; s0 += 32) {
+        const int bl = (s0 + lane < nslot) ? T->blk[s0 + lane] : 0;
+        const int cnt = min(32, nslot - s0);
+#pragma unroll 4
+        for (int j = 0; j < cnt; ++j) {
+          const int b = __shfl_sync(0xffffffffu, bl, j);
+          if (lane < N3) S[(s0 + j) * ST + lane] = __ldg(u + (size_t)b * N3 + lane);
+        }
+      }
+      __syncwarp();
+    }
+    double w[N3];
+#pragma unroll
+    for (int l = 0; l < N3; ++l) w[l] = 0.0;
+    if (on) {
+      const double *Us = S + lane * ST;
+      int nbs[6];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) nbs[f] = (ln.x >> (8 * f)) & 0xff;
+      nbs[4] = ln.y & 0xff;
+      nbs[5] = (ln.y >> 8) & 0xff;
+      const uint32_t gpb = gp_on ? (ln.y >> 16) & 0x3fu : 0u, spb = sipg_on ? (ln.y >> 24) & 0x3fu : 0u;
+      const bool vol = ((ln.y >> 30) & 1u) && cell_on;
+      static_for<0, 3>([&](auto dc) {
+        constexpr int D = decltype(dc)::value;
+        const double *Nl = nbs[2 * D] != 0xff ? S + nbs[2 * D] * ST : Us;  // dummy line source when absent
+        const double *Nh = nbs[2 * D + 1] != 0xff ? S + nbs[2 * D + 1] * ST : Us;
+        const double el = ((spb >> (2 * D)) & 1u) ? 1.0 : 0.0, eh = ((spb >> (2 * D + 1)) & 1u) ? 1.0 : 0.0;
+        if constexpr (MODE == 0) {
+          axis_all<N, D>(w, Us, Nl, Nh, vol ? 1.0 : 0.0, el, eh, tt);
+        } else {
+          const double gl = ((gpb >> (2 * D)) & 1u) ? 1.0 : 0.0, gh = ((gpb >> (2 * D + 1)) & 1u) ? 1.0 : 0.0;
+#pragma unroll
+          for (int t = 0; t < NN; ++t) {
+            double uo[N], a0[N], a1[N];
+            ld_line<N, D>(Us, t, uo);
+            ld_line<N, D>(Nl, t, a0);
+            ld_line<N, D>(Nh, t, a1);
+            sipg_line<N, D, 0>(w, t, uo, a0, el, tt);
+            sipg_line<N, D, 1>(w, t, uo, a1, eh, tt);
+            gp_rows<N, 0, 0, N>(w, [&](int m) { return lix<N, D>(t, m); }, uo, a0, gl, tt);
+            gp_rows<N, 1, 0, N>(w, [&](int m) { return lix<N, D>(t, m); }, uo, a1, gh, tt);
+          }
+        }
+      });
+      // v = (M (x) M (x) M) w
+      static_for<0, 3>([&](auto dc) {
+        constexpr int D = decltype(dc)::value;
+#pragma unroll
+        for (int t = 0; t < NN; ++t) {
+          double x[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            double r = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) r = fma(tt.M[csym<N>(i * N + j)], w[lix<N, D>(t, j)], r);
+            x[i] = r;
+          }
+#pragma unroll
+          for (int i = 0; i < N; ++i) w[lix<N, D>(t, i)] = x[i];
+        }
+      });
+    }
+    __syncwarp();  // every lane is done reading the tile's slots
+    if constexpr (MODE == 1) {
+      if (on)
+#pragma unroll
+        for (int l = 0; l < N3; ++l) w[l] += v[(size_t)myblk * N3 + l];
+    }
+    // ---- write back: own slot, then one bulk store per cell
+    if (on) {
+      double *Us = S + lane * ST;
+      if constexpr ((N % 2) == 0) {
+#pragma unroll
+        for (int l = 0; l < N3; l += 2) *reinterpret_cast<double2 *>(Us + l) = make_double2(w[l], w[l + 1]);
+      } else {
+#pragma unroll
+        for (int l = 0; l < N3; ++l) Us[l] = w[l];
+      }
+    }
+    if constexpr (C::BULK) {
+      fence_proxy_async();
+      if (on) {
+        bulk_s2g(v + (size_t)myblk * N3, S + lane * ST, N3 * 8);
+        bulk_commit();
+      }
+    } else {
+      __syncwarp();
+      for (int c = 0; c < ncell; ++c) {
+        const int b = __shfl_sync(0xffffffffu, myblk, c);
+        if (lane < N3) v[(size_t)b * N3 + lane] = S[c * ST + lane];
+      }
+      __syncwarp();
+    }
+  }
+  if constexpr (C::BULK) bulk_wait0();
+}
+
+// ===================================================================== k_tile2
+// k_tile2<N> (N = 4): the same arithmetic with TWO threads per cell, because a
+// 64-double accumulator plus in-flight lines does not fit 255 registers.
+// Thread (cell, h) owns the P = N/2 z-planes of its half, and works in the
+// z-MIRRORED frame when h = 1 (z -> N-1-z): every operator is invariant under
+// the reflection (GLL/Gauss symmetric, SIPG/GP reflection-invariant), so both
+// halves run the same instructions with the same warp-uniform coefficients
+// (rows 0..P-1 of the z-line operators), only the shared-memory addresses
+// differ.  x/y terms are plane-local.  z terms: each thread evaluates its own
+// (mirrored-lo) z face's traces [u], {d_z u} and swaps them with its partner
+// (__shfl_xor 16; the partner's A changes sign with the frame), and the final
+// z mass sweep swaps the partner's planes the same way.  Lanes l and l^16 are
+// the two halves of cell 16*warp + (l & 15), so every 8-lane quarter of a warp
+// reads 8 different slots (16-byte reads, slot stride 33 x 16 B: conflict free).
+template <int N>
+struct Tile2Cfg {
+  static constexpr int P = N / 2, NN = N * N, N3 = N * NN, NP = NN * P;
+  static constexpr int ST = TileCfg<N>::ST, SMAX = TileCfg<N>::SMAX;
+  static constexpr int SMEM = TileCfg<N>::SMEM;
+  static constexpr int THREADS = 64;
+};
+
+// x or y (D = 0, 1) terms of plane cc (pointers already at the plane)
+template <int N, int D, int W>
+__device__ __forceinline__ void axis_plane(double (&w)[W], const double *Up, const double *Lp, const double *Hp,
+                                           int cc, double ev, double el, double eh, const TileTab<N> &tt) {
+  if constexpr (D == 1 && (N % 2) == 0) {
+#pragma unroll
+    for (int q = 0; q < N; q += 2) {
+      double u0[N], u1[N], a0[N], a1[N];
+      ld_pair<N, D>(Up, q, u0, u1);
+      vol_line<N, D>(w, q + N * cc, u0, ev, tt);
+      vol_line<N, D>(w, q + 1 + N * cc, u1, ev, tt);
+      ld_pair<N, D>(Lp, q, a0, a1);
+      sipg_line<N, D, 0>(w, q + N * cc, u0, a0, el, tt);
+      sipg_line<N, D, 0>(w, q + 1 + N * cc, u1, a1, el, tt);
+      ld_pair<N, D>(Hp, q, a0, a1);
+      sipg_line<N, D, 1>(w, q + N * cc, u0, a0, eh, tt);
+      sipg_line<N, D, 1>(w, q + 1 + N * cc, u1, a1, eh, tt);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double u0[N], a0[N];
+      ld_line<N, D>(Up, q, u0);
+      vol_line<N, D>(w, q + N * cc, u0, ev, tt);
+      ld_line<N, D>(Lp, q, a0);
+      sipg_line<N, D, 0>(w, q + N * cc, u0, a0, el, tt);
+      ld_line<N, D>(Hp, q, a0);
+      sipg_line<N, D, 1>(w, q + N * cc, u0, a0, eh, tt);
+    }
+  }
+}
+
+// z-line t = a + N b read in the thread's frame: position m at zb + zs*m
+template <int N>
+__device__ __forceinline__ void ld_zpair(const double *B, int t, int zb, int zs, double (&a)[N], double (&b)[N]) {
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    const double2 x = *reinterpret_cast<const double2 *>(B + t + zb + zs * m);
+    a[m] = x.x;
+    b[m] = x.y;
+  }
+}
+
+// z terms of line t for the P own planes: volume rows 0..P-1, the own
+// (mirrored-lo) face traces, their exchange with the partner, the SIPG spread
+// of both faces; ghost penalty of either face if flagged.
+template <int N, int W>
+__device__ __forceinline__ void z_line(double (&w)[W], int t, const double (&uo)[N], const double (&ul)[N],
+                                       double ev, double el, unsigned act, const TileTab<N> &tt) {
+  constexpr int P = N / 2, NN = N * N;
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    double r = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) r = fma(tt.L[csym<N>(c * N + j)], uo[j], r);
+    w[t + NN * c] = fma(ev, r, w[t + NN * c]);
+  }
+  double A0 = 0.0, A1 = 0.0;
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    A0 = fma(tt.d0[m], uo[m], A0);
+    A1 = fma(-tt.d0[N - 1 - m], ul[m], A1);
+  }
+  const double Jl = el * (uo[0] - ul[N - 1]);
+  const double Al = el * (A0 + A1);
+  const double Jh = __shfl_xor_sync(act, Jl, 16);
+  const double Ah = -__shfl_xor_sync(act, Al, 16);
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    double &r = w[t + NN * c];
+    r = fma(tt.cJ[c], Jl, fma(tt.cA[c], Al, r));
+    r = fma(tt.cJ[N - 1 - c], Jh, fma(-tt.cA[N - 1 - c], Ah, r));
+  }
+}
+
+// z SIPG of face S (own frame) on line t, rows 0..P-1 only (both faces known)
+template <int N, int S, int W>
+__device__ __forceinline__ void zsipg_line(double (&w)[W], int t, const double (&uo)[N], const double (&un)[N],
+                                           double en, const TileTab<N> &tt) {
+  constexpr int P = N / 2, NN = N * N;
+  double A0 = 0.0, A1 = 0.0;
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    if (S == 0) {
+      A0 = fma(tt.d0[m], uo[m], A0);
+      A1 = fma(-tt.d0[N - 1 - m], un[m], A1);
+    } else {
+      A0 = fma(-tt.d0[N - 1 - m], uo[m], A0);
+      A1 = fma(tt.d0[m], un[m], A1);
+    }
+  }
+  const double J = en * (S ? (uo[N - 1] - un[0]) : (uo[0] - un[N - 1]));
+  const double A = en * (A0 + A1);
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    double &r = w[t + NN * c];
+    if (S == 0) r = fma(tt.cJ[c], J, fma(tt.cA[c], A, r));
+    else r = fma(tt.cJ[N - 1 - c], J, fma(-tt.cA[N - 1 - c], A, r));
+  }
+}
+
+// Per-lane tile record fields (prefetched one tile ahead)
+struct TileLane {
+  int nslot, ncell, myblk, b0, b1;
+  uint2 ln;
+};
+template <int SMAX>
+__device__ __forceinline__ TileLane tile_lane(const TileRec<SMAX> *T, int cell, int tid, int nthr) {
+  TileLane r;
+  r.nslot = T->nslot;
+  r.ncell = T->ncell;
+  r.ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[cell][0]);
+  r.myblk = cell < r.ncell ? T->blk[cell] : 0;
+  r.b0 = tid < r.nslot ? T->blk[tid] : 0;
+  r.b1 = tid + nthr < r.nslot ? T->blk[tid + nthr] : 0;
+  return r;
+}
+
+// MODE 0: volume (per-lane bit) + SIPG (per-face bits) of uncut cells, v = result.
+// MODE 1: ghost penalty (per-face bits) + SIPG (per-face bits: the structured
+//         faces of cut cells), v += result.
+// Lane flags: lane_nb[l][1] byte 2 = GP faces, byte 3 = SIPG faces | volume << 6.
+template <int N, int MODE>
+__global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__ u, double *__restrict__ v,
+                                                      const TileRec<Tile2Cfg<N>::SMAX> *__restrict__ tiles,
+                                                      int ntiles, TileTab<N> tt, uint32_t mask) {
+  static_assert(N % 2 == 0, "k_tile2 needs even N");
+  using C = Tile2Cfg<N>;
+  constexpr int P = C::P, NN = C::NN, N3 = C::N3, NP = C::NP, ST = C::ST;
+  static_assert(C::SMAX <= 2 * C::THREADS, "two slot copies per thread");
+  extern __shared__ __align__(16) double smem[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);  // [0] tile blocks, [1] v blocks (MODE 1)
+  double *S = smem + 2;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int cell = 16 * (tid >> 5) + (lane & 15), h = lane >> 4;
+  const bool cell_on = (mask & TERM_CELL) != 0, sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
+  // the thread's frame: plane cc of the half is physical plane zb + zs cc; z position m at zb + zs m
+  const int zb = h ? NN * (N - 1) : 0, zs = h ? -NN : NN;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  TileLane nx;
+  if ((int)blockIdx.x < ntiles) nx = tile_lane(tiles + blockIdx.x, cell, tid, C::THREADS);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const TileLane cu = nx;
+    const bool on = cell < cu.ncell;
+    if (h == 0) bulk_wait_read0();  // this thread's previous v store has left shared memory
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) mbar_expect_tx(bar, (uint32_t)(cu.nslot * N3 * 8));
+    __syncthreads();
+    if (tid < cu.nslot) bulk_g2s(S + tid * ST, u + (size_t)cu.b0 * N3, N3 * 8, bar);
+    if (tid + C::THREADS < cu.nslot) bulk_g2s(S + (tid + C::THREADS) * ST, u + (size_t)cu.b1 * N3, N3 * 8, bar);
+    if (tile + (int)gridDim.x < ntiles) nx = tile_lane(tiles + tile + gridDim.x, cell, tid, C::THREADS);
+    mbar_wait(bar, it & 1);
+    const unsigned act = __ballot_sync(0xffffffffu, on);
+    double w[NP];
+#pragma unroll
+    for (int l = 0; l < NP; ++l) w[l] = 0.0;
+    int nbs[6];
+    uint32_t gpb = (cu.ln.y >> 16) & 0x3fu, spb = (cu.ln.y >> 24) & 0x3fu;
+    const bool vol = ((cu.ln.y >> 30) & 1u) && cell_on;
+    if (!gp_on) gpb = 0;
+    if (!sipg_on) spb = 0;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) nbs[f] = (cu.ln.x >> (8 * f)) & 0xff;
+    nbs[4] = cu.ln.y & 0xff;
+    nbs[5] = (cu.ln.y >> 8) & 0xff;
+    if (h) {  // mirrored frame: the z faces swap
+      const int x = nbs[4];
+      nbs[4] = nbs[5];
+      nbs[5] = x;
+      gpb = (gpb & 0xfu) | (((gpb >> 4) & 1u) << 5) | (((gpb >> 5) & 1u) << 4);
+      spb = (spb & 0xfu) | (((spb >> 4) & 1u) << 5) | (((spb >> 5) & 1u) << 4);
+    }
+    if (!on) gpb = spb = 0;
+    const double *Us = S + cell * ST;
+    const double *Nb[6];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) Nb[f] = nbs[f] != 0xff ? S + nbs[f] * ST : Us;  // dummy source when absent
+    if (on || MODE == 1) {
+      if constexpr (MODE == 0) {
+        const double ev = vol ? 1.0 : 0.0;
+        // x and y: plane-local
+        static_for<0, 2>([&](auto dc) {
+          constexpr int D = decltype(dc)::value;
+          const double el = ((spb >> (2 * D)) & 1u) ? 1.0 : 0.0, eh = ((spb >> (2 * D + 1)) & 1u) ? 1.0 : 0.0;
+#pragma unroll
+          for (int cc = 0; cc < P; ++cc) {
+            const int pz = zb + zs * cc;
+            axis_plane<N, D>(w, Us + pz, Nb[2 * D] + pz, Nb[2 * D + 1] + pz, cc, ev, el, eh, tt);
+          }
+        });
+        // z: the own (mirrored-lo) face; the other face's traces come from the partner
+        const double el = ((spb >> 4) & 1u) ? 1.0 : 0.0;
+#pragma unroll
+        for (int t = 0; t < NN; t += 2) {
+          double u0[N], u1[N], a0[N], a1[N];
+          ld_zpair<N>(Us, t, zb, zs, u0, u1);
+          ld_zpair<N>(Nb[4], t, zb, zs, a0, a1);
+          z_line<N>(w, t, u0, a0, ev, el, act, tt);
+          z_line<N>(w, t + 1, u1, a1, ev, el, act, tt);
+        }
+      } else {
+        // ghost penalty + structured SIPG, face by face (skipped when no lane of the warp has it)
+        static_for<0, 6>([&](auto fc) {
+          constexpr int F = decltype(fc)::value, D = F / 2, SS = F % 2;
+          const bool g = (gpb >> F) & 1u, sp = (spb >> F) & 1u;
+          const bool anyg = __any_sync(0xffffffffu, g), anys = __any_sync(0xffffffffu, sp);
+          if (!(anyg || anys)) return;
+          const double eg = g ? 1.0 : 0.0, es = sp ? 1.0 : 0.0;
+          const double *Nf = Nb[F];
+          if constexpr (D < 2) {
+#pragma unroll
+            for (int cc = 0; cc < P; ++cc) {
+              const int pz = zb + zs * cc;
+#pragma unroll
+              for (int q = 0; q < N; ++q) {
+                double uo[N], un[N];
+                ld_line<N, D>(Us + pz, q, uo);
+                ld_line<N, D>(Nf + pz, q, un);
+                if (anys) sipg_line<N, D, SS>(w, q + N * cc, uo, un, es, tt);
+                if (anyg)
+                  gp_rows<N, SS, 0, N>(w, [&](int m) { return lix<N, D>(q + N * cc, m); }, uo, un, eg, tt);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < NN; t += 2) {
+              double u0[N], u1[N], a0[N], a1[N];
+              ld_zpair<N>(Us, t, zb, zs, u0, u1);
+              ld_zpair<N>(Nf, t, zb, zs, a0, a1);
+              if (anys) {
+                zsipg_line<N, SS>(w, t, u0, a0, es, tt);
+                zsipg_line<N, SS>(w, t + 1, u1, a1, es, tt);
+              }
+              if (anyg) {
+                gp_rows<N, SS, 0, P>(w, [&](int m) { return t + NN * m; }, u0, a0, eg, tt);
+                gp_rows<N, SS, 0, P>(w, [&](int m) { return t + 1 + NN * m; }, u1, a1, eg, tt);
+              }
+            }
+          }
+        });
+      }
+    }
+    __syncthreads();  // every thread is done reading the tile's blocks
+    if constexpr (MODE == 1) {  // fetch the v blocks of the tile's cells into their slots
+      if (tid == 0) mbar_expect_tx(bar + 1, (uint32_t)(cu.ncell * N3 * 8));
+      __syncthreads();
+      if (on && h == 0) bulk_g2s(S + cell * ST, v + (size_t)cu.myblk * N3, N3 * 8, bar + 1);
+    }
+    if (on) {
+      // v = (M (x) M (x) M) w: x and y sweeps on the own planes ...
+      static_for<0, 2>([&](auto dc) {
+        constexpr int D = decltype(dc)::value;
+#pragma unroll
+        for (int t = 0; t < N * P; ++t) {
+          double x[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            double r = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) r = fma(tt.M[csym<N>(i * N + j)], w[lix<N, D>(t, j)], r);
+            x[i] = r;
+          }
+#pragma unroll
+          for (int i = 0; i < N; ++i) w[lix<N, D>(t, i)] = x[i];
+        }
+      });
+      // ... and z with the partner's planes (its plane c sits at position N-1-c of our frame)
+#pragma unroll
+      for (int t = 0; t < NN; ++t) {
+        double yp[P], x[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) yp[c] = __shfl_xor_sync(act, w[t + NN * c], 16);
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+          double r = 0.0;
+#pragma unroll
+          for (int c = 0; c < P; ++c) {
+            r = fma(tt.M[csym<N>(i * N + c)], w[t + NN * c], r);
+            r = fma(tt.M[csym<N>(i * N + N - 1 - c)], yp[c], r);
+          }
+          x[i] = r;
+        }
+#pragma unroll
+        for (int i = 0; i < P; ++i) w[t + NN * i] = x[i];
+      }
+    }
+    if constexpr (MODE == 1) mbar_wait(bar + 1, it & 1);
+    if (on) {
+      double *Uw = S + cell * ST;
+#pragma unroll
+      for (int c = 0; c < P; ++c)
+#pragma unroll
+        for (int t = 0; t < NN; t += 2) {
+          double2 *q = reinterpret_cast<double2 *>(Uw + zb + zs * c + t);
+          if constexpr (MODE == 1) {
+            const double2 o = *q;
+            *q = make_double2(o.x + w[t + NN * c], o.y + w[t + 1 + NN * c]);
+          } else {
+            *q = make_double2(w[t + NN * c], w[t + 1 + NN * c]);
+          }
+        }
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (on && h == 0) {
+      bulk_s2g(v + (size_t)cu.myblk * N3, S + cell * ST, N3 * 8);
+      bulk_commit();
+    }
+  }
+  if (h == 0) bulk_wait0();
+}

@@ -54,7 +54,8 @@ __device__ __forceinline__ void sipg_fields(const double *U, const double *NBf, 
   FB[N * N + t] = -sg * kp.hh * J0;
 }
 
-template <int N, bool PLAIN>
+// ACC: v += result (the ghost-penalty pass after k_tile / k_tile2, mask = GP)
+template <int N, bool PLAIN, bool ACC = false>
 __global__ void __launch_bounds__(128) k_uncut3(const double *__restrict__ u, double *__restrict__ v,
                                                 const UDesc *__restrict__ desc, int ncell, KParams kp,
                                                 FaceTab ft) {
@@ -313,7 +314,10 @@ __global__ void __launch_bounds__(128) k_uncut3(const double *__restrict__ u, do
     // ---------------- write the block, then reuse this buffer set for cell + 2S
     {
       double *vb = v + (size_t)d.blk * N3;
-      for (int l = t; l < N3; l += LPS) vb[l] = Rb[B::pad(l)];
+      if (ACC)
+        for (int l = t; l < N3; l += LPS) vb[l] += Rb[B::pad(l)];
+      else
+        for (int l = t; l < N3; l += LPS) vb[l] = Rb[B::pad(l)];
     }
     __syncwarp(mask);
     if (cell + 2 * S < ncell) {

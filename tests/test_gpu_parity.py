@@ -229,3 +229,27 @@ def test_full_size_sampled_blocks(cf, cutgen_mod, cfg):
     wd = torch.from_numpy(P.seeded_u(2)).cuda()
     a, b = float(wd @ op.apply(ud)), float(ud @ op.apply(wd))
     assert abs(a - b) <= 1e-11 * abs(a)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_sphere16_tiles(cf, cutgen_mod, p):
+    """A mesh with many warp-tiles (full and partial bricks, plain cells, ghost-
+    penalty cells, cut cells with structured faces): whole operator and the
+    face terms alone."""
+    P = cutgen_mod.generate(cutgen_mod.SPHERE, 16, -1.0, 1.0, p)
+    u = P.seeded_u(10 + p)
+    v, op = gpu_apply(cf, P, u)
+    assert op.stats()["n_uncut"] > 400
+    check(P, v, u)
+    for mask in (2, 8):
+        v, _ = gpu_apply(cf, P, u, mask)
+        check(P, v, u, mask)
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_gyroid_box_boundary(cf, cutgen_mod, p):
+    """Gyroid in [0,1]^3: uncut cells on the box boundary (missing faces)."""
+    P = cutgen_mod.generate(cutgen_mod.GYROID, 8, 0.0, 1.0, p)
+    u = P.seeded_u(21)
+    v, _ = gpu_apply(cf, P, u)
+    check(P, v, u)
