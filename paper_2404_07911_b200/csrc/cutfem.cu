@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <queue>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -73,6 +74,14 @@ struct cutfem_handle {
   int64_t t_off[2][3] = {{0}}, t_cnt[2][3] = {{0}};
   int occ_tile[2] = {1, 1};
   std::vector<char> ttab;  // TileTab<N> bytes
+  CDesc2 *d_cdesc2 = nullptr;  // k_cutp: cut cells grouped per warp (LPT), their cut-face points
+  double *d_fac = nullptr;
+  int *d_wstart = nullptr;      // per part: warp -> first cell (grid_cutp[part] * WARPS + 1 entries)
+  int *d_kstart = nullptr;      // per part: warp -> first point chunk
+  CChunk *d_chunks = nullptr;   // point-chunk plan, per warp in consumption order
+  int64_t w_off[3] = {0};
+  int grid_cutp[3] = {0};
+  int occ_cutp = 1;
   UDesc *d_udesc = nullptr;
   CDesc *d_cdesc = nullptr;
   double *d_vol = nullptr, *d_srf = nullptr, *d_sfp = nullptr;
@@ -137,6 +146,24 @@ int upload_tables(int p) {
     t.gw[a] = (double)r.w[a];
     t.d0[a] = (double)r.tr[(1 * 2 + 0) * n + a];
     t.d1[a] = (double)r.tr[(1 * 2 + 1) * n + a];
+  }
+  // monomial coefficients of l_a in t = 2x - 1 (product expansion in long double)
+  for (int a = 0; a < n; ++a) {
+    std::vector<long double> c(1, 1.0L);
+    for (int m = 0; m < n; ++m) {
+      if (m == a) continue;
+      const long double tm = 2 * r.x[m] - 1, den = (2 * r.x[a] - 1) - tm;
+      std::vector<long double> d(c.size() + 1, 0.0L);
+      for (size_t k = 0; k < c.size(); ++k) {
+        d[k + 1] += c[k] / den;
+        d[k] -= c[k] * tm / den;
+      }
+      c.swap(d);
+    }
+    for (int k = 0; k < n; ++k) {
+      t.mc[a][k] = (double)c[k];
+      t.md[a][k] = (double)(2 * k * c[k]);
+    }
   }
   CU(cudaMemcpyToSymbol(c_ref, &t, sizeof(RefTab), sizeof(RefTab) * (n - 2)));
   return 0;
@@ -396,6 +423,107 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
   }
   int rc = upload(hd, reinterpret_cast<char **>(&hd->d_tiles), all.data(), all.size());
   if (rc) return rc;
+  {
+    // k_cutp: per cut cell its own list of cut-face points in its reference
+    // coordinates [xi, eta, zeta, W] (normal coordinate exactly 0 or 1)
+    std::vector<CDesc2> c2(cd.size());
+    std::vector<double> fac;
+    for (size_t i = 0; i < cd.size(); ++i) {
+      const CDesc &d = cd[i];
+      CDesc2 &e = c2[i];
+      std::memset(&e, 0, sizeof(e));
+      e.blk = d.blk;
+      e.vb = d.vb;
+      e.sb = d.sb;
+      e.nv = d.nv;
+      e.ns = d.ns;
+      e.fb = (int64_t)fac.size() / 4;
+      for (int f = 0; f < 6; ++f) {
+        e.nb[f] = -1;
+        if (!((d.flags >> (12 + f)) & 1u) || d.nb[f] < 0) continue;
+        e.nb[f] = d.nb[f];
+        e.fmask |= 1u << f;
+        const int dd = f >> 1, e1 = dd == 0 ? 1 : 0, e2 = dd == 2 ? 1 : 2;
+        for (int64_t q = pb->sf_ptr[d.sf[f]]; q < pb->sf_ptr[d.sf[f] + 1]; ++q) {
+          double x[4];
+          x[dd] = (f & 1) ? 1.0 : 0.0;
+          x[e1] = pb->sf_pts[3 * q];
+          x[e2] = pb->sf_pts[3 * q + 1];
+          x[3] = pb->sf_pts[3 * q + 2];
+          fac.insert(fac.end(), x, x + 4);
+        }
+      }
+      e.nf = (int32_t)((int64_t)fac.size() / 4 - e.fb);
+    }
+    CU(cudaFuncSetAttribute(k_cutp<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutPCfg<N>::SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_cutp, k_cutp<N>, 32 * CutPCfg<N>::WARPS,
+                                                     CutPCfg<N>::SMEM));
+    hd->occ_cutp = std::max(1, hd->occ_cutp);
+    // per part: longest-processing-time assignment of the cells to the warps of
+    // the launch (cost ~ point chunks + a fixed per-cell part), cells of a warp
+    // stored contiguously, heaviest first
+    constexpr int WP = CutPCfg<N>::WARPS;
+    std::vector<int> ws, ks;
+    std::vector<CChunk> chunk;
+    std::vector<CDesc2> c2o(c2.size());
+    for (int pt = 1; pt <= 2; ++pt) {
+      const int64_t o = hd->r_off[pt][2], n = hd->r_cnt[pt][2];
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + WP - 1) / WP, (int64_t)hd->occ_cutp * hd->sm_count));
+      hd->grid_cutp[pt] = n > 0 ? grid : 0;
+      hd->w_off[pt] = (int64_t)ws.size();
+      const int W = grid * WP;
+      std::vector<int64_t> idx(n);
+      auto cost = [&](const CDesc2 &e) { return (double)((e.nv + e.ns + e.nf + 31) / 32) + 1.5; };
+      for (int64_t i = 0; i < n; ++i) idx[i] = o + i;
+      std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return cost(c2[a]) > cost(c2[b]); });
+      std::vector<std::vector<int64_t>> lists(W);
+      std::priority_queue<std::pair<double, int>, std::vector<std::pair<double, int>>, std::greater<>> heap;
+      for (int w = 0; w < W; ++w) heap.push({0.0, w});
+      for (int64_t i : idx) {
+        auto top = heap.top();
+        heap.pop();
+        lists[top.second].push_back(i);
+        heap.push({top.first + cost(c2[i]), top.second});
+      }
+      int64_t pos = o;
+      for (int w = 0; w < W; ++w) {
+        ws.push_back((int)(pos - o));
+        ks.push_back((int)chunk.size());
+        for (int64_t i : lists[w]) {
+          const CDesc2 &e = c2[i];
+          c2o[pos++] = e;
+          // the chunks of this cell: stream = [volume | interface | cut face] points
+          const int nv = (hd->mask & CUTFEM_TERM_CELL) ? e.nv : 0, ns = (hd->mask & CUTFEM_TERM_NITSCHE) ? e.ns : 0;
+          const int nf = (hd->mask & CUTFEM_TERM_SIPG) ? e.nf : 0;
+          for (int q0 = 0; q0 < nv + ns + nf; q0 += 32) {
+            const int cv = std::max(0, std::min(32, nv - q0));
+            const int qs = std::max(0, q0 - nv), cs = std::max(0, std::min(32 - cv, ns - qs));
+            const int qf = std::max(0, q0 - nv - ns), cf = std::max(0, std::min(32 - cv - cs, nf - qf));
+            CChunk r;
+            r.vo = (int32_t)(e.vb + q0);
+            r.so = (int32_t)(e.sb + qs);
+            r.fo = (int32_t)(e.fb + qf);
+            r.cnt = cv | (cs << 8) | (cf << 16);
+            chunk.push_back(r);
+          }
+        }
+      }
+      ws.push_back((int)(pos - o));
+      ks.push_back((int)chunk.size());
+    }
+    hd->w_off[0] = hd->w_off[1];
+    hd->grid_cutp[0] = -1;  // part 0 launches parts 1 and 2 (see launch_tiles)
+    if ((rc = upload(hd, &hd->d_cdesc2, c2o.data(), c2o.size()))) return rc;
+    if ((rc = upload(hd, &hd->d_fac, fac.data(), fac.size()))) return rc;
+    if ((rc = upload(hd, &hd->d_wstart, ws.data(), ws.size()))) return rc;
+    if ((rc = upload(hd, &hd->d_kstart, ks.data(), ks.size()))) return rc;
+    if ((rc = upload(hd, &hd->d_chunks, chunk.data(), chunk.size()))) return rc;
+    {
+      int64_t mx = (int64_t)fac.size() / 4;
+      for (const CDesc2 &e : c2) mx = std::max(mx, std::max(e.vb + e.nv, e.sb + e.ns));
+      if (mx > INT32_MAX) return fail(CUTFEM_EUNSUPPORTED, "k_cutp point offsets need int32");
+    }
+  }
   hd->ttab.resize(sizeof(TileTab<N>));
   build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
   if constexpr (N == 4) {
@@ -410,7 +538,6 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_tile<N, 0>, 32, C::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_tile<N, 1>, 32, C::SMEM));
   }
-  CU(cudaFuncSetAttribute(k_cutw<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutWCfg<N>::SMEM));
   for (int k = 0; k < 2; ++k) hd->occ_tile[k] = std::max(1, hd->occ_tile[k]);
   return 0;
 }
@@ -440,11 +567,15 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
       CU(cudaEventRecord(hd->ev_fork, st));
       CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
     }
-    using CW = CutWCfg<NT>;
-    const unsigned grid = (unsigned)((nc + CW::WARPS - 1) / CW::WARPS);
-    k_cutw<NT, false><<<grid, 32 * CW::WARPS, CW::SMEM, fork ? hd->side : st>>>(
-        u, v, hd->d_cdesc + hd->r_off[part][2], (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp,
-        hd->d_sfptr, hd->kp, hd->ft);
+    using CP = CutPCfg<NT>;
+    // part 0 = the interior list then the slab-boundary list (each with its own warp schedule)
+    for (int pt = 1; pt <= 2; ++pt) {
+      if (part != 0 && part != pt) continue;
+      if (hd->grid_cutp[pt] <= 0) continue;
+      k_cutp<NT><<<hd->grid_cutp[pt], 32 * CP::WARPS, CP::SMEM, fork ? hd->side : st>>>(
+          u, v, hd->d_cdesc2 + hd->r_off[pt][2], hd->d_chunks, hd->d_vol, hd->d_srf, hd->d_fac,
+          hd->d_wstart + hd->w_off[pt], hd->d_kstart + hd->w_off[pt], hd->kp);
+    }
     CU(cudaGetLastError());
   }
   const TileTab<NT> &tt = *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data());
@@ -636,6 +767,11 @@ void free_handle(cutfem_handle *hd) {
   if (!hd) return;
   cudaFree(hd->d_udesc);
   cudaFree(hd->d_tiles);
+  cudaFree(hd->d_cdesc2);
+  cudaFree(hd->d_wstart);
+  cudaFree(hd->d_kstart);
+  cudaFree(hd->d_chunks);
+  cudaFree(hd->d_fac);
   cudaFree(hd->d_cdesc);
   cudaFree(hd->d_vol);
   cudaFree(hd->d_srf);

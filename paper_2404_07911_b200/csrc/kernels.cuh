@@ -43,6 +43,8 @@ struct RefTab {
   double gw[CUTFEM_NMAX];    // Gauss weights
   double d0[CUTFEM_NMAX];    // l_a'(0)
   double d1[CUTFEM_NMAX];    // l_a'(1)
+  double mc[CUTFEM_NMAX][CUTFEM_NMAX];  // l_a(x) = sum_k mc[a][k] t^k, t = 2x - 1 (k_cutp basis)
+  double md[CUTFEM_NMAX][CUTFEM_NMAX];  // 2 k mc[a][k]: d/dx = 2 d/dt
 };
 
 __constant__ RefTab c_ref[8];  // index N - 2
@@ -866,3 +868,4 @@ struct BF {
 
 #include "kernels_fast.cuh"
 #include "kernels_tile.cuh"
+#include "kernels_cut.cuh"

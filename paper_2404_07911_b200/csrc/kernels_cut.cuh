@@ -1,0 +1,384 @@
+// k_cutp<N> (N = p+1 <= 4): the unstructured terms of the cut cells (Alg. 1
+// "intersected" branch), included by kernels.cuh.
+//
+// One warp per cut cell, lanes = quadrature points (the paper's vectorisation
+// over points), persistent: every warp walks its own list of cells, the
+// lists balanced on the host by longest-processing-time assignment.  Three kinds of points form ONE stream per cell:
+//   volume points     (xi, W):        W grad u . grad phi                    (eq:unstructured_cell)
+//   interface points  (xi, n, W):     Nitsche  W [-(d_n phi) u - phi d_n u + tau/h phi u]
+//   cut-face points   (xi on a face): SIPG over F cap Omega                  (eq:unstructured_face P:489-496)
+// A cut-face point lies on a face of the cell, so its own-side test functions
+// are the cell's tensor basis at that point (value l_m(face) = delta, normal
+// derivative l'_m(face)): its flux  W [(sigma [u] - {d_n u}) [phi] - {d_n phi} [u]]
+// is an ordinary point update with coefficients on phi and d_d phi.  [u] and
+// {d_n u} at the point come from the face traces J_t = u_own - u_nb and
+// A_t = d u_own + d u_nb on the n x n in-face nodes, evaluated by 2-D tensor
+// interpolation (normal reduction first, then in-face evaluation).
+// Every point is integrated into per-lane register accumulators for all n^3
+// DoFs by the factored contraction; one butterfly reduction over the
+// warp per cell, one coalesced write of the block.  The structured faces of the
+// cut cell (full-face SIPG, ghost penalty) are added afterwards by k_tile*<MODE 1>.
+//
+// Latency: the next cell's block + cut-face neighbour blocks are fetched (TMA
+// bulk copies, or cp.async for odd n) into the second buffer set while the
+// current cell's points run; point chunks of 32 are double-buffered across cell
+// boundaries, so the stream never waits on a cold start.
+#pragma once
+#ifndef CUTP_MINB
+#define CUTP_MINB 1
+#endif
+
+struct __align__(16) CDesc2 {
+  int32_t blk;
+  int32_t nb[6];     // neighbour block of each cut face with points, else -1
+  uint32_t fmask;    // bit f: cut face f with points
+  int64_t vb, sb, fb;  // first volume / interface / cut-face point of the cell
+  int32_t nv, ns, nf, pad;
+};
+
+// value + reference gradient at a point from the unpadded block U (16-byte
+// loads of the x rows when n is even)
+template <int N>
+__device__ __forceinline__ void eval_u(const double *U, const double (&vx)[N], const double (&dvx)[N],
+                                       const double (&vy)[N], const double (&dvy)[N], const double (&vz)[N],
+                                       const double (&dvz)[N], double &u0, double &ux, double &uy, double &uz) {
+  u0 = ux = uy = uz = 0.0;
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    double t00 = 0.0, t10 = 0.0, t01 = 0.0;
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double row[N];
+      const double *rp = U + c * N * N + b * N;
+      if constexpr ((N % 2) == 0) {
+#pragma unroll
+        for (int k = 0; k < N; k += 2) {
+          const double2 x = *reinterpret_cast<const double2 *>(rp + k);
+          row[k] = x.x;
+          row[k + 1] = x.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) row[k] = rp[k];
+      }
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        s0 = fma(vx[a], row[a], s0);
+        s1 = fma(dvx[a], row[a], s1);
+      }
+      t00 = fma(vy[b], s0, t00);
+      t10 = fma(dvy[b], s0, t10);
+      t01 = fma(vy[b], s1, t01);
+    }
+    u0 = fma(vz[c], t00, u0);
+    uz = fma(dvz[c], t00, uz);
+    uy = fma(vz[c], t10, uy);
+    ux = fma(vz[c], t01, ux);
+  }
+}
+
+// l_a(x), l_a'(x) from the monomial form in t = 2x - 1 and the symmetry
+// l_{n-1-a}(t) = l_a(-t): even/odd parts in t^2 by Horner.
+template <int N>
+__device__ __forceinline__ void basis_vd_sym(const RefTab &R, double x, double (&v)[N], double (&dv)[N]) {
+  const double t = fma(2.0, x, -1.0), t2 = t * t;
+#pragma unroll
+  for (int a = 0; a < (N + 1) / 2; ++a) {
+    // E = sum_{k even} c_k t^k, O = sum_{k odd} c_k t^k; E' / O' of d/dx = 2 d/dt
+    double E = 0.0, O = 0.0, Ed = 0.0, Od = 0.0;
+#pragma unroll
+    for (int k = N - 1; k >= 0; --k) {
+      if (k % 2 == 0) E = fma(E, t2, R.mc[a][k]);
+      else O = fma(O, t2, R.mc[a][k]);
+    }
+    O *= t;
+#pragma unroll
+    for (int k = N - 1; k >= 1; --k) {  // R.md[a][k] = 2 k mc[a][k]
+      if (k % 2 == 1) Ed = fma(Ed, t2, R.md[a][k]);  // k odd: t^{k-1} even
+      else Od = fma(Od, t2, R.md[a][k]);             // k even: t^{k-1} odd
+    }
+    Od *= t;
+    if (a == N - 1 - a) {
+      v[a] = E + O;
+      dv[a] = Ed + Od;
+    } else {
+      v[a] = E + O;
+      v[N - 1 - a] = E - O;
+      dv[a] = Ed + Od;
+      dv[N - 1 - a] = Od - Ed;
+    }
+  }
+}
+
+// A chunk of <= 32 stream points of one cell: vol rows [vo, vo+cv), interface
+// rows [so, so+cs), cut-face rows [fo, fo+cf).  Built on the host per warp, in the
+// order the warp consumes them.
+struct __align__(16) CChunk {
+  int32_t vo, so, fo;
+  int32_t cnt;  // cv | cs << 8 | cf << 16
+};
+
+template <int N>
+struct CutPCfg {
+  static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
+  static constexpr int WARPS = 4;
+  static constexpr int NB = 4;  // point-chunk ring depth (3 chunks in flight while one is computed)
+  static constexpr int NN = N * N, N3 = N * N * N, N3P = (N3 + 1) & ~1;
+  static constexpr int ACC = N == 4 ? 64 : (N == 3 ? 32 : 8);  // padded n^3 (power of two)
+  // bars(2 + NB) | UB[2][7][N3P] | JAB[6][2][NN] | ring[NB][2 + 256] (header + rows)
+  static constexpr int OFF_UB = (2 + NB + 1) & ~1;
+  static constexpr int OFF_JAB = OFF_UB + 2 * 7 * N3P;
+  static constexpr int OFF_RING = OFF_JAB + ((6 * 2 * NN + 1) & ~1);
+  static constexpr int RSLOT = 2 + 256;
+  static constexpr int WSLOT = OFF_RING + NB * RSLOT;
+  static constexpr int SMEM = WARPS * WSLOT * 8;
+};
+
+template <int N>
+__global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restrict__ u, double *__restrict__ v,
+                                              const CDesc2 *__restrict__ desc, const CChunk *__restrict__ chunks,
+                                              const double *__restrict__ vol_pts, const double *__restrict__ srf_pts,
+                                              const double *__restrict__ fac_pts, const int *__restrict__ wstart,
+                                              const int *__restrict__ kstart, KParams kp) {
+  static_assert(2 * N * N <= 32, "k_cutp needs N <= 4");
+  using C = CutPCfg<N>;
+  using LN = BlkU<N>;
+  constexpr int NN = C::NN, N3 = C::N3, N3P = C::N3P, NB = C::NB;
+  const RefTab &R = c_ref[N - 2];
+  extern __shared__ __align__(16) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp gw owns cells [wstart[gw], wstart[gw+1]) and their chunks [kstart[gw], kstart[gw+1])
+  // (longest-processing-time assignment computed at setup, heaviest first)
+  const int gw = blockIdx.x * C::WARPS + warp;
+  const int c0w = wstart[gw], c1w = wstart[gw + 1];
+  if (c0w >= c1w) return;
+  const int k0w = kstart[gw], k1w = kstart[gw + 1];
+  double *base = smem + warp * C::WSLOT;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(base);  // 0,1: block sets; 2..2+NB: chunk ring
+  double *UB = base + C::OFF_UB, *JAB = base + C::OFF_JAB, *RING = base + C::OFF_RING;
+  const bool cell_on = (kp.mask & TERM_CELL) != 0, nit_on = (kp.mask & TERM_NITSCHE) != 0,
+             sipg_on = (kp.mask & TERM_SIPG) != 0;
+  auto counts = [&](const CDesc2 &d, int &nv, int &ns, int &nf) {
+    nv = cell_on ? d.nv : 0;
+    ns = nit_on ? d.ns : 0;
+    nf = sipg_on ? d.nf : 0;
+  };
+  auto fmask_of = [&](const CDesc2 &d) { return sipg_on ? d.fmask : 0u; };
+  // blocks of a cell (own + cut-face neighbours) into set s
+  auto issue_blocks = [&](const CDesc2 &d, int s) {
+    double *U = UB + s * 7 * N3P;
+    const uint32_t fm = fmask_of(d);
+    if constexpr (C::BULK) {
+      if (lane == 0) {
+        mbar_expect_tx(bar + s, (uint32_t)((1 + __popc(fm)) * N3 * 8));
+        bulk_g2s(U, u + (size_t)d.blk * N3, N3 * 8, bar + s);
+#pragma unroll
+        for (int f = 0; f < 6; ++f)
+          if ((fm >> f) & 1u) bulk_g2s(U + (1 + f) * N3P, u + (size_t)d.nb[f] * N3, N3 * 8, bar + s);
+      }
+    } else {
+      if (lane < N3) {
+        cp_async8(U + lane, u + (size_t)d.blk * N3 + lane);
+#pragma unroll
+        for (int f = 0; f < 6; ++f)
+          if ((fm >> f) & 1u) cp_async8(U + (1 + f) * N3P + lane, u + (size_t)d.nb[f] * N3 + lane);
+      }
+      cp_async_commit();
+    }
+  };
+  // chunk j of the warp's list (record r) into ring slot j % NB (lane 0)
+  auto issue_chunk = [&](int j, const CChunk &r) {
+    if (lane != 0 || j >= k1w) return;
+    const int b = (j - k0w) % NB;
+    double *S = RING + b * C::RSLOT;
+    const int cv = r.cnt & 0xff, cs = (r.cnt >> 8) & 0xff, cf = (r.cnt >> 16) & 0xff;
+    reinterpret_cast<int *>(S)[0] = r.cnt;
+    mbar_expect_tx(bar + 2 + b, (uint32_t)(cv * 32 + cs * 64 + cf * 32));
+    if (cv) bulk_g2s(S + 2, vol_pts + 4 * (size_t)r.vo, (uint32_t)(cv * 32), bar + 2 + b);
+    if (cs) bulk_g2s(S + 2 + 4 * cv, srf_pts + 8 * (size_t)r.so, (uint32_t)(cs * 64), bar + 2 + b);
+    if (cf) bulk_g2s(S + 2 + 4 * cv + 8 * cs, fac_pts + 4 * (size_t)r.fo, (uint32_t)(cf * 32), bar + 2 + b);
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 2 + NB; ++i) mbar_init(bar + i, 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  CDesc2 cd = desc[c0w];
+  issue_blocks(cd, 0);
+  // prologue: NB-1 chunks in flight, the record of the next one prefetched into a register
+  CChunk rn = {0, 0, 0, 0};
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NB - 1; ++j)
+      if (k0w + j < k1w) issue_chunk(k0w + j, chunks[k0w + j]);
+    if (k0w + NB - 1 < k1w) rn = chunks[k0w + NB - 1];
+  }
+  int j = k0w;  // next chunk to consume
+  const double ih = kp.ih, ih2 = kp.ih2;
+  int it = 0;
+  for (int c = c0w; c < c1w; ++c, ++it) {
+    const int set = it & 1;
+    const bool has_next = c + 1 < c1w;
+    CDesc2 nd;
+    if (has_next) nd = desc[c + 1];
+    int nv, ns, nf;
+    counts(cd, nv, ns, nf);
+    const int total = nv + ns + nf, K = (total + 31) / 32;
+    const uint32_t fm = fmask_of(cd);
+    // ---- this cell's blocks
+    if constexpr (C::BULK) {
+      mbar_wait(bar + set, (it >> 1) & 1);
+    } else {
+      cp_async_wait<0>();
+      __syncwarp();
+    }
+    const double *U = UB + set * 7 * N3P;
+    // ---- cut-face traces J_t = u_own - u_nb, A_t = d u_own + d u_nb (lanes: two faces per pass)
+    if (fm) {
+      const int side = lane >= NN ? 1 : 0, t = lane - side * NN;
+      static_for<0, 3>([&](auto dc) {
+        constexpr int D = decltype(dc)::value;
+        const int f = 2 * D + side;
+        if (lane < 2 * NN && ((fm >> f) & 1u)) {
+          const double *NBf = U + (1 + f) * N3P;
+          constexpr int st = LN::template lstride<D>();
+          const int b0 = LN::template lbase<D>(t);
+          const double *dow = side ? R.d1 : R.d0;
+          const double *dnb = side ? R.d0 : R.d1;
+          double A = 0.0;
+#pragma unroll
+          for (int m = 0; m < N; ++m) A = fma(dow[m], U[b0 + m * st], fma(dnb[m], NBf[b0 + m * st], A));
+          const double J = side ? (U[b0 + (N - 1) * st] - NBf[b0]) : (U[b0] - NBf[b0 + (N - 1) * st]);
+          JAB[f * 2 * NN + t] = J;
+          JAB[f * 2 * NN + NN + t] = A;
+        }
+      });
+      __syncwarp();
+    }
+    // ---- next cell's blocks into the other set (its previous user, cell it-1, is done)
+    if (has_next) issue_blocks(nd, set ^ 1);
+    // ---- the point stream
+    double acc[C::ACC];
+#pragma unroll
+    for (int i = 0; i < C::ACC; ++i) acc[i] = 0.0;
+    for (int k = 0; k < K; ++k, ++j) {
+      const int b = (j - k0w) % NB;
+      mbar_wait(bar + 2 + b, ((j - k0w) / NB) & 1);
+      // refill: chunk j+NB-1 goes to the slot consumed at j-1
+      if (lane == 0) {
+        issue_chunk(j + NB - 1, rn);
+        if (j + NB < k1w) rn = chunks[j + NB];
+      }
+      const double *S = RING + b * C::RSLOT;
+      const int cnt = reinterpret_cast<const int *>(S)[0];
+      const int cv = cnt & 0xff, cs = (cnt >> 8) & 0xff, cf = (cnt >> 16) & 0xff;
+      // kind: 0 volume, 1 interface, 2 cut face, 3 idle lane
+      const int kind = lane < cv ? 0 : (lane < cv + cs ? 1 : (lane < cv + cs + cf ? 2 : 3));
+      double xi = 0.5, eta = 0.5, zeta = 0.5, W = 0.0, nx = 0.0, ny = 0.0, nz = 0.0;
+      if (kind == 0 || kind == 2) {
+        const double *pp = S + 2 + (kind == 0 ? 4 * lane : 4 * cv + 8 * cs + 4 * (lane - cv - cs));
+        const double2 p0 = *reinterpret_cast<const double2 *>(pp);
+        const double2 p1 = *reinterpret_cast<const double2 *>(pp + 2);
+        xi = p0.x;
+        eta = p0.y;
+        zeta = p1.x;
+        W = p1.y;
+      } else if (kind == 1) {
+        const double *pp = S + 2 + 4 * cv + 8 * (lane - cv);
+        const double2 p0 = *reinterpret_cast<const double2 *>(pp);
+        const double2 p1 = *reinterpret_cast<const double2 *>(pp + 2);
+        const double2 p2 = *reinterpret_cast<const double2 *>(pp + 4);
+        const double2 p3 = *reinterpret_cast<const double2 *>(pp + 6);
+        xi = p0.x;
+        eta = p0.y;
+        zeta = p1.x;
+        nx = p1.y;
+        ny = p2.x;
+        nz = p2.y;
+        W = p3.x;
+      }
+      double vx[N], dvx[N], vy[N], dvy[N], vz[N], dvz[N];
+      basis_vd_sym<N>(R, xi, vx, dvx);
+      basis_vd_sym<N>(R, eta, vy, dvy);
+      basis_vd_sym<N>(R, zeta, vz, dvz);
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+      if (kind < 2) {
+        double u0, ux, uy, uz;
+        eval_u<N>(U, vx, dvx, vy, dvy, vz, dvz, u0, ux, uy, uz);
+        if (kind == 1) {
+          const double un = (nx * ux + ny * uy + nz * uz) * ih;  // physical normal derivative
+          c0 = W * (kp.tau * u0 - un);
+          const double g = -W * u0 * ih;
+          c1 = g * nx;
+          c2 = g * ny;
+          c3 = g * nz;
+        } else {
+          const double sw = W * ih2;
+          c1 = sw * ux;
+          c2 = sw * uy;
+          c3 = sw * uz;
+        }
+      } else if (kind == 2) {
+        // the face: the coordinate that is exactly 0 or 1
+        const int d = (xi == 0.0 || xi == 1.0) ? 0 : ((eta == 0.0 || eta == 1.0) ? 1 : 2);
+        const int sd = (d == 0 ? xi : (d == 1 ? eta : zeta)) == 1.0 ? 1 : 0;
+        const double *JA = JAB + (2 * d + sd) * 2 * NN, *JB = JA + NN;
+        double ls[N], lt[N];  // in-face bases along e1 < e2
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          ls[i] = d == 0 ? vy[i] : vx[i];
+          lt[i] = d == 2 ? vy[i] : vz[i];
+        }
+        double J = 0.0, A = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < N; ++jj) {
+          double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            r0 = fma(ls[i], JA[i + N * jj], r0);
+            r1 = fma(ls[i], JB[i + N * jj], r1);
+          }
+          J = fma(lt[jj], r0, J);
+          A = fma(lt[jj], r1, A);
+        }
+        const double sg = sd ? kp.i2h : -kp.i2h;  // sign of the own side / (2h)
+        const double k1 = W * fma(kp.sigma, J, -sg * A), k2 = -W * sg * J;
+        c0 = k1;
+        c1 = d == 0 ? k2 : 0.0;
+        c2 = d == 1 ? k2 : 0.0;
+        c3 = d == 2 ? k2 : 0.0;
+      }
+#pragma unroll
+      for (int cz = 0; cz < N; ++cz) {
+        const double T0 = fma(c0, vz[cz], c3 * dvz[cz]);
+        const double T1 = c2 * vz[cz];
+        const double T2 = c1 * vz[cz];
+#pragma unroll
+        for (int by = 0; by < N; ++by) {
+          const double S0 = fma(vy[by], T0, dvy[by] * T1);
+          const double S1 = vy[by] * T2;
+#pragma unroll
+          for (int ax = 0; ax < N; ++ax) {
+            double &r = acc[(cz * N + by) * N + ax];
+            r = fma(vx[ax], S0, fma(dvx[ax], S1, r));
+          }
+        }
+      }
+      __syncwarp();  // every lane is done with ring slot b before it is refilled
+      if (lane == 0) fence_proxy_async();
+    }
+    // ---- reduce over the warp and write the block (every cut cell block written once)
+    butterfly<C::ACC>(acc, lane);
+    double *vb = v + (size_t)cd.blk * N3;
+    if constexpr (C::ACC == 64) {
+      *reinterpret_cast<double2 *>(vb + 2 * lane) = make_double2(acc[0], acc[1]);
+    } else {
+      const int l = BF<C::ACC>::idx(lane, 0);
+      if (BF<C::ACC>::writer(lane) && l < N3) vb[l] = acc[0];
+    }
+    if constexpr (!C::BULK) __syncwarp();
+    if (has_next) cd = nd;
+  }
+}

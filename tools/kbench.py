@@ -38,8 +38,12 @@ def t(fn, K=20):
     return float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
 
 
-res = {"cfg": cfg, "n_dofs": P.n_dofs, "flush": MODE}
-for mask, name in ((15, "all"), (1, "cell"), (2, "sipg"), (4, "nitsche"), (8, "gp"), (0x10 | 0, "none")):
+res = {"cfg": cfg, "n_dofs": P.n_dofs, "flush": MODE, "lib": os.environ.get("CUTFEM_LIB", "default")}
+ALL = ((15, "all"), (1, "cell"), (2, "sipg"), (4, "nitsche"), (8, "gp"), (0x10 | 0, "none"))
+want = os.environ.get("MASKS")
+for mask, name in ALL:
+    if want and name not in want.split(","):
+        continue
     m = mask if mask != 0x10 else 0x10
     try:
         op = cf.CutFEM(P, term_mask=m)
