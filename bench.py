@@ -256,7 +256,12 @@ def run_ours(args, P, cfg, rank, world, local_rank):
     peaks = load_peaks()
     bw = float(peaks.get("hbm_gbs", 6543.7)) * 1e9
     fp64 = costmodel.fp64_peak_tflops() * 1e12
-    kname = {"structured": f"k_uncut3<{P.degree + 1}>", "unstructured": f"k_cutw<{P.degree + 1}>"}
+    n_ = P.degree + 1
+    if n_ <= 4:
+        kname = {"structured": (f"k_tile2<{n_},0>" if n_ == 4 else f"k_tile<{n_},0>") + f" + k_gpw<{n_}>",
+                 "unstructured": f"k_cutp<{n_}>"}
+    else:
+        kname = {"structured": f"k_uncut{'3' if n_ == 5 else ''}<{n_}>", "unstructured": f"k_cut<{n_}>"}
     dom = max(k_ms, key=k_ms.get)
     F_dom = work["F_uncut"] if dom == "structured" else work["F_cut"]
     B_dom = work["B_uncut"] if dom == "structured" else work["B_cut"]

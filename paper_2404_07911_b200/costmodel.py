@@ -50,10 +50,11 @@ def flops_cut_face(n: int, n_pts: int) -> int:
 
 
 def apply_work(stats: dict) -> dict:
-    """F_alg / B_alg per kernel and in total from cutfem_stats() counters.
-    The structured kernel owns uncut cells; the unstructured kernel owns cut
-    cells.  A face is attributed to the kernel of its minus cell... for the
-    split we attribute structured faces and GP faces by their cell counts."""
+    """F_alg / B_alg per kernel family and in total from cutfem_stats() counters.
+    Attribution follows the p <= 3 pipeline: the structured family (k_tile* +
+    k_gpw) owns the uncut cells, the full-face SIPG faces and the ghost-penalty
+    faces; the unstructured kernel (k_cutp) owns the volume / interface points
+    and the cut faces."""
     n = stats["degree"] + 1
     n3 = n ** 3
     nu, nc = stats["n_uncut"], stats["n_cut"]
@@ -62,10 +63,8 @@ def apply_work(stats: dict) -> dict:
     f_uncut = nu * flops_uncut_cell(n)
     f_cut = (stats["n_vol_pts"] * flops_vol_point(n) + stats["n_srf_pts"] * flops_srf_point(n)
              + stats["n_faces_cut"] * 8 * n ** 3 + stats["n_face_pts"] * (8 * n * n + 8 * n + 8))
-    # split face work by the share of face-sides each kernel owns
-    share_cut = nc / max(nu + nc, 1)
-    F_unc = f_uncut + (f_struct + f_gp) * (1 - share_cut)
-    F_cut = f_cut + (f_struct + f_gp) * share_cut
+    F_unc = f_uncut + f_struct + f_gp
+    F_cut = f_cut
     b_vec = 16 * stats["n_dofs"]
     B_unc = 16 * nu * n3 + 32 * nu
     B_cut = (16 * nc * n3 + 64 * nc + 32 * stats["n_vol_pts"] + 56 * stats["n_srf_pts"]

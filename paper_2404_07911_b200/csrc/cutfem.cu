@@ -68,11 +68,13 @@ struct cutfem_handle {
   KParams kp;
   FaceTab ft;
   // thread-per-cell structured kernel (N <= 4): warp-tiles per part (0 all, 1 interior, 2 boundary)
-  // tile sets: [0] uncut cells, volume + SIPG (v = ...); [1] ghost-penalty cells
-  // (cut cells and their uncut neighbours) + the cut cells' structured SIPG (v += ...)
+  // tile sets: [0] uncut cells, volume + SIPG (v = ...); [1] cells with ghost-
+  // penalty faces (cut cells and their uncut neighbours) + the cut cells'
+  // full-face SIPG (v += ..., k_gpw)
   void *d_tiles = nullptr;
-  int64_t t_off[2][3] = {{0}}, t_cnt[2][3] = {{0}};
-  int occ_tile[2] = {1, 1};
+  int64_t t_off[3][3] = {{0}}, t_cnt[3][3] = {{0}};
+  int occ_tile[3] = {1, 1, 1};
+  int persist = 1;  // tile kernels: persistent grid (1) or one tile per CTA (0); env CUTFEM_TILE_PERSIST
   std::vector<char> ttab;  // TileTab<N> bytes
   CDesc2 *d_cdesc2 = nullptr;  // k_cutp: cut cells grouped per warp (LPT), their cut-face points
   double *d_fac = nullptr;
@@ -369,7 +371,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
                 const std::vector<CDesc> &cd) {
   using C = TileCfg<N>;
   // per part (1 interior, 2 slab boundary): K1 = uncut cells, K2 = GP cells
-  std::vector<TCell> set[2][2];
+  std::vector<TCell> set[3][2];
   for (int pt = 1; pt <= 2; ++pt) {
     for (int k = 0; k < 2; ++k)
       for (int64_t i = hd->r_off[pt][k]; i < hd->r_off[pt][k] + hd->r_cnt[pt][k]; ++i) {
@@ -409,7 +411,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
   }
   const int64_t rs = (int64_t)sizeof(TileRec<C::SMAX>);
   std::vector<char> all;
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k) {
     std::vector<char> b0, b1;
     build_tiles<N>(set[k][0], pb, b0);
     build_tiles<N>(set[k][1], pb, b1);
@@ -529,16 +531,15 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
   if constexpr (N == 4) {
     using C2 = Tile2Cfg<N>;
     CU(cudaFuncSetAttribute(k_tile2<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
-    CU(cudaFuncSetAttribute(k_tile2<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_tile2<N, 0>, C2::THREADS, C2::SMEM));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_tile2<N, 1>, C2::THREADS, C2::SMEM));
   } else {
     CU(cudaFuncSetAttribute(k_tile<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    CU(cudaFuncSetAttribute(k_tile<N, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_tile<N, 0>, 32, C::SMEM));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_tile<N, 1>, 32, C::SMEM));
   }
-  for (int k = 0; k < 2; ++k) hd->occ_tile[k] = std::max(1, hd->occ_tile[k]);
+  CU(cudaFuncSetAttribute(k_gpw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, GpwCfg<N>::SMEM));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_gpw<N>, GpwCfg<N>::THREADS,
+                                                   GpwCfg<N>::SMEM));
+  for (int k = 0; k < 3; ++k) hd->occ_tile[k] = std::max(1, hd->occ_tile[k]);
   return 0;
 }
 
@@ -552,21 +553,22 @@ int dispatch_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vecto
   return 0;
 }
 
-// N <= 4: the cut kernel (points + cut faces, v = ...) on the side stream
-// concurrently with K1 (uncut cells, v = ...); then K2 (ghost penalty and the
-// cut cells' structured SIPG, v += ...) once both have written.
+// N <= 4: k_cutp (cut cells: points and cut faces, v = ...) on the side stream
+// concurrently with k_tile*<0> (uncut cells: volume + SIPG, v = ...); once both
+// have written, k_gpw adds the ghost penalty and the cut cells' full-face SIPG.
 template <int N>
 int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which, int part) {
   constexpr int NT = (N <= 4 ? N : 4);
   using C = TileCfg<NT>;
   const int64_t nc = (which & 2) ? hd->r_cnt[part][2] : 0;
-  const int64_t n1 = (which & 1) ? hd->t_cnt[0][part] : 0, n2 = (which & 1) ? hd->t_cnt[1][part] : 0;
-  const bool fork = nc > 0 && n1 > 0;
+  const int64_t n0 = (which & 1) ? hd->t_cnt[0][part] : 0;
+  const int64_t n1 = ((which & 1) && (hd->kp.mask & (TERM_GP | TERM_SIPG))) ? hd->t_cnt[1][part] : 0;
+  const bool fork = nc > 0 && n0 > 0;
+  if (fork) {
+    CU(cudaEventRecord(hd->ev_fork, st));
+    CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
+  }
   if (nc > 0) {
-    if (fork) {
-      CU(cudaEventRecord(hd->ev_fork, st));
-      CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
-    }
     using CP = CutPCfg<NT>;
     // part 0 = the interior list then the slab-boundary list (each with its own warp schedule)
     for (int pt = 1; pt <= 2; ++pt) {
@@ -580,29 +582,23 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
   }
   const TileTab<NT> &tt = *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data());
   const auto *tl = reinterpret_cast<const TileRec<C::SMAX> *>(hd->d_tiles);
-  auto grid_of = [&](int64_t nt, int k) {
-    return (unsigned)std::min<int64_t>(nt, (int64_t)hd->occ_tile[k] * hd->sm_count);
-  };
-  if (n1 > 0) {
-    const auto *t1 = tl + hd->t_off[0][part];
+  if (n0 > 0) {
+    const unsigned grid = (unsigned)(hd->persist & 1 ? std::min<int64_t>(n0, (int64_t)hd->occ_tile[0] * hd->sm_count) : n0);
     if constexpr (NT == 4)
-      k_tile2<NT, 0><<<grid_of(n1, 0), Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, t1, (int)n1, tt,
-                                                                                        hd->kp.mask);
+      k_tile2<NT, 0><<<grid, Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, tl + hd->t_off[0][part], (int)n0,
+                                                                              tt, hd->kp.mask);
     else
-      k_tile<NT, 0><<<grid_of(n1, 0), 32, C::SMEM, st>>>(u, v, t1, (int)n1, tt, hd->kp.mask);
+      k_tile<NT, 0><<<grid, 32, C::SMEM, st>>>(u, v, tl + hd->t_off[0][part], (int)n0, tt, hd->kp.mask);
     CU(cudaGetLastError());
   }
   if (fork) {
     CU(cudaEventRecord(hd->ev_join, hd->side));
     CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
   }
-  if (n2 > 0 && (hd->kp.mask & (TERM_GP | TERM_SIPG))) {
-    const auto *t2 = tl + hd->t_off[1][part];
-    if constexpr (NT == 4)
-      k_tile2<NT, 1><<<grid_of(n2, 1), Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, t2, (int)n2, tt,
-                                                                                        hd->kp.mask);
-    else
-      k_tile<NT, 1><<<grid_of(n2, 1), 32, C::SMEM, st>>>(u, v, t2, (int)n2, tt, hd->kp.mask);
+  if (n1 > 0) {
+    const unsigned grid = (unsigned)(hd->persist & 2 ? std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count) : n1);
+    k_gpw<NT><<<grid, GpwCfg<NT>::THREADS, GpwCfg<NT>::SMEM, st>>>(u, v, tl + hd->t_off[1][part], (int)n1, tt,
+                                                                  hd->kp.mask);
     CU(cudaGetLastError());
   }
   return 0;
@@ -1027,6 +1023,8 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   if ((rc = upload(hd, &hd->d_volptr, pb->vol_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_srfptr, pb->srf_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_sfptr, pb->sf_ptr, (size_t)(nsf ? nsf + 1 : 0)))) return rc;
+  if (const char *e = std::getenv("CUTFEM_TILE_PERSIST")) hd->persist = std::atoi(e);
+  else hd->persist = 3;
   if (!std::getenv("CUTFEM_NO_TILE") && (rc = dispatch_tiles(hd, pb, ud, cd))) return rc;
   if ((rc = upload_tables(p))) return rc;
   if ((rc = dispatch_attrs(n))) return rc;

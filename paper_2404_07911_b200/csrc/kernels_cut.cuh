@@ -382,3 +382,4 @@ __global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restric
     if (has_next) cd = nd;
   }
 }
+

@@ -242,8 +242,7 @@ __global__ void __launch_bounds__(32, T1MINB) k_tile(const double *__restrict__ 
     const bool on = lane < ncell;
     // ---- stage the tile's blocks (own cells first, then the halo)
     if constexpr (C::BULK) {
-      bulk_wait_read0();     // previous tile's v stores have left shared memory
-      fence_proxy_async();   // ... and so have this lane's generic reads
+      fence_proxy_async();   // this lane's generic accesses precede the bulk writes into the slots
       __syncwarp();
       if (lane == 0) mbar_expect_tx(bar, (uint32_t)(nslot * N3 * 8));
       __syncwarp();
@@ -315,12 +314,6 @@ __global__ void __launch_bounds__(32, T1MINB) k_tile(const double *__restrict__ 
       });
     }
     __syncwarp();  // every lane is done reading the tile's slots
-    if constexpr (MODE == 1) {
-      if (on)
-#pragma unroll
-        for (int l = 0; l < N3; ++l) w[l] += v[(size_t)myblk * N3 + l];
-    }
-    // ---- write back: own slot, then one bulk store per cell
     if (on) {
       double *Us = S + lane * ST;
       if constexpr ((N % 2) == 0) {
@@ -331,22 +324,16 @@ __global__ void __launch_bounds__(32, T1MINB) k_tile(const double *__restrict__ 
         for (int l = 0; l < N3; ++l) Us[l] = w[l];
       }
     }
-    if constexpr (C::BULK) {
-      fence_proxy_async();
-      if (on) {
-        bulk_s2g(v + (size_t)myblk * N3, S + lane * ST, N3 * 8);
-        bulk_commit();
-      }
-    } else {
-      __syncwarp();
-      for (int c = 0; c < ncell; ++c) {
-        const int b = __shfl_sync(0xffffffffu, myblk, c);
-        if (lane < N3) v[(size_t)b * N3 + lane] = S[c * ST + lane];
-      }
-      __syncwarp();
+    __syncwarp();
+    // ---- coalesced write-back of the cell blocks (MODE 1: read-add-write)
+    for (int e = lane; e < ncell * N3; e += 32) {
+      const int c = e / N3, l = e - c * N3;
+      const int b = T->blk[c];
+      double x = S[c * ST + l];
+      if constexpr (MODE == 1) x += v[(size_t)b * N3 + l];
+      v[(size_t)b * N3 + l] = x;
     }
   }
-  if constexpr (C::BULK) bulk_wait0();
 }
 
 // ===================================================================== k_tile2
@@ -490,8 +477,9 @@ __device__ __forceinline__ TileLane tile_lane(const TileRec<SMAX> *T, int cell, 
 }
 
 // MODE 0: volume (per-lane bit) + SIPG (per-face bits) of uncut cells, v = result.
-// MODE 1: ghost penalty (per-face bits) + SIPG (per-face bits: the structured
-//         faces of cut cells), v += result.
+// MODE 1: ghost penalty (per-face bits) of uncut cells next to cut cells, v += result.
+// MODE 2: ghost penalty + SIPG of the structured faces of cut cells, v = result
+//         (v is then a scratch vector, added by k_addcut once k_cutp has written).
 // Lane flags: lane_nb[l][1] byte 2 = GP faces, byte 3 = SIPG faces | volume << 6.
 template <int N, int MODE>
 __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__ u, double *__restrict__ v,
@@ -511,7 +499,6 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
   const int zb = h ? NN * (N - 1) : 0, zs = h ? -NN : NN;
   if (tid == 0) {
     mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -521,8 +508,7 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const TileLane cu = nx;
     const bool on = cell < cu.ncell;
-    if (h == 0) bulk_wait_read0();  // this thread's previous v store has left shared memory
-    fence_proxy_async();
+    fence_proxy_async();  // this thread's generic accesses to the slots precede the next bulk writes
     __syncthreads();
     if (tid == 0) mbar_expect_tx(bar, (uint32_t)(cu.nslot * N3 * 8));
     __syncthreads();
@@ -555,7 +541,7 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
     const double *Nb[6];
 #pragma unroll
     for (int f = 0; f < 6; ++f) Nb[f] = nbs[f] != 0xff ? S + nbs[f] * ST : Us;  // dummy source when absent
-    if (on || MODE == 1) {
+    if (on || MODE != 0) {
       if constexpr (MODE == 0) {
         const double ev = vol ? 1.0 : 0.0;
         // x and y: plane-local
@@ -621,11 +607,6 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
       }
     }
     __syncthreads();  // every thread is done reading the tile's blocks
-    if constexpr (MODE == 1) {  // fetch the v blocks of the tile's cells into their slots
-      if (tid == 0) mbar_expect_tx(bar + 1, (uint32_t)(cu.ncell * N3 * 8));
-      __syncthreads();
-      if (on && h == 0) bulk_g2s(S + cell * ST, v + (size_t)cu.myblk * N3, N3 * 8, bar + 1);
-    }
     if (on) {
       // v = (M (x) M (x) M) w: x and y sweeps on the own planes ...
       static_for<0, 2>([&](auto dc) {
@@ -663,29 +644,219 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
 #pragma unroll
         for (int i = 0; i < P; ++i) w[t + NN * i] = x[i];
       }
-    }
-    if constexpr (MODE == 1) mbar_wait(bar + 1, it & 1);
-    if (on) {
       double *Uw = S + cell * ST;
 #pragma unroll
       for (int c = 0; c < P; ++c)
 #pragma unroll
-        for (int t = 0; t < NN; t += 2) {
-          double2 *q = reinterpret_cast<double2 *>(Uw + zb + zs * c + t);
-          if constexpr (MODE == 1) {
-            const double2 o = *q;
-            *q = make_double2(o.x + w[t + NN * c], o.y + w[t + 1 + NN * c]);
-          } else {
-            *q = make_double2(w[t + NN * c], w[t + 1 + NN * c]);
+        for (int t = 0; t < NN; t += 2)
+          *reinterpret_cast<double2 *>(Uw + zb + zs * c + t) = make_double2(w[t + NN * c], w[t + 1 + NN * c]);
+    }
+    __syncwarp();  // both halves of the warp's 16 cells are in their slots
+    // ---- coalesced write-back: one 512-byte row (a cell block) per instruction
+    {
+      static_assert(N3 == 64, "one double2 per lane per block");
+      const int c0 = 16 * (tid >> 5);
+      const int ncw = min(16, cu.ncell - c0);
+#pragma unroll
+      for (int g = 0; g < 16; g += 8) {
+        double2 x[8];
+        int ob[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          ob[c] = __shfl_sync(0xffffffffu, cu.myblk, g + c);
+          if (g + c < ncw) {
+            x[c] = *reinterpret_cast<const double2 *>(S + (c0 + g + c) * ST + 2 * lane);
+            if constexpr (MODE == 1) {
+              const double2 o = *reinterpret_cast<const double2 *>(v + (size_t)ob[c] * N3 + 2 * lane);
+              x[c].x += o.x;
+              x[c].y += o.y;
+            }
           }
         }
-    }
-    fence_proxy_async();
-    __syncwarp();
-    if (on && h == 0) {
-      bulk_s2g(v + (size_t)cu.myblk * N3, S + cell * ST, N3 * 8);
-      bulk_commit();
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (g + c < ncw) *reinterpret_cast<double2 *>(v + (size_t)ob[c] * N3 + 2 * lane) = x[c];
+      }
     }
   }
-  if (h == 0) bulk_wait0();
+
+}
+
+// ===================================================================== k_gpw
+// k_gpw<N> (N <= 4): ghost penalty of every cell next to a cut cell plus the
+// full-face SIPG of the cut cells (their faces shared with uncut cells),
+// v += result.  Runs after k_tile*<0> and k_cutp have written v.
+// Same w-space arithmetic as k_tile2 (w += M^{-1}-premultiplied line operators,
+// v += (M (x) M (x) M) w), organised for SMALL CODE: 4 threads per cell, each
+// taking every 4th line of a face in a runtime loop, the accumulator w in
+// shared memory (disjoint lines per thread within one axis; a __syncwarp between
+// axes), faces unrolled only over their 6 (axis, side) variants so the line
+// operators stay warp-uniform constant-bank operands.
+template <int N>
+struct GpwCfg {
+  static constexpr bool BULK = TileCfg<N>::BULK;
+  static constexpr int N3 = N * N * N, ST = TileCfg<N>::ST, SMAX = TileCfg<N>::SMAX;
+  static constexpr int WST = N3 + 2;  // w row stride (doubles): consecutive cells on different banks
+  static constexpr int THREADS = 128;
+  static constexpr int SMEM = 16 + SMAX * ST * 8 + 32 * WST * 8;
+};
+
+template <int N>
+__global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, double *__restrict__ v,
+                                             const TileRec<GpwCfg<N>::SMAX> *__restrict__ tiles, int ntiles,
+                                             TileTab<N> tt, uint32_t mask) {
+  using C = GpwCfg<N>;
+  constexpr int NN = N * N, N3 = C::N3, ST = C::ST, WST = C::WST;
+  extern __shared__ __align__(16) double smem[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  double *S = smem + 2;
+  double *Wb = S + C::SMAX * ST;
+  const int tid = threadIdx.x, cell = tid >> 2, r = tid & 3;
+  const bool sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
+  if (C::BULK && tid == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const TileRec<C::SMAX> *T = tiles + tile;
+    const int nslot = T->nslot, ncell = T->ncell;
+    const bool on = cell < ncell;
+    const uint2 ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[cell][0]);
+    // ---- stage the tile's blocks
+    if constexpr (C::BULK) {
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) mbar_expect_tx(bar, (uint32_t)(nslot * N3 * 8));
+      __syncthreads();
+      for (int s = tid; s < nslot; s += C::THREADS) bulk_g2s(S + s * ST, u + (size_t)T->blk[s] * N3, N3 * 8, bar);
+    } else {
+      __syncthreads();
+      for (int e = tid; e < nslot * N3; e += C::THREADS) {
+        const int s = e / N3, l = e - s * N3;
+        S[s * ST + l] = __ldg(u + (size_t)T->blk[s] * N3 + l);
+      }
+    }
+    double *W = Wb + cell * WST;
+    for (int l = r; l < N3; l += 4) W[l] = 0.0;
+    if constexpr (C::BULK) mbar_wait(bar, it & 1);
+    __syncthreads();
+    int nbs[6];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) nbs[f] = (ln.x >> (8 * f)) & 0xff;
+    nbs[4] = ln.y & 0xff;
+    nbs[5] = (ln.y >> 8) & 0xff;
+    const uint32_t gpb = (on && gp_on) ? (ln.y >> 16) & 0x3fu : 0u;
+    const uint32_t spb = (on && sipg_on) ? (ln.y >> 24) & 0x3fu : 0u;
+    const double *Us = S + (on ? cell : 0) * ST;
+    static_for<0, 6>([&](auto fc) {
+      constexpr int F = decltype(fc)::value, D = F / 2, SS = F % 2;
+      constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
+      const bool g = (gpb >> F) & 1u, sp = (spb >> F) & 1u;
+      const bool anyg = __any_sync(0xffffffffu, g), anys = __any_sync(0xffffffffu, sp);
+      if (anyg || anys) {
+        const double eg = g ? 1.0 : 0.0, es = sp ? 1.0 : 0.0;
+        const double *Nf = (g || sp) ? S + nbs[F] * ST : Us;
+#pragma unroll 1
+        for (int t = r; t < NN; t += 4) {
+          const int t0 = t % N, t1 = t / N;
+          const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
+          double uo[N], un[N], out[N];
+#pragma unroll
+          for (int m = 0; m < N; ++m) {
+            uo[m] = Us[b0 + m * str];
+            un[m] = Nf[b0 + m * str];
+            out[m] = 0.0;
+          }
+          if (anyg) {
+#pragma unroll
+            for (int m = 0; m < N; ++m) {
+              double x = 0.0;
+#pragma unroll
+              for (int a = 0; a < N; ++a) {
+                const int k = SS ? (N - 1 - m) * N + (N - 1 - a) : m * N + a;
+                x = fma(tt.Goo[k], uo[a], fma(tt.Gon[k], un[a], x));
+              }
+              out[m] = eg * x;
+            }
+          }
+          if (anys) {
+            double A0 = 0.0, A1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < N; ++m) {
+              if (SS == 0) {
+                A0 = fma(tt.d0[m], uo[m], A0);
+                A1 = fma(-tt.d0[N - 1 - m], un[m], A1);
+              } else {
+                A0 = fma(-tt.d0[N - 1 - m], uo[m], A0);
+                A1 = fma(tt.d0[m], un[m], A1);
+              }
+            }
+            const double J = es * (SS ? (uo[N - 1] - un[0]) : (uo[0] - un[N - 1]));
+            const double A = es * (A0 + A1);
+#pragma unroll
+            for (int m = 0; m < N; ++m) {
+              if (SS == 0) out[m] = fma(tt.cJ[m], J, fma(tt.cA[m], A, out[m]));
+              else out[m] = fma(tt.cJ[N - 1 - m], J, fma(-tt.cA[N - 1 - m], A, out[m]));
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < N; ++m) W[b0 + m * str] += out[m];
+        }
+      }
+      if (SS == 1) __syncwarp();  // the next axis updates other threads' positions
+    });
+    // ---- v += (M (x) M (x) M) w, sweeps in shared memory
+    static_for<0, 3>([&](auto dc) {
+      constexpr int D = decltype(dc)::value;
+      constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
+#pragma unroll 1
+      for (int t = r; t < NN; t += 4) {
+        const int t0 = t % N, t1 = t / N;
+        const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
+        double x[N], y[N];
+#pragma unroll
+        for (int m = 0; m < N; ++m) x[m] = W[b0 + m * str];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) s = fma(tt.M[csym<N>(i * N + j)], x[j], s);
+          y[i] = s;
+        }
+#pragma unroll
+        for (int m = 0; m < N; ++m) W[b0 + m * str] = y[m];
+      }
+      __syncwarp();
+    });
+    __syncthreads();  // all w final; all slot reads done (the next tile's copies may start)
+    // ---- v += w: each warp its 8 cells, all loads in flight before the adds
+    {
+      const int wrp = tid >> 5, ln32 = tid & 31;
+      const int bl = (ln32 < 8 && 8 * wrp + ln32 < ncell) ? T->blk[8 * wrp + ln32] : 0;
+      constexpr int PER = (N3 + 31) / 32;  // elements of a block per lane
+      double x[8][PER];
+      size_t o[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        o[c] = (size_t)__shfl_sync(0xffffffffu, bl, c) * N3;
+        const bool cv = 8 * wrp + c < ncell;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int l = ln32 + 32 * k;
+          x[c][k] = (cv && l < N3) ? v[o[c] + l] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const bool cv = 8 * wrp + c < ncell;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int l = ln32 + 32 * k;
+          if (cv && l < N3) v[o[c] + l] = x[c][k] + Wb[(8 * wrp + c) * WST + l];
+        }
+      }
+    }
+  }
 }
