@@ -119,6 +119,76 @@ struct __align__(16) CChunk {
   int32_t cnt;  // cv | cs << 8 | cf << 16
 };
 
+// values only (cut-face points need no in-face derivatives)
+template <int N>
+__device__ __forceinline__ void basis_v_sym(const RefTab &R, double x, double (&v)[N]) {
+  const double t = fma(2.0, x, -1.0), t2 = t * t;
+#pragma unroll
+  for (int a = 0; a < (N + 1) / 2; ++a) {
+    double E = 0.0, O = 0.0;
+#pragma unroll
+    for (int k = N - 1; k >= 0; --k) {
+      if (k % 2 == 0) E = fma(E, t2, R.mc[a][k]);
+      else O = fma(O, t2, R.mc[a][k]);
+    }
+    O *= t;
+    v[a] = E + O;
+    if (a != N - 1 - a) v[N - 1 - a] = E - O;
+  }
+}
+
+// One cut-face point of the face with normal axis D (own-side reference
+// coordinates; the normal coordinate is exactly 0 or 1).  Own-side test
+// functions at the point: l_m(face) = delta_{m,fo} along D, l'_m(face) = dw[m],
+// in-face values ls (lower in-face axis), lt (upper).  [u] = J and
+// d u_own + d u_nb = A are interpolated from the face traces; the
+// flux  W [(sigma J - s A/(2h)) phi - (s J/(2h)) d_D phi]  (s = +-1: own side)
+// is a rank-structured update of the n^3 accumulators.
+template <int N, int D, int ACC>
+__device__ __forceinline__ void face_point(double (&acc)[ACC], const RefTab &R, const double *JAB, double xi,
+                                           double eta, double zeta, double W, const KParams &kp) {
+  constexpr int NN = N * N;
+  const double xd = D == 0 ? xi : (D == 1 ? eta : zeta);
+  const int sd = xd == 1.0 ? 1 : 0;
+  double ls[N], lt[N];
+  basis_v_sym<N>(R, D == 0 ? eta : xi, ls);
+  basis_v_sym<N>(R, D == 2 ? eta : zeta, lt);
+  const double *JA = JAB + (2 * D + sd) * 2 * NN, *JB = JA + NN;
+  double J = 0.0, A = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      r0 = fma(ls[i], JA[i + N * j], r0);
+      r1 = fma(ls[i], JB[i + N * j], r1);
+    }
+    J = fma(lt[j], r0, J);
+    A = fma(lt[j], r1, A);
+  }
+  const double sg = sd ? kp.i2h : -kp.i2h;  // sign of the own side / (2h)
+  const double k1 = W * fma(kp.sigma, J, -sg * A), k2 = -W * sg * J;
+  // normal-direction factor T_m = k1 delta_{m,fo} + k2 l'_m(face)
+  double T[N];
+#pragma unroll
+  for (int m = 0; m < N; ++m) T[m] = k2 * (sd ? R.d1[m] : R.d0[m]);
+  if (sd) T[N - 1] += k1;
+  else T[0] += k1;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double P = ls[i] * lt[j];
+#pragma unroll
+      for (int m = 0; m < N; ++m) {
+        // (i, j) run over the in-face axes in ascending order, m along D
+        const int a = D == 0 ? m : i, b = D == 0 ? i : (D == 1 ? m : j), c = D == 2 ? m : j;
+        double &r = acc[(c * N + b) * N + a];
+        r = fma(P, T[m], r);
+      }
+    }
+}
+
 template <int N>
 struct CutPCfg {
   static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
@@ -299,12 +369,12 @@ __global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restric
         nz = p2.y;
         W = p3.x;
       }
-      double vx[N], dvx[N], vy[N], dvy[N], vz[N], dvz[N];
-      basis_vd_sym<N>(R, xi, vx, dvx);
-      basis_vd_sym<N>(R, eta, vy, dvy);
-      basis_vd_sym<N>(R, zeta, vz, dvz);
-      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
       if (kind < 2) {
+        double vx[N], dvx[N], vy[N], dvy[N], vz[N], dvz[N];
+        basis_vd_sym<N>(R, xi, vx, dvx);
+        basis_vd_sym<N>(R, eta, vy, dvy);
+        basis_vd_sym<N>(R, zeta, vz, dvz);
+        double c0 = 0.0, c1, c2, c3;
         double u0, ux, uy, uz;
         eval_u<N>(U, vx, dvx, vy, dvy, vz, dvz, u0, ux, uy, uz);
         if (kind == 1) {
@@ -320,51 +390,28 @@ __global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restric
           c2 = sw * uy;
           c3 = sw * uz;
         }
+#pragma unroll
+        for (int cz = 0; cz < N; ++cz) {
+          const double T0 = fma(c0, vz[cz], c3 * dvz[cz]);
+          const double T1 = c2 * vz[cz];
+          const double T2 = c1 * vz[cz];
+#pragma unroll
+          for (int by = 0; by < N; ++by) {
+            const double S0 = fma(vy[by], T0, dvy[by] * T1);
+            const double S1 = vy[by] * T2;
+#pragma unroll
+            for (int ax = 0; ax < N; ++ax) {
+              double &r = acc[(cz * N + by) * N + ax];
+              r = fma(vx[ax], S0, fma(dvx[ax], S1, r));
+            }
+          }
+        }
       } else if (kind == 2) {
-        // the face: the coordinate that is exactly 0 or 1
+        // cut-face point: the face is the coordinate that is exactly 0 or 1
         const int d = (xi == 0.0 || xi == 1.0) ? 0 : ((eta == 0.0 || eta == 1.0) ? 1 : 2);
-        const int sd = (d == 0 ? xi : (d == 1 ? eta : zeta)) == 1.0 ? 1 : 0;
-        const double *JA = JAB + (2 * d + sd) * 2 * NN, *JB = JA + NN;
-        double ls[N], lt[N];  // in-face bases along e1 < e2
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-          ls[i] = d == 0 ? vy[i] : vx[i];
-          lt[i] = d == 2 ? vy[i] : vz[i];
-        }
-        double J = 0.0, A = 0.0;
-#pragma unroll
-        for (int jj = 0; jj < N; ++jj) {
-          double r0 = 0.0, r1 = 0.0;
-#pragma unroll
-          for (int i = 0; i < N; ++i) {
-            r0 = fma(ls[i], JA[i + N * jj], r0);
-            r1 = fma(ls[i], JB[i + N * jj], r1);
-          }
-          J = fma(lt[jj], r0, J);
-          A = fma(lt[jj], r1, A);
-        }
-        const double sg = sd ? kp.i2h : -kp.i2h;  // sign of the own side / (2h)
-        const double k1 = W * fma(kp.sigma, J, -sg * A), k2 = -W * sg * J;
-        c0 = k1;
-        c1 = d == 0 ? k2 : 0.0;
-        c2 = d == 1 ? k2 : 0.0;
-        c3 = d == 2 ? k2 : 0.0;
-      }
-#pragma unroll
-      for (int cz = 0; cz < N; ++cz) {
-        const double T0 = fma(c0, vz[cz], c3 * dvz[cz]);
-        const double T1 = c2 * vz[cz];
-        const double T2 = c1 * vz[cz];
-#pragma unroll
-        for (int by = 0; by < N; ++by) {
-          const double S0 = fma(vy[by], T0, dvy[by] * T1);
-          const double S1 = vy[by] * T2;
-#pragma unroll
-          for (int ax = 0; ax < N; ++ax) {
-            double &r = acc[(cz * N + by) * N + ax];
-            r = fma(vx[ax], S0, fma(dvx[ax], S1, r));
-          }
-        }
+        if (d == 0) face_point<N, 0>(acc, R, JAB, xi, eta, zeta, W, kp);
+        else if (d == 1) face_point<N, 1>(acc, R, JAB, xi, eta, zeta, W, kp);
+        else face_point<N, 2>(acc, R, JAB, xi, eta, zeta, W, kp);
       }
       __syncwarp();  // every lane is done with ring slot b before it is refilled
       if (lane == 0) fence_proxy_async();
