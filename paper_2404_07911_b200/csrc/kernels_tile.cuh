@@ -719,11 +719,37 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
   }
   __syncthreads();
   uint32_t it = 0;
+  const int wrp = tid >> 5, ln32 = tid & 31;
+  constexpr int PER = (N3 + 31) / 32;  // elements of a block per lane in the write-back
+  // tile record fields, prefetched one tile ahead
+  int nx_nslot = 0, nx_ncell = 0, nx_bl = 0;
+  uint2 nx_ln = make_uint2(0, 0);
+  auto fetch = [&](int tl) {
+    const TileRec<C::SMAX> *T = tiles + tl;
+    nx_nslot = T->nslot;
+    nx_ncell = T->ncell;
+    nx_ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[cell][0]);
+    nx_bl = (ln32 < 8 && 8 * wrp + ln32 < nx_ncell) ? T->blk[8 * wrp + ln32] : 0;
+  };
+  if ((int)blockIdx.x < ntiles) fetch(blockIdx.x);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const TileRec<C::SMAX> *T = tiles + tile;
-    const int nslot = T->nslot, ncell = T->ncell;
+    const int nslot = nx_nslot, ncell = nx_ncell, bl = nx_bl;
     const bool on = cell < ncell;
-    const uint2 ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[cell][0]);
+    const uint2 ln = nx_ln;
+    // the v rows this warp adds to, loaded now and consumed at the end of the tile
+    double xv[8][PER];
+    size_t o[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      o[c] = (size_t)__shfl_sync(0xffffffffu, bl, c) * N3;
+      const bool cv = 8 * wrp + c < ncell;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int l = ln32 + 32 * k;
+        xv[c][k] = (cv && l < N3) ? v[o[c] + l] : 0.0;
+      }
+    }
     // ---- stage the tile's blocks
     if constexpr (C::BULK) {
       fence_proxy_async();
@@ -740,6 +766,7 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
     }
     double *W = Wb + cell * WST;
     for (int l = r; l < N3; l += 4) W[l] = 0.0;
+    if (tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
     if constexpr (C::BULK) mbar_wait(bar, it & 1);
     __syncthreads();
     int nbs[6];
@@ -831,31 +858,14 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
       __syncwarp();
     });
     __syncthreads();  // all w final; all slot reads done (the next tile's copies may start)
-    // ---- v += w: each warp its 8 cells, all loads in flight before the adds
-    {
-      const int wrp = tid >> 5, ln32 = tid & 31;
-      const int bl = (ln32 < 8 && 8 * wrp + ln32 < ncell) ? T->blk[8 * wrp + ln32] : 0;
-      constexpr int PER = (N3 + 31) / 32;  // elements of a block per lane
-      double x[8][PER];
-      size_t o[8];
+    // ---- v += w (the warp's 8 cells; v rows were loaded at the start of the tile)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        o[c] = (size_t)__shfl_sync(0xffffffffu, bl, c) * N3;
-        const bool cv = 8 * wrp + c < ncell;
+    for (int c = 0; c < 8; ++c) {
+      const bool cv = 8 * wrp + c < ncell;
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          const int l = ln32 + 32 * k;
-          x[c][k] = (cv && l < N3) ? v[o[c] + l] : 0.0;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const bool cv = 8 * wrp + c < ncell;
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          const int l = ln32 + 32 * k;
-          if (cv && l < N3) v[o[c] + l] = x[c][k] + Wb[(8 * wrp + c) * WST + l];
-        }
+      for (int k = 0; k < PER; ++k) {
+        const int l = ln32 + 32 * k;
+        if (cv && l < N3) v[o[c] + l] = xv[c][k] + Wb[(8 * wrp + c) * WST + l];
       }
     }
   }
