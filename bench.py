@@ -338,6 +338,33 @@ def run_ours(args, P, cfg, rank, world, local_rank):
         except Exception as e:  # the comparison path must not hide the main number
             line["csr"] = {"error": str(e)[:200]}
 
+    if args.cg > 0:
+        # BASELINE configs[4]: unpreconditioned CG on f = 1 (Dirichlet zero via Nitsche), all in the
+        # library's kernels; timed on the device (max over ranks), L2 not flushed between iterations
+        b = op.rhs_const(1.0)
+        x = torch.zeros(op.n_ext_dofs, dtype=torch.float64, device=dev)
+        op.cg(b, x, iters=2)  # warm-up (work vectors)
+        x.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        x, hist = op.cg(b, x, iters=args.cg)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        cg_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([cg_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            cg_ms = float(t.item())
+        line["cg"] = {"iters": int(len(hist) - 1), "ms": cg_ms, "ms_per_iter": cg_ms / max(len(hist) - 1, 1),
+                      "applies_per_s": (len(hist) - 1) / (cg_ms * 1e-3),
+                      "res0": float(hist[0]), "res_final": float(hist[-1]),
+                      "apply_share": ms_step * (len(hist) - 1) / cg_ms,
+                      "what": "unpreconditioned CG, f = 1, x0 = 0; rhs + dots + axpys in library kernels, "
+                              "dots all-reduced over ranks"}
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nb, dt = oracle_sample(P, args.cpu_s)
         line["cpu_baseline"] = {"value": nb * (P.degree + 1) ** 3 / dt, "unit": UNIT, "cores": cpu_threads(),
@@ -362,6 +389,7 @@ def main():
     ap.add_argument("--cpu-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=3.0)
     ap.add_argument("--w-cut", type=float, default=7.0, help="slab-balance weight of a cut cell (uncut = 1)")
+    ap.add_argument("--cg", type=int, default=0, help="also time this many CG iterations (C5: 50)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -171,6 +171,28 @@ int cutfem_setup_dist(const cutfem_problem *global_pb, int32_t x_begin, int32_t 
                       const void *nccl_id, int device, cutfem_handle **out);
 int cutfem_dist_info(const cutfem_handle *hd, int64_t *n_own_blocks, int64_t *n_ghost_lo, int64_t *n_ghost_hi);
 
+/* ---- Solver loop around the operator (C5: BASELINE.json configs[4]).
+ *
+ * cutfem_rhs_const: b_i = f * int_Ω phi_i (PAPER §2.1 P:78 right-hand side for a
+ * constant source; with g = 0 on Γ the Nitsche data terms vanish): the tensor
+ * (p+1)-point Gauss rule on uncut cells, the cell's volume rule on cut cells.
+ * b_dev: device, n_dofs doubles (owned blocks), overwritten.  Stream ordered.
+ *
+ * cutfem_cg: unpreconditioned conjugate gradients on A x = b (the iterative
+ * solver the operator evaluation serves), x0 = x_dev (in/out, the
+ * owned blocks; a distributed handle needs room for the ghost blocks too).
+ * Runs exactly `iters` iterations, or stops early once ||r|| <= tol ||b|| when
+ * tol > 0.  All vector work (dots, axpys) runs in the library's kernels with the
+ * CG scalars kept on the device; dot products are reduced deterministically
+ * (fixed-order two-level sum) and, on distributed handles, summed across ranks
+ * by ncclAllReduce (two per iteration).  res_hist (host, may be NULL): >= iters+1
+ * entries, receives ||r_k||_2, k = 0..done.  iters_done (may be NULL) receives
+ * the number of iterations run.  Work vectors are owned by the handle.  The call
+ * synchronises the stream once at the end. */
+int cutfem_rhs_const(cutfem_handle *hd, double f, double *b_dev, void *cuda_stream);
+int cutfem_cg(cutfem_handle *hd, const double *b_dev, double *x_dev, int iters, double tol, double *res_hist,
+              int *iters_done, void *cuda_stream);
+
 int cutfem_stats(const cutfem_handle *hd, cutfem_stats_t *out);
 const char *cutfem_last_error(void);
 int cutfem_destroy(cutfem_handle *hd);

@@ -82,7 +82,7 @@ EXPORTS = ["cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_
            "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_nnz", "cutfem_csr_download",
            "cutfem_stats", "cutfem_last_error", "cutfem_destroy", "cutfem_partition_x",
            "cutfem_local_build", "cutfem_local_free", "cutfem_nccl_unique_id", "cutfem_setup_dist",
-           "cutfem_dist_info"]
+           "cutfem_dist_info", "cutfem_rhs_const", "cutfem_cg"]
 
 
 class _Local(ctypes.Structure):
@@ -114,6 +114,8 @@ def load(path: str | None = None):
     L.cutfem_csr_nnz.restype = i64
     L.cutfem_csr_download.argtypes = [vp, vp, vp, vp]
     L.cutfem_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+    L.cutfem_rhs_const.argtypes = [vp, ctypes.c_double, vp, vp]
+    L.cutfem_cg.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_double, vp, ctypes.POINTER(ctypes.c_int), vp]
     L.cutfem_last_error.restype = ctypes.c_char_p
     L.cutfem_destroy.argtypes = [vp]
     L.cutfem_partition_x.argtypes = [ctypes.POINTER(_Problem), ctypes.c_int, ctypes.c_double, vp]
@@ -305,6 +307,27 @@ class CutFEM:
         _check(self._L.cutfem_apply_host(self._h, u.ctypes.data, v.ctypes.data,
                                          _stream_ptr(stream) if stream else None))
         return v
+
+    def rhs_const(self, f: float = 1.0, b=None, stream=None):
+        """b = f * int_Omega phi_i (device, owned blocks)."""
+        import torch
+        if b is None:
+            b = torch.empty(self.n_dofs, dtype=torch.float64, device=f"cuda:{self.device}")
+        _check(self._L.cutfem_rhs_const(self._h, float(f), b.data_ptr(), _stream_ptr(stream)))
+        return b
+
+    def cg(self, b, x=None, iters: int = 50, tol: float = 0.0, stream=None):
+        """Unpreconditioned CG on A x = b in the library's kernels; x (in/out) needs
+        n_ext_dofs entries.  Returns (x, residual norms ||r_k||, k = 0..done)."""
+        import torch
+        if x is None:
+            x = torch.zeros(self.n_ext_dofs, dtype=torch.float64, device=b.device)
+        assert x.numel() == self.n_ext_dofs and b.numel() == self.n_dofs
+        hist = np.zeros(int(iters) + 1, dtype=np.float64)
+        done = ctypes.c_int()
+        _check(self._L.cutfem_cg(self._h, b.data_ptr(), x.data_ptr(), int(iters), float(tol), hist.ctypes.data,
+                                 ctypes.byref(done), _stream_ptr(stream)))
+        return x, hist[:done.value + 1]
 
     def csr_assemble(self) -> int:
         nnz = ctypes.c_int64()

@@ -1,0 +1,284 @@
+// cg.inl — right-hand side and the CG loop around the operator (included by
+// cutfem.cu; C ABI in include/cutfem.h).  BASELINE.json configs[4]: 50
+// unpreconditioned CG iterations on f = 1 with Dirichlet zero via Nitsche.
+//
+// All vector work runs in these kernels; the CG scalars stay on the device
+// (rr[k] = ||r_k||^2, pq[k] = p_k . A p_k), so an iteration needs no host sync.
+// Dot products: fixed grid, per-block tree sums, one final block summing the
+// partials in order -> bitwise reproducible; on a distributed handle each dot is
+// then summed over ranks with ncclAllReduce (two per iteration).
+
+namespace {
+
+constexpr int CG_BLOCKS = 296;  // 2 per SM: fixed, so reductions are reproducible
+constexpr int CG_THREADS = 256;
+
+__device__ __forceinline__ double block_sum(double x, double *sh) {
+  const int t = threadIdx.x;
+  sh[t] = x;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (t < s) sh[t] += sh[t + s];
+    __syncthreads();
+  }
+  return sh[0];
+}
+
+// partial[b] = sum over this block's grid-stride range of a_i * b_i
+__global__ void __launch_bounds__(CG_THREADS) k_dot(const double *__restrict__ a, const double *__restrict__ b,
+                                                    int64_t n, double *__restrict__ partial) {
+  __shared__ double sh[CG_THREADS];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * CG_THREADS)
+    s = fma(a[i], b[i], s);
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(CG_THREADS) k_dot_final(const double *__restrict__ partial, int np,
+                                                          double *__restrict__ out) {
+  __shared__ double sh[CG_THREADS];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += CG_THREADS) s += partial[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// x += alpha p, r -= alpha q (alpha = rr[k] / pq[k]); partial sums of |r|^2
+__global__ void __launch_bounds__(CG_THREADS) k_cg_xr(double *__restrict__ x, double *__restrict__ r,
+                                                      const double *__restrict__ p, const double *__restrict__ q,
+                                                      int64_t n, const double *__restrict__ rr,
+                                                      const double *__restrict__ pq, int k,
+                                                      double *__restrict__ partial) {
+  __shared__ double sh[CG_THREADS];
+  const double alpha = rr[k] / pq[k];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * CG_THREADS) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// p = r + beta p, beta = rr[k+1] / rr[k]
+__global__ void __launch_bounds__(CG_THREADS) k_cg_p(double *__restrict__ p, const double *__restrict__ r, int64_t n,
+                                                     const double *__restrict__ rr, int k) {
+  const double beta = rr[k + 1] / rr[k];
+  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * CG_THREADS)
+    p[i] = fma(beta, p[i], r[i]);
+}
+
+// r = b - q, p = r, partial sums of |r|^2
+__global__ void __launch_bounds__(CG_THREADS) k_cg_init(double *__restrict__ r, double *__restrict__ p,
+                                                        const double *__restrict__ b, const double *__restrict__ q,
+                                                        int64_t n, double *__restrict__ partial) {
+  __shared__ double sh[CG_THREADS];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * CG_THREADS) {
+    const double ri = b[i] - q[i];
+    r[i] = ri;
+    p[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// ---- right-hand side b = f int_Ω phi_i
+struct RhsTab {
+  double m[CUTFEM_NMAX];  // int_0^1 l_a = sum_q w_q l_a(g_q)
+  double x[CUTFEM_NMAX];  // GLL nodes
+  double cinv[CUTFEM_NMAX];
+};
+
+// uncut cells: b = f h^3 m_a m_b m_c (tensor Gauss, exact)
+__global__ void k_rhs_uncut(double *__restrict__ b, const UDesc *__restrict__ desc, int64_t ncell, int n, double fh3,
+                            RhsTab t) {
+  const int n3 = n * n * n;
+  const int64_t total = ncell * n3;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / n3;
+    const int l = (int)(e - c * n3);
+    const int a = l % n, bb = (l / n) % n, cc = l / (n * n);
+    b[(size_t)desc[c].blk * n3 + l] = fh3 * t.m[a] * t.m[bb] * t.m[cc];
+  }
+}
+
+// cut cells (one CTA per cell): b_l = f sum_q W_q phi_l(x_q) over the volume rule;
+// 1-D bases of a point chunk staged in shared memory
+__global__ void __launch_bounds__(128) k_rhs_cut(double *__restrict__ b, const CDesc *__restrict__ desc,
+                                                 const double *__restrict__ vol, int n, double f, RhsTab t) {
+  __shared__ double bas[128][3][CUTFEM_NMAX];
+  __shared__ double wq[128];
+  const CDesc d = desc[blockIdx.x];
+  const int n3 = n * n * n;
+  double acc[6] = {0, 0, 0, 0, 0, 0};  // n^3 <= 729 -> <= 6 per thread
+  for (int64_t q0 = 0; q0 < d.nv; q0 += 128) {
+    const int cnt = (int)min((int64_t)128, (int64_t)d.nv - q0);
+    if (threadIdx.x < cnt) {
+      const double *pq = vol + 4 * (d.vb + q0 + threadIdx.x);
+      for (int dim = 0; dim < 3; ++dim) {
+        const double xv = pq[dim];
+        for (int a = 0; a < n; ++a) {
+          double prod = t.cinv[a];
+          for (int m = 0; m < n; ++m)
+            if (m != a) prod *= xv - t.x[m];
+          bas[threadIdx.x][dim][a] = prod;
+        }
+      }
+      wq[threadIdx.x] = pq[3];
+    }
+    __syncthreads();
+    for (int k = 0; k < 6; ++k) {
+      const int l = threadIdx.x + 128 * k;
+      if (l >= n3) break;
+      const int a = l % n, bb = (l / n) % n, cc = l / (n * n);
+      double s = acc[k];
+      for (int q = 0; q < cnt; ++q) s = fma(wq[q] * bas[q][0][a], bas[q][1][bb] * bas[q][2][cc], s);
+      acc[k] = s;
+    }
+    __syncthreads();
+  }
+  for (int k = 0; k < 6; ++k) {
+    const int l = threadIdx.x + 128 * k;
+    if (l < n3) b[(size_t)d.blk * n3 + l] = f * acc[k];
+  }
+}
+
+}  // namespace
+
+struct cutfem_cg_work {
+  double *r = nullptr, *p = nullptr, *q = nullptr, *partial = nullptr, *rr = nullptr, *pq = nullptr;
+  int cap = 0;  // iterations the scalar arrays hold
+};
+
+void cg_free(cutfem_cg_work *w) {
+  if (!w) return;
+  cudaFree(w->r);
+  cudaFree(w->p);
+  cudaFree(w->q);
+  cudaFree(w->partial);
+  cudaFree(w->rr);
+  cudaFree(w->pq);
+  delete w;
+}
+
+namespace {
+
+int cg_reduce(cutfem_handle *hd, double *partial, double *out, cudaStream_t st) {
+  k_dot_final<<<1, CG_THREADS, 0, st>>>(partial, CG_BLOCKS, out);
+  CU(cudaGetLastError());
+  if (hd->dist && hd->nranks > 1) {
+    ncclResult_t r = ncclAllReduce(out, out, 1, ncclDouble, ncclSum, (ncclComm_t)hd->comm, st);
+    if (r != ncclSuccess) return fail(CUTFEM_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cutfem_rhs_const(cutfem_handle *hd, double f, double *b_dev, void *cuda_stream) {
+  if (!hd) return fail(CUTFEM_EINVAL, "null handle");
+  if (hd->stats.n_dofs > 0 && !b_dev) return fail(CUTFEM_EINVAL, "null vector");
+  CU(cudaSetDevice(hd->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int n = hd->n, p = hd->degree;
+  cutfem_tables::Ref r = cutfem_tables::build(p);
+  RhsTab t;
+  std::memset(&t, 0, sizeof(t));
+  for (int a = 0; a < n; ++a) {
+    long double m = 0;
+    for (int q = 0; q < n; ++q) m += r.w[q] * cutfem_tables::lag(r.x, a, r.g[q]);
+    t.m[a] = (double)m;
+    t.x[a] = (double)r.x[a];
+    t.cinv[a] = (double)r.cinv[a];
+  }
+  const double h = hd->h;
+  if (hd->n_uncut > 0) {
+    const int64_t total = hd->n_uncut * (int64_t)n * n * n;
+    const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 8 * hd->sm_count);
+    k_rhs_uncut<<<grid, 256, 0, st>>>(b_dev, hd->d_udesc, hd->n_uncut, n, f * h * h * h, t);
+    CU(cudaGetLastError());
+  }
+  if (hd->n_cut > 0) {
+    k_rhs_cut<<<(unsigned)hd->n_cut, 128, 0, st>>>(b_dev, hd->d_cdesc, hd->d_vol, n, f, t);
+    CU(cudaGetLastError());
+  }
+  return 0;
+}
+
+int cutfem_cg(cutfem_handle *hd, const double *b_dev, double *x_dev, int iters, double tol, double *res_hist,
+              int *iters_done, void *cuda_stream) {
+  if (!hd) return fail(CUTFEM_EINVAL, "null handle");
+  if (iters < 0) return fail(CUTFEM_EINVAL, "iters < 0");
+  if (hd->stats.n_dofs > 0 && (!b_dev || !x_dev)) return fail(CUTFEM_EINVAL, "null vector");
+  CU(cudaSetDevice(hd->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int64_t n = hd->stats.n_dofs, next = hd->stats.n_ext_dofs;
+  if (!hd->cg) hd->cg = new cutfem_cg_work();
+  cutfem_cg_work &w = *hd->cg;
+  if (!w.r) {
+    CU(cudaMalloc(&w.r, sizeof(double) * std::max<int64_t>(n, 1)));
+    CU(cudaMalloc(&w.p, sizeof(double) * std::max<int64_t>(next, 1)));  // ghost room for the apply
+    CU(cudaMalloc(&w.q, sizeof(double) * std::max<int64_t>(n, 1)));
+    CU(cudaMalloc(&w.partial, sizeof(double) * CG_BLOCKS));
+    hd->dev_bytes += (int64_t)sizeof(double) * (2 * n + next + CG_BLOCKS);
+  }
+  if (w.cap < iters + 1) {
+    cudaFree(w.rr);
+    cudaFree(w.pq);
+    w.cap = iters + 1;
+    CU(cudaMalloc(&w.rr, sizeof(double) * (w.cap + 1)));
+    CU(cudaMalloc(&w.pq, sizeof(double) * (w.cap + 1)));
+  }
+  int rc;
+  // r0 = b - A x0, p0 = r0, rr[0] = |r0|^2
+  if ((rc = dispatch_apply(hd, x_dev, w.q, st))) return rc;
+  k_cg_init<<<CG_BLOCKS, CG_THREADS, 0, st>>>(w.r, w.p, b_dev, w.q, n, w.partial);
+  CU(cudaGetLastError());
+  if ((rc = cg_reduce(hd, w.partial, w.rr, st))) return rc;
+  double bb = 0.0;
+  if (tol > 0) {
+    k_dot<<<CG_BLOCKS, CG_THREADS, 0, st>>>(b_dev, b_dev, n, w.partial);
+    if ((rc = cg_reduce(hd, w.partial, w.pq + w.cap, st))) return rc;
+    CU(cudaMemcpyAsync(&bb, w.pq + w.cap, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
+  int k = 0;
+  for (; k < iters; ++k) {
+    if ((rc = dispatch_apply(hd, w.p, w.q, st))) return rc;  // q = A p (halo exchange inside)
+    k_dot<<<CG_BLOCKS, CG_THREADS, 0, st>>>(w.p, w.q, n, w.partial);
+    if ((rc = cg_reduce(hd, w.partial, w.pq + k, st))) return rc;
+    k_cg_xr<<<CG_BLOCKS, CG_THREADS, 0, st>>>(x_dev, w.r, w.p, w.q, n, w.rr, w.pq, k, w.partial);
+    CU(cudaGetLastError());
+    if ((rc = cg_reduce(hd, w.partial, w.rr + k + 1, st))) return rc;
+    k_cg_p<<<CG_BLOCKS, CG_THREADS, 0, st>>>(w.p, w.r, n, w.rr, k);
+    CU(cudaGetLastError());
+    if (tol > 0) {
+      double rk = 0.0;
+      CU(cudaMemcpyAsync(&rk, w.rr + k + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      if (std::sqrt(rk) <= tol * std::sqrt(bb)) {
+        ++k;
+        break;
+      }
+    }
+  }
+  if (res_hist) {
+    std::vector<double> h2(k + 1);
+    CU(cudaMemcpyAsync(h2.data(), w.rr, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int i = 0; i <= k; ++i) res_hist[i] = std::sqrt(h2[i]);
+  } else {
+    CU(cudaStreamSynchronize(st));
+  }
+  if (iters_done) *iters_done = k;
+  return 0;
+}
+
+}  // extern "C"

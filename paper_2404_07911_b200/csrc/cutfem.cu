@@ -43,6 +43,9 @@ int fail(int code, const std::string &msg) {
 
 }  // namespace
 
+struct cutfem_cg_work;                    // cg.inl
+void cg_free(cutfem_cg_work *w);
+
 struct cutfem_handle {
   int device = 0;
   int degree = 1;
@@ -104,6 +107,7 @@ struct cutfem_handle {
   std::vector<uint8_t> color;  // (i + 2j + 3k) mod 7, distance-2 colouring for CSR probing
   cutfem_stats_t stats;
   int64_t dev_bytes = 0;
+  cutfem_cg_work *cg = nullptr;  // CG work vectors (lazy)
 };
 
 namespace {
@@ -461,6 +465,9 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_cutp, k_cutp<N>, 32 * CutPCfg<N>::WARPS,
                                                      CutPCfg<N>::SMEM));
     hd->occ_cutp = std::max(1, hd->occ_cutp);
+    // CTAs of k_cutp per SM (env CUTFEM_CUTP_CTAS): fewer leaves room for the
+    // concurrent uncut-cell kernel on every SM
+    if (const char *e = std::getenv("CUTFEM_CUTP_CTAS")) hd->occ_cutp = std::max(1, std::min(hd->occ_cutp, std::atoi(e)));
     // per part: longest-processing-time assignment of the cells to the warps of
     // the launch (cost ~ point chunks + a fixed per-cell part), cells of a warp
     // stored contiguously, heaviest first
@@ -763,6 +770,7 @@ void free_handle(cutfem_handle *hd) {
   if (!hd) return;
   cudaFree(hd->d_udesc);
   cudaFree(hd->d_tiles);
+  cg_free(hd->cg);
   cudaFree(hd->d_cdesc2);
   cudaFree(hd->d_wstart);
   cudaFree(hd->d_kstart);
@@ -1144,3 +1152,4 @@ int cutfem_destroy(cutfem_handle *hd) {
 
 #include "csr.inl"
 #include "dist.inl"
+#include "cg.inl"

@@ -253,3 +253,42 @@ def test_gyroid_box_boundary(cf, cutgen_mod, p):
     u = P.seeded_u(21)
     v, _ = gpu_apply(cf, P, u)
     check(P, v, u)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "gyroid"])
+def test_rhs_const_matches_oracle(cf, cutgen_mod, cfg):
+    """b = f int_Omega phi_i vs the oracle's quadrature sum."""
+    P = cutgen_mod.config("C1") if cfg == "C1" else cutgen_mod.generate(cutgen_mod.GYROID, 8, 0.0, 1.0, 3)
+    op = cf.CutFEM(P)
+    b = op.rhs_const(2.5).cpu().numpy()
+    bo = Oracle(P).rhs(lambda x: 2.5 * np.ones(len(x)))
+    assert np.abs(b - bo).max() <= 1e-13 * np.abs(bo).max()
+    # sum of b = f |Omega| (partition of unity); cross-check with the volume weights
+    vol = P.vol_pts[:, 3].sum() + P.h ** 3 * (P.n_active - P.n_cut)
+    assert abs(b.sum() - 2.5 * vol) <= 1e-12 * 2.5 * vol
+
+
+def test_cg_matches_oracle_cg(cf, cutgen_mod):
+    """30 unpreconditioned CG iterations in the library's kernels vs the oracle's
+    CG on its own operator: the same iterates up to rounding growth."""
+    from oracle.operator import cg as oracle_cg
+    P = cutgen_mod.config("C1")
+    op = cf.CutFEM(P)
+    b = op.rhs_const(1.0)
+    x, hist = op.cg(b, iters=30)
+    O = Oracle(P)
+    xo, it = oracle_cg(O.apply, b.cpu().numpy(), tol=0.0, maxiter=30)
+    assert len(hist) == 31 and it == 30
+    xg = x.cpu().numpy()
+    assert np.abs(xg - xo).max() <= 1e-8 * np.abs(xo).max()
+    r = b - op.apply(x)
+    assert abs(float(r.norm()) - hist[-1]) <= 1e-8 * hist[0]
+
+
+def test_cg_tolerance_stop(cf, cutgen_mod):
+    P = cutgen_mod.config("C1")
+    op = cf.CutFEM(P)
+    b = op.rhs_const(1.0)
+    x, hist = op.cg(b, iters=2000, tol=1e-9)
+    assert hist[-1] <= 1e-9 * float(b.norm()) and len(hist) < 2001
+    assert float((b - op.apply(x)).norm()) <= 1e-8 * float(b.norm())
