@@ -10,7 +10,7 @@
 
 namespace {
 
-constexpr int CG_BLOCKS = 296;  // 2 per SM: fixed, so reductions are reproducible
+constexpr int CG_BLOCKS = 1184;  // 8 per SM: fixed, so reductions are reproducible
 constexpr int CG_THREADS = 256;
 
 __device__ __forceinline__ double block_sum(double x, double *sh) {
@@ -24,13 +24,17 @@ __device__ __forceinline__ double block_sum(double x, double *sh) {
   return sh[0];
 }
 
-// partial[b] = sum over this block's grid-stride range of a_i * b_i
+// partial[b] = sum over this block's grid-stride range of a_i * b_i (n even: every
+// block has n^3 >= 8 entries; 16-byte accesses)
 __global__ void __launch_bounds__(CG_THREADS) k_dot(const double *__restrict__ a, const double *__restrict__ b,
                                                     int64_t n, double *__restrict__ partial) {
   __shared__ double sh[CG_THREADS];
   double s = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * CG_THREADS)
-    s = fma(a[i], b[i], s);
+  const double2 *a2 = reinterpret_cast<const double2 *>(a), *b2 = reinterpret_cast<const double2 *>(b);
+  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n / 2; i += (int64_t)gridDim.x * CG_THREADS) {
+    const double2 x = a2[i], y = b2[i];
+    s = fma(x.x, y.x, fma(x.y, y.y, s));
+  }
   s = block_sum(s, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
@@ -53,11 +57,14 @@ __global__ void __launch_bounds__(CG_THREADS) k_cg_xr(double *__restrict__ x, do
   __shared__ double sh[CG_THREADS];
   const double alpha = rr[k] / pq[k];
   double s = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * CG_THREADS) {
-    x[i] = fma(alpha, p[i], x[i]);
-    const double ri = fma(-alpha, q[i], r[i]);
-    r[i] = ri;
-    s = fma(ri, ri, s);
+  double2 *x2 = reinterpret_cast<double2 *>(x), *r2 = reinterpret_cast<double2 *>(r);
+  const double2 *p2 = reinterpret_cast<const double2 *>(p), *q2 = reinterpret_cast<const double2 *>(q);
+  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n / 2; i += (int64_t)gridDim.x * CG_THREADS) {
+    const double2 xi = x2[i], pi = p2[i], qi = q2[i], ri0 = r2[i];
+    x2[i] = make_double2(fma(alpha, pi.x, xi.x), fma(alpha, pi.y, xi.y));
+    const double2 ri = make_double2(fma(-alpha, qi.x, ri0.x), fma(-alpha, qi.y, ri0.y));
+    r2[i] = ri;
+    s = fma(ri.x, ri.x, fma(ri.y, ri.y, s));
   }
   s = block_sum(s, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
@@ -67,8 +74,12 @@ __global__ void __launch_bounds__(CG_THREADS) k_cg_xr(double *__restrict__ x, do
 __global__ void __launch_bounds__(CG_THREADS) k_cg_p(double *__restrict__ p, const double *__restrict__ r, int64_t n,
                                                      const double *__restrict__ rr, int k) {
   const double beta = rr[k + 1] / rr[k];
-  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * CG_THREADS)
-    p[i] = fma(beta, p[i], r[i]);
+  double2 *p2 = reinterpret_cast<double2 *>(p);
+  const double2 *r2 = reinterpret_cast<const double2 *>(r);
+  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n / 2; i += (int64_t)gridDim.x * CG_THREADS) {
+    const double2 pi = p2[i], ri = r2[i];
+    p2[i] = make_double2(fma(beta, pi.x, ri.x), fma(beta, pi.y, ri.y));
+  }
 }
 
 // r = b - q, p = r, partial sums of |r|^2
