@@ -410,7 +410,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       c.gp = d.flags & nbm & 0x3fu;
       c.sipg = (d.flags >> 6) & nbm & 0x3fu;  // structured (full, uncut) faces of the cut cell
       c.vol = false;
-      if (c.gp | c.sipg) set[1][pt - 1].push_back(c);
+      (void)c;  // cut cells: their structured faces are done inside k_cutp
     }
   }
   const int64_t rs = (int64_t)sizeof(TileRec<C::SMAX>);
@@ -445,9 +445,12 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       e.ns = d.ns;
       e.fb = (int64_t)fac.size() / 4;
       for (int f = 0; f < 6; ++f) {
-        e.nb[f] = -1;
+        e.nb[f] = d.nb[f] >= 0 ? d.nb[f] : -1;
+        if (d.nb[f] >= 0) {
+          if (d.flags & (1u << f)) e.smask |= 1u << f;               // ghost penalty (the cell is cut)
+          if (d.flags & (1u << (6 + f))) e.smask |= 1u << (8 + f);   // full face inside Omega: SIPG
+        }
         if (!((d.flags >> (12 + f)) & 1u) || d.nb[f] < 0) continue;
-        e.nb[f] = d.nb[f];
         e.fmask |= 1u << f;
         const int dd = f >> 1, e1 = dd == 0 ? 1 : 0, e2 = dd == 2 ? 1 : 2;
         for (int64_t q = pb->sf_ptr[d.sf[f]]; q < pb->sf_ptr[d.sf[f] + 1]; ++q) {
@@ -560,9 +563,9 @@ int dispatch_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vecto
   return 0;
 }
 
-// N <= 4: k_cutp (cut cells: points and cut faces, v = ...) on the side stream
-// concurrently with k_tile*<0> (uncut cells: volume + SIPG, v = ...); once both
-// have written, k_gpw adds the ghost penalty and the cut cells' full-face SIPG.
+// N <= 4: k_cutp (cut cells: every term, v = ...) on the side stream,
+// concurrently with k_tile*<0> (uncut cells: volume + SIPG, v = ...) followed by
+// k_gpw (uncut cells next to cut cells: + ghost penalty, v += ...).
 template <int N>
 int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which, int part) {
   constexpr int NT = (N <= 4 ? N : 4);
@@ -583,7 +586,8 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
       if (hd->grid_cutp[pt] <= 0) continue;
       k_cutp<NT><<<hd->grid_cutp[pt], 32 * CP::WARPS, CP::SMEM, fork ? hd->side : st>>>(
           u, v, hd->d_cdesc2 + hd->r_off[pt][2], hd->d_chunks, hd->d_vol, hd->d_srf, hd->d_fac,
-          hd->d_wstart + hd->w_off[pt], hd->d_kstart + hd->w_off[pt], hd->kp);
+          hd->d_wstart + hd->w_off[pt], hd->d_kstart + hd->w_off[pt], hd->kp,
+          *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data()));
     }
     CU(cudaGetLastError());
   }
@@ -598,15 +602,15 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
       k_tile<NT, 0><<<grid, 32, C::SMEM, st>>>(u, v, tl + hd->t_off[0][part], (int)n0, tt, hd->kp.mask);
     CU(cudaGetLastError());
   }
-  if (fork) {
-    CU(cudaEventRecord(hd->ev_join, hd->side));
-    CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
-  }
-  if (n1 > 0) {
+  if (n1 > 0) {  // uncut cells next to cut cells: + ghost penalty (needs only k_tile*<0>)
     const unsigned grid = (unsigned)(hd->persist & 2 ? std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count) : n1);
     k_gpw<NT><<<grid, GpwCfg<NT>::THREADS, GpwCfg<NT>::SMEM, st>>>(u, v, tl + hd->t_off[1][part], (int)n1, tt,
                                                                   hd->kp.mask);
     CU(cudaGetLastError());
+  }
+  if (fork) {
+    CU(cudaEventRecord(hd->ev_join, hd->side));
+    CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
   }
   return 0;
 }

@@ -30,10 +30,11 @@
 
 struct __align__(16) CDesc2 {
   int32_t blk;
-  int32_t nb[6];     // neighbour block of each cut face with points, else -1
+  int32_t nb[6];     // neighbour block of each face with work, else -1
   uint32_t fmask;    // bit f: cut face f with points
   int64_t vb, sb, fb;  // first volume / interface / cut-face point of the cell
-  int32_t nv, ns, nf, pad;
+  int32_t nv, ns, nf;
+  uint32_t smask;    // bits 0-5: ghost-penalty faces, bits 8-13: full-face SIPG faces
 };
 
 // value + reference gradient at a point from the unpadded block U (16-byte
@@ -201,7 +202,8 @@ struct CutPCfg {
   static constexpr int OFF_JAB = OFF_UB + 2 * 7 * N3P;
   static constexpr int OFF_RING = OFF_JAB + ((6 * 2 * NN + 1) & ~1);
   static constexpr int RSLOT = 2 + 256;
-  static constexpr int WSLOT = OFF_RING + NB * RSLOT;
+  static constexpr int OFF_WS = OFF_RING + NB * RSLOT;  // w of the structured faces (n^3)
+  static constexpr int WSLOT = OFF_WS + ((N3 + 1) & ~1);
   static constexpr int SMEM = WARPS * WSLOT * 8;
 };
 
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restric
                                               const CDesc2 *__restrict__ desc, const CChunk *__restrict__ chunks,
                                               const double *__restrict__ vol_pts, const double *__restrict__ srf_pts,
                                               const double *__restrict__ fac_pts, const int *__restrict__ wstart,
-                                              const int *__restrict__ kstart, KParams kp) {
+                                              const int *__restrict__ kstart, KParams kp, TileTab<N> tt) {
   static_assert(2 * N * N <= 32, "k_cutp needs N <= 4");
   using C = CutPCfg<N>;
   using LN = BlkU<N>;
@@ -226,7 +228,8 @@ __global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restric
   const int k0w = kstart[gw], k1w = kstart[gw + 1];
   double *base = smem + warp * C::WSLOT;
   uint64_t *bar = reinterpret_cast<uint64_t *>(base);  // 0,1: block sets; 2..2+NB: chunk ring
-  double *UB = base + C::OFF_UB, *JAB = base + C::OFF_JAB, *RING = base + C::OFF_RING;
+  double *UB = base + C::OFF_UB, *JAB = base + C::OFF_JAB, *RING = base + C::OFF_RING, *WS = base + C::OFF_WS;
+  const bool gp_on = (kp.mask & TERM_GP) != 0;
   const bool cell_on = (kp.mask & TERM_CELL) != 0, nit_on = (kp.mask & TERM_NITSCHE) != 0,
              sipg_on = (kp.mask & TERM_SIPG) != 0;
   auto counts = [&](const CDesc2 &d, int &nv, int &ns, int &nf) {
@@ -235,10 +238,12 @@ __global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restric
     nf = sipg_on ? d.nf : 0;
   };
   auto fmask_of = [&](const CDesc2 &d) { return sipg_on ? d.fmask : 0u; };
+  auto gmask_of = [&](const CDesc2 &d) { return gp_on ? (d.smask & 0x3fu) : 0u; };
+  auto smask_of = [&](const CDesc2 &d) { return sipg_on ? ((d.smask >> 8) & 0x3fu) : 0u; };
   // blocks of a cell (own + cut-face neighbours) into set s
   auto issue_blocks = [&](const CDesc2 &d, int s) {
     double *U = UB + s * 7 * N3P;
-    const uint32_t fm = fmask_of(d);
+    const uint32_t fm = fmask_of(d) | gmask_of(d) | smask_of(d);  // neighbour blocks needed
     if constexpr (C::BULK) {
       if (lane == 0) {
         mbar_expect_tx(bar + s, (uint32_t)((1 + __popc(fm)) * N3 * 8));
@@ -326,6 +331,87 @@ __global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restric
         }
       });
       __syncwarp();
+    }
+    // ---- structured faces of the cut cell (ghost penalty, full-face SIPG) in w-space:
+    //      w += M^-1-premultiplied line operators along each face normal, then
+    //      w <- (M (x) M (x) M) w; added to the point sums at the end (lanes 0..15 = lines)
+    const uint32_t gm = gmask_of(cd), sm = smask_of(cd);
+    if (gm | sm) {
+      for (int l = lane; l < N3; l += 32) WS[l] = 0.0;
+      __syncwarp();
+      static_for<0, 6>([&](auto fc) {
+        constexpr int F = fc.value, D = F / 2, SS = F % 2;
+        constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
+        const bool g = (gm >> F) & 1u, sp = (sm >> F) & 1u;
+        if ((g || sp) && lane < NN) {
+          const double *NBf = U + (1 + F) * N3P;
+          const int t0 = lane % N, t1 = lane / N;
+          const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
+          double uo[N], un[N], out[N];
+#pragma unroll
+          for (int m = 0; m < N; ++m) {
+            uo[m] = U[b0 + m * str];
+            un[m] = NBf[b0 + m * str];
+            out[m] = 0.0;
+          }
+          if (g) {
+#pragma unroll
+            for (int m = 0; m < N; ++m) {
+              double x = 0.0;
+#pragma unroll
+              for (int a = 0; a < N; ++a) {
+                const int k = SS ? (N - 1 - m) * N + (N - 1 - a) : m * N + a;
+                x = fma(tt.Goo[k], uo[a], fma(tt.Gon[k], un[a], x));
+              }
+              out[m] = x;
+            }
+          }
+          if (sp) {
+            double A0 = 0.0, A1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < N; ++m) {
+              if (SS == 0) {
+                A0 = fma(tt.d0[m], uo[m], A0);
+                A1 = fma(-tt.d0[N - 1 - m], un[m], A1);
+              } else {
+                A0 = fma(-tt.d0[N - 1 - m], uo[m], A0);
+                A1 = fma(tt.d0[m], un[m], A1);
+              }
+            }
+            const double J = SS ? (uo[N - 1] - un[0]) : (uo[0] - un[N - 1]);
+            const double A = A0 + A1;
+#pragma unroll
+            for (int m = 0; m < N; ++m) {
+              if (SS == 0) out[m] = fma(tt.cJ[m], J, fma(tt.cA[m], A, out[m]));
+              else out[m] = fma(tt.cJ[N - 1 - m], J, fma(-tt.cA[N - 1 - m], A, out[m]));
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < N; ++m) WS[b0 + m * str] += out[m];
+        }
+        __syncwarp();
+      });
+      static_for<0, 3>([&](auto dc) {
+        constexpr int D = dc.value;
+        constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
+        if (lane < NN) {
+          const int t0 = lane % N, t1 = lane / N;
+          const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
+          double x[N], y[N];
+#pragma unroll
+          for (int m = 0; m < N; ++m) x[m] = WS[b0 + m * str];
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) sacc = fma(tt.M[csym<N>(i * N + j)], x[j], sacc);
+            y[i] = sacc;
+          }
+#pragma unroll
+          for (int m = 0; m < N; ++m) WS[b0 + m * str] = y[m];
+        }
+        __syncwarp();
+      });
     }
     // ---- next cell's blocks into the other set (its previous user, cell it-1, is done)
     if (has_next) issue_blocks(nd, set ^ 1);
@@ -419,11 +505,17 @@ __global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restric
     // ---- reduce over the warp and write the block (every cut cell block written once)
     butterfly<C::ACC>(acc, lane);
     double *vb = v + (size_t)cd.blk * N3;
+    const bool st_on = (gm | sm) != 0;
     if constexpr (C::ACC == 64) {
-      *reinterpret_cast<double2 *>(vb + 2 * lane) = make_double2(acc[0], acc[1]);
+      double2 r = make_double2(acc[0], acc[1]);
+      if (st_on) {
+        r.x += WS[2 * lane];
+        r.y += WS[2 * lane + 1];
+      }
+      *reinterpret_cast<double2 *>(vb + 2 * lane) = r;
     } else {
       const int l = BF<C::ACC>::idx(lane, 0);
-      if (BF<C::ACC>::writer(lane) && l < N3) vb[l] = acc[0];
+      if (BF<C::ACC>::writer(lane) && l < N3) vb[l] = acc[0] + (st_on ? WS[l] : 0.0);
     }
     if constexpr (!C::BULK) __syncwarp();
     if (has_next) cd = nd;
