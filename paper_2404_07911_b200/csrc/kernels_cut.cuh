@@ -339,76 +339,86 @@ __global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restric
     if (gm | sm) {
       for (int l = lane; l < N3; l += 32) WS[l] = 0.0;
       __syncwarp();
-      static_for<0, 6>([&](auto fc) {
-        constexpr int F = fc.value, D = F / 2, SS = F % 2;
+      // per axis: lanes 0..15 the lo face in the own frame, lanes 16..31 the hi face in
+      // the line-reversed frame (same lo-face coefficients: all operators are
+      // centro-symmetric); the hi half's rows are folded into the lo half by a shuffle
+      const int hs = lane >> 4, t = lane & 15;
+      static_for<0, 3>([&](auto dc) {
+        constexpr int D = dc.value;
         constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
-        const bool g = (gm >> F) & 1u, sp = (sm >> F) & 1u;
-        if ((g || sp) && lane < NN) {
-          const double *NBf = U + (1 + F) * N3P;
-          const int t0 = lane % N, t1 = lane / N;
-          const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
+        const int f = 2 * D + hs;
+        const bool g = ((gm >> f) & 1u) != 0, sp = ((sm >> f) & 1u) != 0;
+        const bool anyg = __any_sync(0xffffffffu, g), anys = __any_sync(0xffffffffu, sp);
+        if (anyg || anys) {
+          const double *NBf = U + (1 + (g || sp ? f : 2 * D)) * N3P;
+          const int tt0 = (t < NN ? t : 0) % N, tt1 = (t < NN ? t : 0) / N;
+          const int b0 = D == 0 ? N * tt0 + NN * tt1 : (D == 1 ? tt0 + NN * tt1 : tt0 + N * tt1);
           double uo[N], un[N], out[N];
 #pragma unroll
           for (int m = 0; m < N; ++m) {
-            uo[m] = U[b0 + m * str];
-            un[m] = NBf[b0 + m * str];
+            const int pm = hs ? N - 1 - m : m;
+            uo[m] = U[b0 + pm * str];
+            un[m] = (g || sp) ? NBf[b0 + pm * str] : 0.0;
             out[m] = 0.0;
           }
-          if (g) {
+          if (anyg) {
+            const double eg = g ? 1.0 : 0.0;
 #pragma unroll
             for (int m = 0; m < N; ++m) {
               double x = 0.0;
 #pragma unroll
-              for (int a = 0; a < N; ++a) {
-                const int k = SS ? (N - 1 - m) * N + (N - 1 - a) : m * N + a;
-                x = fma(tt.Goo[k], uo[a], fma(tt.Gon[k], un[a], x));
-              }
-              out[m] = x;
+              for (int a2 = 0; a2 < N; ++a2) x = fma(tt.Goo[m * N + a2], uo[a2], fma(tt.Gon[m * N + a2], un[a2], x));
+              out[m] = eg * x;
             }
           }
-          if (sp) {
+          if (anys) {
             double A0 = 0.0, A1 = 0.0;
 #pragma unroll
             for (int m = 0; m < N; ++m) {
-              if (SS == 0) {
-                A0 = fma(tt.d0[m], uo[m], A0);
-                A1 = fma(-tt.d0[N - 1 - m], un[m], A1);
-              } else {
-                A0 = fma(-tt.d0[N - 1 - m], uo[m], A0);
-                A1 = fma(tt.d0[m], un[m], A1);
-              }
+              A0 = fma(tt.d0[m], uo[m], A0);
+              A1 = fma(-tt.d0[N - 1 - m], un[m], A1);
             }
-            const double J = SS ? (uo[N - 1] - un[0]) : (uo[0] - un[N - 1]);
-            const double A = A0 + A1;
+            const double es = sp ? 1.0 : 0.0;
+            const double J = es * (uo[0] - un[N - 1]);
+            const double A = es * (A0 + A1);
 #pragma unroll
-            for (int m = 0; m < N; ++m) {
-              if (SS == 0) out[m] = fma(tt.cJ[m], J, fma(tt.cA[m], A, out[m]));
-              else out[m] = fma(tt.cJ[N - 1 - m], J, fma(-tt.cA[N - 1 - m], A, out[m]));
-            }
+            for (int m = 0; m < N; ++m) out[m] = fma(tt.cJ[m], J, fma(tt.cA[m], A, out[m]));
           }
+          double o2[N];
 #pragma unroll
-          for (int m = 0; m < N; ++m) WS[b0 + m * str] += out[m];
+          for (int m = 0; m < N; ++m) o2[m] = __shfl_xor_sync(0xffffffffu, out[m], 16);
+          if (hs == 0 && t < NN) {
+#pragma unroll
+            for (int m = 0; m < N; ++m) WS[b0 + m * str] += out[m] + o2[N - 1 - m];
+          }
         }
         __syncwarp();
       });
+      // w <- (M (x) M (x) M) w: line t, rows split between the halves (the hi half in the
+      // reversed frame computes rows n-1, n-2, ... with the same coefficients)
       static_for<0, 3>([&](auto dc) {
         constexpr int D = dc.value;
         constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
-        if (lane < NN) {
-          const int t0 = lane % N, t1 = lane / N;
-          const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
-          double x[N], y[N];
+        constexpr int R = (N % 2 == 0) ? N / 2 : N;  // rows per half (odd n: the lo half does all)
+        const bool act = t < NN && ((N % 2 == 0) || hs == 0);
+        double x[N], y[R];
+        const int tt0 = (t < NN ? t : 0) % N, tt1 = (t < NN ? t : 0) / N;
+        const int b0 = D == 0 ? N * tt0 + NN * tt1 : (D == 1 ? tt0 + NN * tt1 : tt0 + N * tt1);
+        if (act) {
 #pragma unroll
-          for (int m = 0; m < N; ++m) x[m] = WS[b0 + m * str];
+          for (int m = 0; m < N; ++m) x[m] = WS[b0 + (hs ? N - 1 - m : m) * str];
 #pragma unroll
-          for (int i = 0; i < N; ++i) {
+          for (int i = 0; i < R; ++i) {
             double sacc = 0.0;
 #pragma unroll
             for (int j = 0; j < N; ++j) sacc = fma(tt.M[csym<N>(i * N + j)], x[j], sacc);
             y[i] = sacc;
           }
+        }
+        __syncwarp();
+        if (act) {
 #pragma unroll
-          for (int m = 0; m < N; ++m) WS[b0 + m * str] = y[m];
+          for (int i = 0; i < R; ++i) WS[b0 + (hs ? N - 1 - i : i) * str] = y[i];
         }
         __syncwarp();
       });
