@@ -464,6 +464,13 @@ struct CutCfg {
   static constexpr int CHUNK = N <= 4 ? 128 : (N <= 6 ? 64 : 32);
   static constexpr int FROW = 2 * N + 3;  // cut-face point row: l(s), l(t), c1, c2 (+pad)
   static constexpr int KPT = (N3 + THREADS - 1) / THREADS;
+  // integration phase: each thread owns RPT x-rows (b, c) of the block (sharing the
+  // x-basis loads), TG threads cover the N^2 rows, G groups split the chunk's points
+  // (N >= 7; below, one thread per DoF looping over the points is faster)
+  static constexpr bool ROWINT = N >= 7;
+  static constexpr int RPT = ROWINT ? 4 : 1;
+  static constexpr int TG = ROWINT ? (NN + RPT - 1) / RPT : THREADS;
+  static constexpr int G = ROWINT ? THREADS / TG : 1;
   // U, NB, T, R (padded blocks) + JA, JB, FC1, FC2 (NN each) + point rows
   static constexpr int SMEM_D = 4 * Blk<N>::SZ + 4 * NN + CHUNK * ROW;
   static constexpr int SMEM = SMEM_D * 8;
@@ -534,11 +541,12 @@ __device__ __forceinline__ void eval_point_l(const double *U, const double (&vx)
 
 template <int N, bool SURF>
 __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int64_t pb, int64_t pe,
-                                             const double *U, double *PS, double (&acc)[CutCfg<N>::KPT],
+                                             const double *U, double *PS, double (&acc)[CutCfg<N>::RPT][N],
                                              const KParams &kp, const RefTab &R) {
   using C = CutCfg<N>;
-  constexpr int NN = C::NN, N3 = C::N3, ROW = C::ROW;
+  constexpr int NN = C::NN, ROW = C::ROW, RPT = C::RPT, TG = C::TG, G = C::G;
   const int tid = threadIdx.x;
+  const int grp = tid / TG, rl = tid % TG;
   const double h = kp.h, ih = 1.0 / h, ih2 = ih * ih;
   for (int64_t c0 = pb; c0 < pe; c0 += C::CHUNK) {
     if (tid < C::CHUNK) {
@@ -580,12 +588,12 @@ __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int
         c3 = g * nz;
       } else {
         c0v = 0.0;
-        const double s = W * ih2;
-        c1 = s * ux;
-        c2 = s * uy;
-        c3 = s * uz;
+        const double sw = W * ih2;
+        c1 = sw * ux;
+        c2 = sw * uy;
+        c3 = sw * uz;
       }
-      // I (z and y stages per point); the x stage is the reduction below
+      // I (z and y stages per point); the x stage is the row integration below
       double T0[N], T1[N], T2[N];
 #pragma unroll
       for (int c = 0; c < N; ++c) {
@@ -609,18 +617,41 @@ __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int
     }
     __syncthreads();
     const int cnt = (int)((pe - c0) < C::CHUNK ? (pe - c0) : C::CHUNK);
+    if constexpr (!C::ROWINT) {
+      // one thread per DoF (a, bc): acc[k][0] over all the chunk's points
 #pragma unroll
-    for (int k = 0; k < C::KPT; ++k) {
-      const int l = tid + k * C::THREADS;
-      if (l < N3) {
-        const int a = l % N, bc = l / N;
-        double s = acc[k];
-        for (int qq = 0; qq < cnt; ++qq) {
-          const double *row = PS + qq * ROW;
-          s = fma(row[2 * NN + a], row[bc], s);
-          s = fma(row[2 * NN + N + a], row[NN + bc], s);
+      for (int k = 0; k < C::KPT; ++k) {
+        const int l = tid + k * C::THREADS;
+        if (l < N * NN) {
+          const int a = l % N, bc = l / N;
+          double sacc = acc[0][k];
+          for (int qq = 0; qq < cnt; ++qq) {
+            const double *row = PS + qq * ROW;
+            sacc = fma(row[2 * NN + a], row[bc], sacc);
+            sacc = fma(row[2 * NN + N + a], row[NN + bc], sacc);
+          }
+          acc[0][k] = sacc;
         }
-        acc[k] = s;
+      }
+    } else if (grp < G) {
+      // x stage: acc[r][a] += vx[a] S0[bc_r] + dvx[a] S1[bc_r] over this group's points
+      for (int qq = grp; qq < cnt; qq += G) {
+        const double *row = PS + qq * ROW;
+        double xv[N], xd[N];
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          xv[a] = row[2 * NN + a];
+          xd[a] = row[2 * NN + N + a];
+        }
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          const int bc = rl * RPT + r;
+          if (bc < NN) {
+            const double s0 = row[bc], s1 = row[NN + bc];
+#pragma unroll
+            for (int a = 0; a < N; ++a) acc[r][a] = fma(xv[a], s0, fma(xd[a], s1, acc[r][a]));
+          }
+        }
       }
     }
     __syncthreads();
@@ -651,17 +682,41 @@ __global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, doubl
     for (int l = tid; l < N3; l += TH) U[B::pad(l)] = __ldg(ub + l);
   }
   __syncthreads();
-  double acc[C::KPT];
+  double acc[C::RPT][N];
 #pragma unroll
-  for (int k = 0; k < C::KPT; ++k) acc[k] = 0.0;
+  for (int r = 0; r < C::RPT; ++r)
+#pragma unroll
+    for (int a = 0; a < N; ++a) acc[r][a] = 0.0;
   if (kp.mask & TERM_CELL)
     point_chunks<N, false>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], U, PS, acc, kp, R);
   if (kp.mask & TERM_NITSCHE)
     point_chunks<N, true>(srf_pts, srf_ptr[dsc.cut], srf_ptr[dsc.cut + 1], U, PS, acc, kp, R);
+  if constexpr (!C::ROWINT) {
+    static_assert(C::KPT <= N, "acc[0] holds the thread's DoFs");
 #pragma unroll
-  for (int k = 0; k < C::KPT; ++k) {
-    const int l = tid + k * TH;
-    if (l < N3) Rb[B::pad(l)] = acc[k];
+    for (int k = 0; k < C::KPT; ++k) {
+      const int l = tid + k * TH;
+      if (l < N3) Rb[B::pad(l)] = acc[0][k];
+    }
+  } else {
+    // sum the groups' partial rows (the chunk buffer is free now) into Rb
+    static_assert(C::G * N3 <= C::CHUNK * C::ROW, "reduction buffer");
+    const int grp = tid / C::TG, rl = tid % C::TG;
+    if (grp < C::G) {
+#pragma unroll
+      for (int r = 0; r < C::RPT; ++r) {
+        const int bc = rl * C::RPT + r;
+        if (bc < NN)
+#pragma unroll
+          for (int a = 0; a < N; ++a) PS[grp * N3 + a + N * bc] = acc[r][a];
+      }
+    }
+    __syncthreads();
+    for (int l = tid; l < N3; l += TH) {
+      double s = 0.0;
+      for (int g = 0; g < C::G; ++g) s += PS[g * N3 + l];
+      Rb[B::pad(l)] = s;
+    }
   }
   __syncthreads();
 
