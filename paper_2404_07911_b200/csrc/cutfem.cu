@@ -77,6 +77,7 @@ struct cutfem_handle {
   void *d_tiles = nullptr;
   int64_t t_off[3][3] = {{0}}, t_cnt[3][3] = {{0}};
   int occ_tile[3] = {1, 1, 1};
+  bool cut_last = false;  // launch k_cutp after the uncut-cell kernels (env CUTFEM_CUT_LAST)
   int persist = 1;  // tile kernels: persistent grid (1) or one tile per CTA (0); env CUTFEM_TILE_PERSIST
   std::vector<char> ttab;  // TileTab<N> bytes
   CDesc2 *d_cdesc2 = nullptr;  // k_cutp: cut cells grouped per warp (LPT), their cut-face points
@@ -574,11 +575,13 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
   const int64_t n0 = (which & 1) ? hd->t_cnt[0][part] : 0;
   const int64_t n1 = ((which & 1) && (hd->kp.mask & (TERM_GP | TERM_SIPG))) ? hd->t_cnt[1][part] : 0;
   const bool fork = nc > 0 && n0 > 0;
+  const bool cut_last = hd->cut_last;
   if (fork) {
     CU(cudaEventRecord(hd->ev_fork, st));
     CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
   }
-  if (nc > 0) {
+  auto launch_cut = [&]() -> int {
+    if (nc <= 0) return 0;
     using CP = CutPCfg<NT>;
     // part 0 = the interior list then the slab-boundary list (each with its own warp schedule)
     for (int pt = 1; pt <= 2; ++pt) {
@@ -590,7 +593,10 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
           *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data()));
     }
     CU(cudaGetLastError());
-  }
+    return 0;
+  };
+  int rc;
+  if (!cut_last && (rc = launch_cut())) return rc;
   const TileTab<NT> &tt = *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data());
   const auto *tl = reinterpret_cast<const TileRec<C::SMAX> *>(hd->d_tiles);
   if (n0 > 0) {
@@ -608,6 +614,7 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
                                                                   hd->kp.mask);
     CU(cudaGetLastError());
   }
+  if (cut_last && (rc = launch_cut())) return rc;
   if (fork) {
     CU(cudaEventRecord(hd->ev_join, hd->side));
     CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
@@ -1035,6 +1042,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   if ((rc = upload(hd, &hd->d_volptr, pb->vol_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_srfptr, pb->srf_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_sfptr, pb->sf_ptr, (size_t)(nsf ? nsf + 1 : 0)))) return rc;
+  hd->cut_last = std::getenv("CUTFEM_CUT_LAST") != nullptr;
   if (const char *e = std::getenv("CUTFEM_TILE_PERSIST")) hd->persist = std::atoi(e);
   else hd->persist = 3;
   if (!std::getenv("CUTFEM_NO_TILE") && (rc = dispatch_tiles(hd, pb, ud, cd))) return rc;

@@ -27,6 +27,9 @@
 #ifndef CUTP_MINB
 #define CUTP_MINB 1
 #endif
+#ifndef CUTP_WARPS
+#define CUTP_WARPS 1  // warps (cut cells in flight) per CTA: 1 lets other kernels share SMs
+#endif
 
 struct __align__(16) CDesc2 {
   int32_t blk;
@@ -193,7 +196,7 @@ __device__ __forceinline__ void face_point(double (&acc)[ACC], const RefTab &R, 
 template <int N>
 struct CutPCfg {
   static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
-  static constexpr int WARPS = 4;
+  static constexpr int WARPS = CUTP_WARPS;
   static constexpr int NB = 4;  // point-chunk ring depth (3 chunks in flight while one is computed)
   static constexpr int NN = N * N, N3 = N * N * N, N3P = (N3 + 1) & ~1;
   static constexpr int ACC = N == 4 ? 64 : (N == 3 ? 32 : 8);  // padded n^3 (power of two)
@@ -208,7 +211,7 @@ struct CutPCfg {
 };
 
 template <int N>
-__global__ void __launch_bounds__(128, CUTP_MINB) k_cutp(const double *__restrict__ u, double *__restrict__ v,
+__global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const double *__restrict__ u, double *__restrict__ v,
                                               const CDesc2 *__restrict__ desc, const CChunk *__restrict__ chunks,
                                               const double *__restrict__ vol_pts, const double *__restrict__ srf_pts,
                                               const double *__restrict__ fac_pts, const int *__restrict__ wstart,
