@@ -357,7 +357,7 @@ void build_tiles(const std::vector<TCell> &cells, const cutfem_problem *pb, std:
     std::vector<size_t> g(ord.begin() + i, ord.begin() + j);
     std::unordered_map<int32_t, int> trial = set;
     blocks_of(g, trial);
-    if (cur.size() + g.size() > 32 || (int)trial.size() > C::SMAX) {
+    if ((int)(cur.size() + g.size()) > C::TC || (int)trial.size() > C::SMAX) {
       flush();
       trial.clear();
       blocks_of(g, trial);
@@ -554,12 +554,57 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
   return 0;
 }
 
+// N = 5, 6: uncut cells through k_uncw (every structured term, GP included); cut
+// cells stay on k_cut.  (N = 7: one 121 KB tile per SM is slower than k_uncut.)
+template <int N>
+int setup_uncw(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<UDesc> &ud) {
+  using C = TileCfg<N>;
+  std::vector<TCell> part[2];
+  for (int pt = 1; pt <= 2; ++pt)
+    for (int k = 0; k < 2; ++k)
+      for (int64_t i = hd->r_off[pt][k]; i < hd->r_off[pt][k] + hd->r_cnt[pt][k]; ++i) {
+        const UDesc &d = ud[i];
+        TCell c;
+        c.blk = d.blk;
+        uint32_t nbm = 0;
+        for (int f = 0; f < 6; ++f) {
+          c.nb[f] = d.nb[f];
+          if (d.nb[f] >= 0) nbm |= 1u << f;
+        }
+        c.gp = d.flags & nbm & 0x3fu;
+        c.sipg = nbm;
+        c.vol = true;
+        part[pt - 1].push_back(c);
+      }
+  const int64_t rs = (int64_t)sizeof(TileRec<C::SMAX>);
+  std::vector<char> b0, b1;
+  build_tiles<N>(part[0], pb, b0);
+  build_tiles<N>(part[1], pb, b1);
+  hd->t_off[0][0] = hd->t_off[0][1] = 0;
+  hd->t_cnt[0][1] = (int64_t)b0.size() / rs;
+  hd->t_off[0][2] = hd->t_cnt[0][1];
+  hd->t_cnt[0][2] = (int64_t)b1.size() / rs;
+  hd->t_cnt[0][0] = hd->t_cnt[0][1] + hd->t_cnt[0][2];
+  b0.insert(b0.end(), b1.begin(), b1.end());
+  int rc = upload(hd, reinterpret_cast<char **>(&hd->d_tiles), b0.data(), b0.size());
+  if (rc) return rc;
+  hd->ttab.resize(sizeof(TileTab<N>));
+  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
+  CU(cudaFuncSetAttribute(k_uncw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncwCfg<N>::SMEM));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_uncw<N>, UncwCfg<N>::THREADS,
+                                                   UncwCfg<N>::SMEM));
+  hd->occ_tile[0] = std::max(1, hd->occ_tile[0]);
+  return 0;
+}
+
 int dispatch_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<UDesc> &ud,
                    const std::vector<CDesc> &cd) {
   switch (hd->n) {
     case 2: return setup_tiles<2>(hd, pb, ud, cd);
     case 3: return setup_tiles<3>(hd, pb, ud, cd);
     case 4: return setup_tiles<4>(hd, pb, ud, cd);
+    case 5: return setup_uncw<5>(hd, pb, ud);
+    case 6: return setup_uncw<6>(hd, pb, ud);
   }
   return 0;
 }
@@ -653,7 +698,17 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
     }
     CU(cudaGetLastError());
   }
-  if (nu > 0) {
+  if (nu > 0 && (N == 5 || N == 6) && hd->d_tiles) {
+    constexpr int NU = (N == 5 || N == 6) ? N : 5;
+    const int64_t nt = hd->t_cnt[0][part];
+    if (nt > 0) {
+      const unsigned grid = (unsigned)std::min<int64_t>(nt, (int64_t)hd->occ_tile[0] * hd->sm_count);
+      k_uncw<NU><<<grid, UncwCfg<NU>::THREADS, UncwCfg<NU>::SMEM, st>>>(
+          u, v, reinterpret_cast<const TileRec<TileCfg<NU>::SMAX> *>(hd->d_tiles) + hd->t_off[0][part], (int)nt,
+          *reinterpret_cast<const TileTab<NU> *>(hd->ttab.data()), hd->kp.mask);
+      CU(cudaGetLastError());
+    }
+  } else if (nu > 0) {
     if (N <= 5) {
       constexpr int NC = (N <= 5 ? N : 5);
       using C = Uncut3Cfg<NC>;

@@ -40,12 +40,15 @@
 
 template <int N>
 struct TileCfg {
-  static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
   static constexpr int N3 = N * N * N;
-  static constexpr int ST = N == 2 ? 10 : (N == 3 ? 27 : 66);  // slot stride (doubles)
-  static constexpr int SMAX = N == 4 ? 100 : 128;             // slots per tile
+  static constexpr bool BULK = CUTFEM_USE_BULK && (N3 * 8) % 16 == 0;  // 16-byte multiple blocks
+  // slot stride (doubles): consecutive slots on different banks for 8- / 16-byte reads
+  static constexpr int ST = N == 2 ? 10 : (N == 3 ? 27 : (N == 4 ? 66 : (BULK ? N3 + 2 : N3)));
+  static constexpr int TC = N <= 4 ? 32 : (N == 5 ? 16 : 8);   // cells per tile
+  static constexpr int SMAX = N <= 3 ? 128 : (N == 4 ? 100 : (N == 5 ? 60 : 36));  // slots per tile
   static constexpr int SMEM = 16 + SMAX * ST * 8;
-  static constexpr int BX = 2, BY = 4, BZ = 4;  // brick of the background grid
+  // brick of the background grid
+  static constexpr int BX = 2, BY = N <= 4 ? 4 : 2, BZ = N <= 5 ? 4 : 2;
 };
 
 // One warp-tile.  lane_nb[l] = {slot of faces 0..3 (bytes), slot of faces 4,5
@@ -867,6 +870,180 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
         const int l = ln32 + 32 * k;
         if (cv && l < N3) v[o[c] + l] = xv[c][k] + Wb[(8 * wrp + c) * WST + l];
       }
+    }
+  }
+}
+
+
+// ===================================================================== k_uncw
+// k_uncw<N> (N = 5, 6): uncut cells at high degree, every structured term (volume,
+// SIPG on all faces, ghost penalty on faces to cut cells), v = result.  The same
+// w-space arithmetic as k_tile2, organised like k_gpw (runtime line loops, w in
+// shared memory, small code): TPC threads per cell take every TPC-th line; the
+// volume line operator and both faces of an axis touch the same lines, so only a
+// __syncwarp separates the axes.
+template <int N>
+struct UncwCfg {
+  static constexpr int N3 = N * N * N, NN = N * N;
+  static constexpr int TC = TileCfg<N>::TC, TPC = 128 / TC;
+  static constexpr int WST = N3 + ((N3 & 1) ? 0 : 1);  // odd: consecutive cells on different banks
+  static constexpr int THREADS = 128;
+  static constexpr int SMEM = TileCfg<N>::SMEM + TC * WST * 8;
+};
+
+template <int N>
+__global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, double *__restrict__ v,
+                                              const TileRec<TileCfg<N>::SMAX> *__restrict__ tiles, int ntiles,
+                                              TileTab<N> tt, uint32_t mask) {
+  using TC_ = TileCfg<N>;
+  using C = UncwCfg<N>;
+  constexpr int NN = C::NN, N3 = C::N3, ST = TC_::ST, WST = C::WST, TPC = C::TPC;
+  static_assert(32 % TPC == 0, "a cell's threads in one warp");
+  extern __shared__ __align__(16) double smem[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  double *S = smem + 2;
+  double *Wb = S + TC_::SMAX * ST;
+  const int tid = threadIdx.x, cell = tid / TPC, r = tid % TPC;
+  const bool cell_on = (mask & TERM_CELL) != 0, sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
+  if (TC_::BULK && tid == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const TileRec<TC_::SMAX> *T = tiles + tile;
+    const int nslot = T->nslot, ncell = T->ncell;
+    const bool on = cell < ncell;
+    const uint2 ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[on ? cell : 0][0]);
+    // ---- stage the tile's blocks
+    if constexpr (TC_::BULK) {
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) mbar_expect_tx(bar, (uint32_t)(nslot * N3 * 8));
+      __syncthreads();
+      for (int sl = tid; sl < nslot; sl += C::THREADS) bulk_g2s(S + sl * ST, u + (size_t)T->blk[sl] * N3, N3 * 8, bar);
+    } else {
+      __syncthreads();
+      for (int sl = 0; sl < nslot; ++sl) {
+        const double *src = u + (size_t)T->blk[sl] * N3;
+        for (int l = tid; l < N3; l += C::THREADS) S[sl * ST + l] = __ldg(src + l);
+      }
+    }
+    double *W = Wb + (on ? cell : 0) * WST;
+    if (on)
+      for (int l = r; l < N3; l += TPC) W[l] = 0.0;
+    if constexpr (TC_::BULK) mbar_wait(bar, it & 1);
+    __syncthreads();
+    int nbs[6];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) nbs[f] = (ln.x >> (8 * f)) & 0xff;
+    nbs[4] = ln.y & 0xff;
+    nbs[5] = (ln.y >> 8) & 0xff;
+    const uint32_t gpb = (on && gp_on) ? (ln.y >> 16) & 0x3fu : 0u;
+    const uint32_t spb = (on && sipg_on) ? (ln.y >> 24) & 0x3fu : 0u;
+    const bool vol = on && cell_on && ((ln.y >> 30) & 1u);
+    const double *Us = S + (on ? cell : 0) * ST;
+    static_for<0, 3>([&](auto dc) {
+      constexpr int D = decltype(dc)::value;
+      constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
+      const bool gl = (gpb >> (2 * D)) & 1u, gh = (gpb >> (2 * D + 1)) & 1u;
+      const bool sl = (spb >> (2 * D)) & 1u, sh = (spb >> (2 * D + 1)) & 1u;
+      const double *Nl = (gl || sl) ? S + nbs[2 * D] * ST : Us;
+      const double *Nh = (gh || sh) ? S + nbs[2 * D + 1] * ST : Us;
+      if (on) {
+#pragma unroll 1
+        for (int t = r; t < NN; t += TPC) {
+          const int t0 = t % N, t1 = t / N;
+          const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
+          double uo[N], out[N];
+#pragma unroll
+          for (int m = 0; m < N; ++m) uo[m] = Us[b0 + m * str];
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            double x = 0.0;
+            if (vol) {
+#pragma unroll
+              for (int j = 0; j < N; ++j) x = fma(tt.L[csym<N>(i * N + j)], uo[j], x);
+            }
+            out[i] = x;
+          }
+          static_for<0, 2>([&](auto sc) {
+            constexpr int SS = decltype(sc)::value;
+            const bool g = SS ? gh : gl, sp = SS ? sh : sl;
+            if (!(g || sp)) return;
+            const double *Nf = SS ? Nh : Nl;
+            double un[N];
+#pragma unroll
+            for (int m = 0; m < N; ++m) un[m] = Nf[b0 + m * str];
+            if (g) {
+#pragma unroll
+              for (int m = 0; m < N; ++m) {
+                double x = out[m];
+#pragma unroll
+                for (int a = 0; a < N; ++a) {
+                  const int k = SS ? (N - 1 - m) * N + (N - 1 - a) : m * N + a;
+                  x = fma(tt.Goo[k], uo[a], fma(tt.Gon[k], un[a], x));
+                }
+                out[m] = x;
+              }
+            }
+            if (sp) {
+              double A0 = 0.0, A1 = 0.0;
+#pragma unroll
+              for (int m = 0; m < N; ++m) {
+                if (SS == 0) {
+                  A0 = fma(tt.d0[m], uo[m], A0);
+                  A1 = fma(-tt.d0[N - 1 - m], un[m], A1);
+                } else {
+                  A0 = fma(-tt.d0[N - 1 - m], uo[m], A0);
+                  A1 = fma(tt.d0[m], un[m], A1);
+                }
+              }
+              const double J = SS ? (uo[N - 1] - un[0]) : (uo[0] - un[N - 1]);
+              const double A = A0 + A1;
+#pragma unroll
+              for (int m = 0; m < N; ++m) {
+                if (SS == 0) out[m] = fma(tt.cJ[m], J, fma(tt.cA[m], A, out[m]));
+                else out[m] = fma(tt.cJ[N - 1 - m], J, fma(-tt.cA[N - 1 - m], A, out[m]));
+              }
+            }
+          });
+#pragma unroll
+          for (int m = 0; m < N; ++m) W[b0 + m * str] += out[m];
+        }
+      }
+      __syncwarp();  // the next axis updates other threads' positions
+    });
+    // ---- v = (M (x) M (x) M) w, sweeps in shared memory
+    static_for<0, 3>([&](auto dc) {
+      constexpr int D = decltype(dc)::value;
+      constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
+      if (on) {
+#pragma unroll 1
+        for (int t = r; t < NN; t += TPC) {
+          const int t0 = t % N, t1 = t / N;
+          const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
+          double x[N], y[N];
+#pragma unroll
+          for (int m = 0; m < N; ++m) x[m] = W[b0 + m * str];
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) sacc = fma(tt.M[csym<N>(i * N + j)], x[j], sacc);
+            y[i] = sacc;
+          }
+#pragma unroll
+          for (int m = 0; m < N; ++m) W[b0 + m * str] = y[m];
+        }
+      }
+      __syncwarp();
+    });
+    __syncthreads();  // all w final; all slot reads done (the next tile's copies may start)
+    for (int e = tid; e < ncell * N3; e += C::THREADS) {
+      const int c = e / N3, l = e - c * N3;
+      v[(size_t)T->blk[c] * N3 + l] = Wb[c * WST + l];
     }
   }
 }

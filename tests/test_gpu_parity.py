@@ -292,3 +292,16 @@ def test_cg_tolerance_stop(cf, cutgen_mod):
     x, hist = op.cg(b, iters=2000, tol=1e-9)
     assert hist[-1] <= 1e-9 * float(b.norm()) and len(hist) < 2001
     assert float((b - op.apply(x)).norm()) <= 1e-8 * float(b.norm())
+
+
+@pytest.mark.parametrize("p,N", [(4, 10), (5, 9), (6, 8)])
+def test_sphere_high_degree_tiles(cf, cutgen_mod, p, N):
+    """k_uncw (p = 4, 5) and k_uncut (p = 6): several tiles of uncut cells, plain and
+    next to cut cells."""
+    P = cutgen_mod.generate(cutgen_mod.SPHERE, N, -1.0, 1.0, p)
+    u = P.seeded_u(30 + p)
+    v, op = gpu_apply(cf, P, u)
+    assert op.stats()["n_uncut"] > 30
+    check(P, v, u)
+    v, _ = gpu_apply(cf, P, u, 8)
+    check(P, v, u, 8)
