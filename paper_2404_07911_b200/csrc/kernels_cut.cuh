@@ -206,7 +206,8 @@ struct CutPCfg {
   static constexpr int OFF_RING = OFF_JAB + ((6 * 2 * NN + 1) & ~1);
   static constexpr int RSLOT = 2 + 256;
   static constexpr int OFF_WS = OFF_RING + NB * RSLOT;  // w of the structured faces (n^3)
-  static constexpr int WSLOT = OFF_WS + ((N3 + 1) & ~1);
+  static constexpr int OFF_RED = OFF_WS + ((N3 + 1) & ~1);  // reduction transpose [32][33]
+  static constexpr int WSLOT = OFF_RED + 32 * 33;
   static constexpr int SMEM = WARPS * WSLOT * 8;
 };
 
@@ -516,19 +517,30 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
       if (lane == 0) fence_proxy_async();
     }
     // ---- reduce over the warp and write the block (every cut cell block written once)
-    butterfly<C::ACC>(acc, lane);
+    // padded shared-memory transpose, 32 entries per pass: lane l sums entry
+    // 32 pass + l over the 32 lanes (fixed order)
+    double *RED = base + C::OFF_RED;
     double *vb = v + (size_t)cd.blk * N3;
     const bool st_on = (gm | sm) != 0;
-    if constexpr (C::ACC == 64) {
-      double2 r = make_double2(acc[0], acc[1]);
-      if (st_on) {
-        r.x += WS[2 * lane];
-        r.y += WS[2 * lane + 1];
+#pragma unroll
+    for (int ps = 0; ps < (C::ACC + 31) / 32; ++ps) {
+      constexpr int RW = C::ACC < 32 ? C::ACC : 32;
+#pragma unroll
+      for (int i = 0; i < RW; ++i) RED[i * 33 + lane] = acc[ps * 32 + i];
+      __syncwarp();
+      const int l = ps * 32 + lane;
+      if (lane < RW && l < N3) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          s0 += RED[lane * 33 + k];
+          s1 += RED[lane * 33 + k + 1];
+          s2 += RED[lane * 33 + k + 2];
+          s3 += RED[lane * 33 + k + 3];
+        }
+        vb[l] = ((s0 + s1) + (s2 + s3)) + (st_on ? WS[l] : 0.0);
       }
-      *reinterpret_cast<double2 *>(vb + 2 * lane) = r;
-    } else {
-      const int l = BF<C::ACC>::idx(lane, 0);
-      if (BF<C::ACC>::writer(lane) && l < N3) vb[l] = acc[0] + (st_on ? WS[l] : 0.0);
+      __syncwarp();
     }
     if constexpr (!C::BULK) __syncwarp();
     if (has_next) cd = nd;
