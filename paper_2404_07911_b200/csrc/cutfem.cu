@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <queue>
 #include <cmath>
 #include <cstdio>
@@ -435,6 +436,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     // coordinates [xi, eta, zeta, W] (normal coordinate exactly 0 or 1)
     std::vector<CDesc2> c2(cd.size());
     std::vector<double> fac;
+    std::vector<std::array<int32_t, 3>> fax(cd.size(), std::array<int32_t, 3>{0, 0, 0});  // face points per axis
     for (size_t i = 0; i < cd.size(); ++i) {
       const CDesc &d = cd[i];
       CDesc2 &e = c2[i];
@@ -464,6 +466,8 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         }
       }
       e.nf = (int32_t)((int64_t)fac.size() / 4 - e.fb);
+      for (int f = 0; f < 6; ++f)
+        if ((e.fmask >> f) & 1u) fax[i][f >> 1] += (int32_t)(pb->sf_ptr[d.sf[f] + 1] - pb->sf_ptr[d.sf[f]]);
     }
     CU(cudaFuncSetAttribute(k_cutp<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutPCfg<N>::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_cutp, k_cutp<N>, 32 * CutPCfg<N>::WARPS,
@@ -505,20 +509,36 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         for (int64_t i : lists[w]) {
           const CDesc2 &e = c2[i];
           c2o[pos++] = e;
-          // the chunks of this cell: stream = [volume | interface | cut face] points
+          // the chunks of this cell: [volume | interface] points in chunks of 32, then the
+          // cut-face points axis by axis (a chunk never mixes a face point with another
+          // kind or another face axis: the warp then runs one code path per chunk)
           const int nv = (hd->mask & CUTFEM_TERM_CELL) ? e.nv : 0, ns = (hd->mask & CUTFEM_TERM_NITSCHE) ? e.ns : 0;
-          const int nf = (hd->mask & CUTFEM_TERM_SIPG) ? e.nf : 0;
-          for (int q0 = 0; q0 < nv + ns + nf; q0 += 32) {
+          const bool fon = (hd->mask & CUTFEM_TERM_SIPG) != 0;
+          const size_t k0 = chunk.size();
+          for (int q0 = 0; q0 < nv + ns; q0 += 32) {
             const int cv = std::max(0, std::min(32, nv - q0));
             const int qs = std::max(0, q0 - nv), cs = std::max(0, std::min(32 - cv, ns - qs));
-            const int qf = std::max(0, q0 - nv - ns), cf = std::max(0, std::min(32 - cv - cs, nf - qf));
             CChunk r;
             r.vo = (int32_t)(e.vb + q0);
             r.so = (int32_t)(e.sb + qs);
-            r.fo = (int32_t)(e.fb + qf);
-            r.cnt = cv | (cs << 8) | (cf << 16);
+            r.fo = (int32_t)e.fb;
+            r.cnt = cv | (cs << 8);
             chunk.push_back(r);
           }
+          int64_t fo = e.fb;
+          for (int ax = 0; ax < 3 && fon; ++ax) {
+            const int na = fax[i][ax];
+            for (int q0 = 0; q0 < na; q0 += 32) {
+              CChunk r;
+              r.vo = (int32_t)e.vb;
+              r.so = (int32_t)e.sb;
+              r.fo = (int32_t)(fo + q0);
+              r.cnt = std::min(32, na - q0) << 16;
+              chunk.push_back(r);
+            }
+            fo += na;
+          }
+          c2o[pos - 1].nchunk = (int32_t)(chunk.size() - k0);
         }
       }
       ws.push_back((int)(pos - o));

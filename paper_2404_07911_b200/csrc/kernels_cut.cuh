@@ -38,6 +38,8 @@ struct __align__(16) CDesc2 {
   int64_t vb, sb, fb;  // first volume / interface / cut-face point of the cell
   int32_t nv, ns, nf;
   uint32_t smask;    // bits 0-5: ghost-penalty faces, bits 8-13: full-face SIPG faces
+  int32_t nchunk;    // point chunks of the cell in the plan (a new chunk starts at the
+                     // volume/interface -> face boundary and at every face-axis boundary)
 };
 
 // value + reference gradient at a point from the unpadded block U (16-byte
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     if (has_next) nd = desc[c + 1];
     int nv, ns, nf;
     counts(cd, nv, ns, nf);
-    const int total = nv + ns + nf, K = (total + 31) / 32;
+    const int K = cd.nchunk;
     const uint32_t fm = fmask_of(cd);
     // ---- this cell's blocks
     if constexpr (C::BULK) {
