@@ -289,9 +289,8 @@ struct TCell {
 // partial bricks merged in brick order) and number the slots: own cells first
 // (slot = cell index), then the face-neighbour halo of the faces with work, face
 // by face (so that the lanes of one face read consecutive slots).
-template <int N>
+template <class C>
 void build_tiles(const std::vector<TCell> &cells, const cutfem_problem *pb, std::vector<char> &out) {
-  using C = TileCfg<N>;
   using R = TileRec<C::SMAX>;
   auto used = [&](const TCell &c, int f) { return c.nb[f] >= 0 && (((c.gp | c.sipg) >> f) & 1u); };
   std::vector<std::pair<int64_t, int64_t>> key(cells.size());
@@ -415,15 +414,23 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       (void)c;  // cut cells: their structured faces are done inside k_cutp
     }
   }
-  const int64_t rs = (int64_t)sizeof(TileRec<C::SMAX>);
+  // set 0: k_tile* tiles (TileCfg<N>); set 1: k_gpw tiles (smaller, GpwCfg<N>::T).
+  // Offsets are in BYTES (the record sizes differ).
+  using CG = typename GpwCfg<N>::T;
   std::vector<char> all;
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 2; ++k) {
+    const int64_t rs = k == 0 ? (int64_t)sizeof(TileRec<C::SMAX>) : (int64_t)sizeof(TileRec<CG::SMAX>);
     std::vector<char> b0, b1;
-    build_tiles<N>(set[k][0], pb, b0);
-    build_tiles<N>(set[k][1], pb, b1);
-    hd->t_off[k][0] = hd->t_off[k][1] = (int64_t)all.size() / rs;
+    if (k == 0) {
+      build_tiles<C>(set[k][0], pb, b0);
+      build_tiles<C>(set[k][1], pb, b1);
+    } else {
+      build_tiles<CG>(set[k][0], pb, b0);
+      build_tiles<CG>(set[k][1], pb, b1);
+    }
+    hd->t_off[k][0] = hd->t_off[k][1] = (int64_t)all.size();
     hd->t_cnt[k][1] = (int64_t)b0.size() / rs;
-    hd->t_off[k][2] = hd->t_off[k][1] + hd->t_cnt[k][1];
+    hd->t_off[k][2] = hd->t_off[k][1] + (int64_t)b0.size();
     hd->t_cnt[k][2] = (int64_t)b1.size() / rs;
     hd->t_cnt[k][0] = hd->t_cnt[k][1] + hd->t_cnt[k][2];
     all.insert(all.end(), b0.begin(), b0.end());
@@ -598,8 +605,8 @@ int setup_uncw(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<UD
       }
   const int64_t rs = (int64_t)sizeof(TileRec<C::SMAX>);
   std::vector<char> b0, b1;
-  build_tiles<N>(part[0], pb, b0);
-  build_tiles<N>(part[1], pb, b1);
+  build_tiles<TileCfg<N>>(part[0], pb, b0);
+  build_tiles<TileCfg<N>>(part[1], pb, b1);
   hd->t_off[0][0] = hd->t_off[0][1] = 0;
   hd->t_cnt[0][1] = (int64_t)b0.size() / rs;
   hd->t_off[0][2] = hd->t_cnt[0][1];
@@ -663,20 +670,20 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
   int rc;
   if (!cut_last && (rc = launch_cut())) return rc;
   const TileTab<NT> &tt = *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data());
-  const auto *tl = reinterpret_cast<const TileRec<C::SMAX> *>(hd->d_tiles);
+  const char *tb = reinterpret_cast<const char *>(hd->d_tiles);  // byte offsets per set
   if (n0 > 0) {
     const unsigned grid = (unsigned)(hd->persist & 1 ? std::min<int64_t>(n0, (int64_t)hd->occ_tile[0] * hd->sm_count) : n0);
+    const auto *t0 = reinterpret_cast<const TileRec<C::SMAX> *>(tb + hd->t_off[0][part]);
     if constexpr (NT == 4)
-      k_tile2<NT, 0><<<grid, Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, tl + hd->t_off[0][part], (int)n0,
-                                                                              tt, hd->kp.mask);
+      k_tile2<NT, 0><<<grid, Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, t0, (int)n0, tt, hd->kp.mask);
     else
-      k_tile<NT, 0><<<grid, 32, C::SMEM, st>>>(u, v, tl + hd->t_off[0][part], (int)n0, tt, hd->kp.mask);
+      k_tile<NT, 0><<<grid, 32, C::SMEM, st>>>(u, v, t0, (int)n0, tt, hd->kp.mask);
     CU(cudaGetLastError());
   }
   if (n1 > 0) {  // uncut cells next to cut cells: + ghost penalty (needs only k_tile*<0>)
     const unsigned grid = (unsigned)(hd->persist & 2 ? std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count) : n1);
-    k_gpw<NT><<<grid, GpwCfg<NT>::THREADS, GpwCfg<NT>::SMEM, st>>>(u, v, tl + hd->t_off[1][part], (int)n1, tt,
-                                                                  hd->kp.mask);
+    k_gpw<NT><<<grid, GpwCfg<NT>::THREADS, GpwCfg<NT>::SMEM, st>>>(
+        u, v, reinterpret_cast<const TileRec<GpwCfg<NT>::SMAX> *>(tb + hd->t_off[1][part]), (int)n1, tt, hd->kp.mask);
     CU(cudaGetLastError());
   }
   if (cut_last && (rc = launch_cut())) return rc;
@@ -1218,6 +1225,32 @@ int cutfem_apply_host(cutfem_handle *hd, const double *u_host, double *v_host, v
   CU(cudaMemcpyAsync(v_host, hd->d_v, bytes, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   return 0;
+}
+
+// debug: kernel timeline of the last applies (build with -DCUTFEM_TIMELINE; not in the
+// public header).  reset != 0 clears it; out[2k], out[2k+1] = first start / last end (ns)
+int cutfem_debug_timeline(int reset, unsigned long long *out) {
+#ifdef CUTFEM_TIMELINE
+  unsigned long long h[8][2];
+  if (reset) {
+    for (int k = 0; k < 8; ++k) {
+      h[k][0] = ~0ull;
+      h[k][1] = 0;
+    }
+    CU(cudaMemcpyToSymbol(g_tl, h, sizeof(h)));
+  } else {
+    CU(cudaMemcpyFromSymbol(h, g_tl, sizeof(h)));
+    for (int k = 0; k < 8; ++k) {
+      out[2 * k] = h[k][0];
+      out[2 * k + 1] = h[k][1];
+    }
+  }
+  return 0;
+#else
+  (void)reset;
+  (void)out;
+  return fail(CUTFEM_EUNSUPPORTED, "built without CUTFEM_TIMELINE");
+#endif
 }
 
 int cutfem_stats(const cutfem_handle *hd, cutfem_stats_t *out) {

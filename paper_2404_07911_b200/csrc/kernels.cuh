@@ -20,6 +20,25 @@
 #include <type_traits>
 
 #define CUTFEM_NMAX 9
+
+// Opt-in timeline probe (build with -DCUTFEM_TIMELINE; tools/timeline.py): first CTA
+// start and last CTA end of each kernel family, from %globaltimer (ns).  Not in the
+// default build (it uses atomics).
+#ifdef CUTFEM_TIMELINE
+__device__ unsigned long long g_tl[8][2];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_BEGIN(k) \
+  if (threadIdx.x == 0) atomicMin(&g_tl[k][0], gtimer());
+#define TL_END(k) \
+  if (threadIdx.x == 0) atomicMax(&g_tl[k][1], gtimer());
+#else
+#define TL_BEGIN(k)
+#define TL_END(k)
+#endif
 #ifndef CUTFEM_USE_BULK
 #define CUTFEM_USE_BULK 1
 #endif

@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
   const int gw = blockIdx.x * C::WARPS + warp;
   const int c0w = wstart[gw], c1w = wstart[gw + 1];
   if (c0w >= c1w) return;
+  TL_BEGIN(0);
   const int k0w = kstart[gw], k1w = kstart[gw + 1];
   double *base = smem + warp * C::WSLOT;
   uint64_t *bar = reinterpret_cast<uint64_t *>(base);  // 0,1: block sets; 2..2+NB: chunk ring
@@ -547,5 +548,6 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     if constexpr (!C::BULK) __syncwarp();
     if (has_next) cd = nd;
   }
+  TL_END(0);
 }
 

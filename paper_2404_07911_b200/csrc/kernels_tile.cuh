@@ -38,18 +38,21 @@
 #define T1MINB 1
 #endif
 
-template <int N>
-struct TileCfg {
+// Tiles of TCELLS cells (a brick of the background grid) + their face-neighbour halo.
+template <int N, int TCELLS>
+struct TileCfgX {
   static constexpr int N3 = N * N * N;
   static constexpr bool BULK = CUTFEM_USE_BULK && (N3 * 8) % 16 == 0;  // 16-byte multiple blocks
   // slot stride (doubles): consecutive slots on different banks for 8- / 16-byte reads
   static constexpr int ST = N == 2 ? 10 : (N == 3 ? 27 : (N == 4 ? 66 : (BULK ? N3 + 2 : N3)));
-  static constexpr int TC = N <= 4 ? 32 : (N == 5 ? 16 : 8);   // cells per tile
-  static constexpr int SMAX = N <= 3 ? 128 : (N == 4 ? 100 : (N == 5 ? 60 : 36));  // slots per tile
+  static constexpr int TC = TCELLS;  // cells per tile
+  // slots per tile: the brick + its face halo (2x4x4: 32 + 64, 2x2x4: 16 + 40, 2x2x2: 8 + 24)
+  static constexpr int SMAX = TC == 32 ? (N <= 3 ? 128 : 100) : (TC == 16 ? 60 : 36);
   static constexpr int SMEM = 16 + SMAX * ST * 8;
-  // brick of the background grid
-  static constexpr int BX = 2, BY = N <= 4 ? 4 : 2, BZ = N <= 5 ? 4 : 2;
+  static constexpr int BX = 2, BY = TC == 32 ? 4 : 2, BZ = TC == 8 ? 2 : 4;
 };
+template <int N>
+struct TileCfg : TileCfgX<N, (N <= 4 ? 32 : (N == 5 ? 16 : 8))> {};
 
 // One warp-tile.  lane_nb[l] = {slot of faces 0..3 (bytes), slot of faces 4,5
 // (bytes 0,1) | ghost-penalty face bits << 16}; slot 255 = no neighbour.  Lane l
@@ -500,6 +503,7 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
   const bool cell_on = (mask & TERM_CELL) != 0, sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
   // the thread's frame: plane cc of the half is physical plane zb + zs cc; z position m at zb + zs m
   const int zb = h ? NN * (N - 1) : 0, zs = h ? -NN : NN;
+  TL_BEGIN(1);
   if (tid == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
@@ -683,6 +687,7 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
     }
   }
 
+  TL_END(1);
 }
 
 // ===================================================================== k_gpw
@@ -697,11 +702,16 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
 // operators stay warp-uniform constant-bank operands.
 template <int N>
 struct GpwCfg {
-  static constexpr bool BULK = TileCfg<N>::BULK;
-  static constexpr int N3 = N * N * N, ST = TileCfg<N>::ST, SMAX = TileCfg<N>::SMAX;
+  // small tiles: ~one tile per CTA is in flight, so shorter tiles mean a shorter kernel
+  static constexpr int TC = N == 4 ? 8 : (N == 3 ? 16 : 32);
+  using T = TileCfgX<N, TC>;
+  static constexpr bool BULK = T::BULK;
+  static constexpr int N3 = N * N * N, ST = T::ST, SMAX = T::SMAX;
   static constexpr int WST = N3 + 2;  // w row stride (doubles): consecutive cells on different banks
   static constexpr int THREADS = 128;
-  static constexpr int SMEM = 16 + SMAX * ST * 8 + 32 * WST * 8;
+  static constexpr int TPC = THREADS / TC;  // threads per cell
+  static constexpr int CPW = TC / 4;        // cells per warp in the write-back
+  static constexpr int SMEM = 16 + SMAX * ST * 8 + TC * WST * 8;
 };
 
 template <int N>
@@ -714,12 +724,14 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
   double *S = smem + 2;
   double *Wb = S + C::SMAX * ST;
-  const int tid = threadIdx.x, cell = tid >> 2, r = tid & 3;
+  constexpr int TPC = C::TPC, CPW = C::CPW;
+  const int tid = threadIdx.x, cell = tid / TPC, r = tid % TPC;
   const bool sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
   if (C::BULK && tid == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
   }
+  TL_BEGIN(2);
   __syncthreads();
   uint32_t it = 0;
   const int wrp = tid >> 5, ln32 = tid & 31;
@@ -732,7 +744,7 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
     nx_nslot = T->nslot;
     nx_ncell = T->ncell;
     nx_ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[cell][0]);
-    nx_bl = (ln32 < 8 && 8 * wrp + ln32 < nx_ncell) ? T->blk[8 * wrp + ln32] : 0;
+    nx_bl = (ln32 < CPW && CPW * wrp + ln32 < nx_ncell) ? T->blk[CPW * wrp + ln32] : 0;
   };
   if ((int)blockIdx.x < ntiles) fetch(blockIdx.x);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -741,12 +753,12 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
     const bool on = cell < ncell;
     const uint2 ln = nx_ln;
     // the v rows this warp adds to, loaded now and consumed at the end of the tile
-    double xv[8][PER];
-    size_t o[8];
+    double xv[CPW][PER];
+    size_t o[CPW];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < CPW; ++c) {
       o[c] = (size_t)__shfl_sync(0xffffffffu, bl, c) * N3;
-      const bool cv = 8 * wrp + c < ncell;
+      const bool cv = CPW * wrp + c < ncell;
 #pragma unroll
       for (int k = 0; k < PER; ++k) {
         const int l = ln32 + 32 * k;
@@ -768,7 +780,7 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
       }
     }
     double *W = Wb + cell * WST;
-    for (int l = r; l < N3; l += 4) W[l] = 0.0;
+    for (int l = r; l < N3; l += TPC) W[l] = 0.0;
     if (tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
     if constexpr (C::BULK) mbar_wait(bar, it & 1);
     __syncthreads();
@@ -789,7 +801,7 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
         const double eg = g ? 1.0 : 0.0, es = sp ? 1.0 : 0.0;
         const double *Nf = (g || sp) ? S + nbs[F] * ST : Us;
 #pragma unroll 1
-        for (int t = r; t < NN; t += 4) {
+        for (int t = r; t < NN; t += TPC) {
           const int t0 = t % N, t1 = t / N;
           const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
           double uo[N], un[N], out[N];
@@ -842,7 +854,7 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
       constexpr int D = decltype(dc)::value;
       constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
 #pragma unroll 1
-      for (int t = r; t < NN; t += 4) {
+      for (int t = r; t < NN; t += TPC) {
         const int t0 = t % N, t1 = t / N;
         const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
         double x[N], y[N];
@@ -863,15 +875,16 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
     __syncthreads();  // all w final; all slot reads done (the next tile's copies may start)
     // ---- v += w (the warp's 8 cells; v rows were loaded at the start of the tile)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const bool cv = 8 * wrp + c < ncell;
+    for (int c = 0; c < CPW; ++c) {
+      const bool cv = CPW * wrp + c < ncell;
 #pragma unroll
       for (int k = 0; k < PER; ++k) {
         const int l = ln32 + 32 * k;
-        if (cv && l < N3) v[o[c] + l] = xv[c][k] + Wb[(8 * wrp + c) * WST + l];
+        if (cv && l < N3) v[o[c] + l] = xv[c][k] + Wb[(CPW * wrp + c) * WST + l];
       }
     }
   }
+  TL_END(2);
 }
 
 

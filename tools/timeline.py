@@ -1,0 +1,38 @@
+"""Kernel timeline of one apply (first CTA start / last CTA end per kernel family),
+with a library built with -DCUTFEM_TIMELINE:
+  python tools/build_variant.py tl -DCUTFEM_TIMELINE
+  CUTFEM_LIB=build/variants/libcutfem_tl.so python tools/timeline.py [CFG]"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import cutgen
+import paper_2404_07911_b200 as cf
+
+P = cutgen.config(sys.argv[1] if len(sys.argv) > 1 else "C2")
+op = cf.CutFEM(P)
+L = op._L
+L.cutfem_debug_timeline.argtypes = [ctypes.c_int, ctypes.c_void_p]
+u = torch.from_numpy(P.seeded_u(0)).cuda()
+v = torch.empty_like(u)
+flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+names = {0: "k_cutp", 1: "k_tile2", 2: "k_gpw"}
+for rep in range(4):
+    flush.zero_()
+    torch.cuda.synchronize()
+    assert L.cutfem_debug_timeline(1, None) == 0
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    op.apply(u, v)
+    b.record()
+    torch.cuda.synchronize()
+    out = (ctypes.c_ulonglong * 16)()
+    L.cutfem_debug_timeline(0, ctypes.addressof(out))
+    t0 = min(out[2 * k] for k in names if out[2 * k] != 2 ** 64 - 1)
+    row = {names[k]: (round((out[2 * k] - t0) / 1e3, 1), round((out[2 * k + 1] - t0) / 1e3, 1)) for k in names
+           if out[2 * k] != 2 ** 64 - 1}
+    print(f"apply {a.elapsed_time(b) * 1e3:.1f} us  (start, end) us: {row}")
