@@ -84,8 +84,9 @@ struct cutfem_handle {
   CDesc2 *d_cdesc2 = nullptr;  // k_cutp: cut cells grouped per warp (LPT), their cut-face points
   double *d_fac = nullptr;
   int *d_wstart = nullptr;      // per part: warp -> first cell (grid_cutp[part] * WARPS + 1 entries)
-  int *d_kstart = nullptr;      // per part: warp -> first point chunk
-  CChunk *d_chunks = nullptr;   // point-chunk plan, per warp in consumption order
+  int *d_kstart = nullptr;      // per part: warp -> first packet
+  CPacket *d_chunks = nullptr;  // packets of the point-chunk stream, per warp in consumption order
+  char *d_stream = nullptr;     // the packed stream (chunk headers + point rows)
   int64_t w_off[3] = {0};
   int grid_cutp[3] = {0};
   int occ_cutp = 1;
@@ -551,13 +552,50 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       ws.push_back((int)(pos - o));
       ks.push_back((int)chunk.size());
     }
+    // pack every warp's chunks, in consumption order, into a contiguous stream
+    // (16-byte chunk header {cnt} + volume rows [xi,eta,zeta,W] + interface rows
+    // [xi,eta,zeta,nx,ny,nz,W,0] + cut-face rows [xi,eta,zeta,W]) and cut it into
+    // packets of <= CUTP_PK bytes, one bulk copy each
+    std::vector<double> strm;
+    std::vector<CPacket> pk;
+    std::vector<int> ps;
+    ps.reserve(ks.size());
+    for (size_t w = 0; w + 1 < ks.size(); ++w) {
+      ps.push_back((int)pk.size());
+      if (ks[w + 1] < ks[w]) continue;  // part boundary entry (no chunks)
+      CPacket cur = {(int64_t)strm.size() * 8, 0, 0};
+      for (int k = ks[w]; k < ks[w + 1]; ++k) {
+        const CChunk &r = chunk[k];
+        const int cv = r.cnt & 0xff, cs = (r.cnt >> 8) & 0xff, cf = (r.cnt >> 16) & 0xff;
+        const int bytes = 16 + 32 * cv + 64 * cs + 32 * cf;
+        if (cur.nch > 0 && cur.bytes + bytes > CutPCfg<N>::PK) {
+          pk.push_back(cur);
+          cur = {(int64_t)strm.size() * 8, 0, 0};
+        }
+        double hdr[2] = {0.0, 0.0};
+        std::memcpy(hdr, &r.cnt, sizeof(int32_t));
+        strm.insert(strm.end(), hdr, hdr + 2);
+        strm.insert(strm.end(), pb->vol_pts + 4 * (size_t)r.vo, pb->vol_pts + 4 * ((size_t)r.vo + cv));
+        for (int q = 0; q < cs; ++q) {
+          const double *x = pb->srf_pts + 7 * ((size_t)r.so + q);
+          strm.insert(strm.end(), x, x + 7);
+          strm.push_back(0.0);
+        }
+        strm.insert(strm.end(), fac.begin() + 4 * (size_t)r.fo, fac.begin() + 4 * ((size_t)r.fo + cf));
+        cur.bytes += bytes;
+        ++cur.nch;
+      }
+      if (cur.nch > 0) pk.push_back(cur);
+    }
+    ps.push_back((int)pk.size());
     hd->w_off[0] = hd->w_off[1];
     hd->grid_cutp[0] = -1;  // part 0 launches parts 1 and 2 (see launch_tiles)
     if ((rc = upload(hd, &hd->d_cdesc2, c2o.data(), c2o.size()))) return rc;
     if ((rc = upload(hd, &hd->d_fac, fac.data(), fac.size()))) return rc;
     if ((rc = upload(hd, &hd->d_wstart, ws.data(), ws.size()))) return rc;
-    if ((rc = upload(hd, &hd->d_kstart, ks.data(), ks.size()))) return rc;
-    if ((rc = upload(hd, &hd->d_chunks, chunk.data(), chunk.size()))) return rc;
+    if ((rc = upload(hd, &hd->d_kstart, ps.data(), ps.size()))) return rc;
+    if ((rc = upload(hd, &hd->d_chunks, pk.data(), pk.size()))) return rc;
+    if ((rc = upload(hd, &hd->d_stream, reinterpret_cast<const char *>(strm.data()), strm.size() * 8))) return rc;
     {
       int64_t mx = (int64_t)fac.size() / 4;
       for (const CDesc2 &e : c2) mx = std::max(mx, std::max(e.vb + e.nv, e.sb + e.ns));
@@ -660,7 +698,7 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
       if (part != 0 && part != pt) continue;
       if (hd->grid_cutp[pt] <= 0) continue;
       k_cutp<NT><<<hd->grid_cutp[pt], 32 * CP::WARPS, CP::SMEM, fork ? hd->side : st>>>(
-          u, v, hd->d_cdesc2 + hd->r_off[pt][2], hd->d_chunks, hd->d_vol, hd->d_srf, hd->d_fac,
+          u, v, hd->d_cdesc2 + hd->r_off[pt][2], hd->d_chunks, hd->d_stream,
           hd->d_wstart + hd->w_off[pt], hd->d_kstart + hd->w_off[pt], hd->kp,
           *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data()));
     }
@@ -868,6 +906,7 @@ void free_handle(cutfem_handle *hd) {
   cudaFree(hd->d_wstart);
   cudaFree(hd->d_kstart);
   cudaFree(hd->d_chunks);
+  cudaFree(hd->d_stream);
   cudaFree(hd->d_fac);
   cudaFree(hd->d_cdesc);
   cudaFree(hd->d_vol);

@@ -125,6 +125,20 @@ struct __align__(16) CChunk {
   int32_t cnt;  // cv | cs << 8 | cf << 16
 };
 
+// A packet: consecutive chunks of one warp's stream, stored contiguously (each
+// chunk = a 16-byte header {cnt} followed by its rows), fetched by ONE bulk copy.
+struct __align__(16) CPacket {
+  int64_t off;    // byte offset in the stream buffer
+  int32_t bytes;  // multiple of 16
+  int32_t nch;    // chunks in the packet
+};
+#ifndef CUTP_PK
+#define CUTP_PK 4096  // packet capacity (bytes)
+#endif
+#ifndef CUTP_NB
+#define CUTP_NB 3  // packet ring depth
+#endif
+
 // values only (cut-face points need no in-face derivatives)
 template <int N>
 __device__ __forceinline__ void basis_v_sym(const RefTab &R, double x, double (&v)[N]) {
@@ -199,26 +213,27 @@ template <int N>
 struct CutPCfg {
   static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
   static constexpr int WARPS = CUTP_WARPS;
-  static constexpr int NB = 4;  // point-chunk ring depth (3 chunks in flight while one is computed)
+  static constexpr int NB = CUTP_NB;  // packet ring depth (NB-1 packets in flight while one is consumed)
+  static constexpr int PK = CUTP_PK;  // packet capacity in bytes (>= the largest chunk, 16 + 32 * 64)
   static constexpr int NN = N * N, N3 = N * N * N, N3P = (N3 + 1) & ~1;
   static constexpr int ACC = N == 4 ? 64 : (N == 3 ? 32 : 8);  // padded n^3 (power of two)
-  // bars(2 + NB) | UB[2][7][N3P] | JAB[6][2][NN] | ring[NB][2 + 256] (header + rows)
+  // bars(2 + NB) | UB[2][7][N3P] | JAB[6][2][NN] | ring[NB][2 + PK/8] (nch + packet)
   static constexpr int OFF_UB = (2 + NB + 1) & ~1;
   static constexpr int OFF_JAB = OFF_UB + 2 * 7 * N3P;
   static constexpr int OFF_RING = OFF_JAB + ((6 * 2 * NN + 1) & ~1);
-  static constexpr int RSLOT = 2 + 256;
+  static constexpr int RSLOT = 2 + PK / 8;
   static constexpr int OFF_WS = OFF_RING + NB * RSLOT;  // w of the structured faces (n^3)
-  static constexpr int OFF_RED = OFF_WS + ((N3 + 1) & ~1);  // reduction transpose [32][33]
-  static constexpr int WSLOT = OFF_RED + 32 * 33;
+  static constexpr int OFF_RED = OFF_WS + ((N3 + 1) & ~1);  // reduction transpose [RW][33]
+  static constexpr int RW = ACC < 16 ? ACC : 16;                // accumulators per reduction pass
+  static constexpr int WSLOT = OFF_RED + RW * 33;
   static constexpr int SMEM = WARPS * WSLOT * 8;
 };
 
 template <int N>
 __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const double *__restrict__ u, double *__restrict__ v,
-                                              const CDesc2 *__restrict__ desc, const CChunk *__restrict__ chunks,
-                                              const double *__restrict__ vol_pts, const double *__restrict__ srf_pts,
-                                              const double *__restrict__ fac_pts, const int *__restrict__ wstart,
-                                              const int *__restrict__ kstart, KParams kp, TileTab<N> tt) {
+                                              const CDesc2 *__restrict__ desc, const CPacket *__restrict__ packets,
+                                              const char *__restrict__ stream, const int *__restrict__ wstart,
+                                              const int *__restrict__ pstart, KParams kp, TileTab<N> tt) {
   static_assert(2 * N * N <= 32, "k_cutp needs N <= 4");
   using C = CutPCfg<N>;
   using LN = BlkU<N>;
@@ -226,13 +241,13 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
   const RefTab &R = c_ref[N - 2];
   extern __shared__ __align__(16) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // warp gw owns cells [wstart[gw], wstart[gw+1]) and their chunks [kstart[gw], kstart[gw+1])
+  // warp gw owns cells [wstart[gw], wstart[gw+1]) and their packets [pstart[gw], pstart[gw+1])
   // (longest-processing-time assignment computed at setup, heaviest first)
   const int gw = blockIdx.x * C::WARPS + warp;
   const int c0w = wstart[gw], c1w = wstart[gw + 1];
   if (c0w >= c1w) return;
   TL_BEGIN(0);
-  const int k0w = kstart[gw], k1w = kstart[gw + 1];
+  const int p0w = pstart[gw], p1w = pstart[gw + 1];
   double *base = smem + warp * C::WSLOT;
   uint64_t *bar = reinterpret_cast<uint64_t *>(base);  // 0,1: block sets; 2..2+NB: chunk ring
   double *UB = base + C::OFF_UB, *JAB = base + C::OFF_JAB, *RING = base + C::OFF_RING, *WS = base + C::OFF_WS;
@@ -269,17 +284,14 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
       cp_async_commit();
     }
   };
-  // chunk j of the warp's list (record r) into ring slot j % NB (lane 0)
-  auto issue_chunk = [&](int j, const CChunk &r) {
-    if (lane != 0 || j >= k1w) return;
-    const int b = (j - k0w) % NB;
+  // packet j of the warp's list (record r) into ring slot (j - p0w) % NB (lane 0)
+  auto issue_packet = [&](int j, const CPacket &r) {
+    if (lane != 0 || j >= p1w) return;
+    const int b = (j - p0w) % NB;
     double *S = RING + b * C::RSLOT;
-    const int cv = r.cnt & 0xff, cs = (r.cnt >> 8) & 0xff, cf = (r.cnt >> 16) & 0xff;
-    reinterpret_cast<int *>(S)[0] = r.cnt;
-    mbar_expect_tx(bar + 2 + b, (uint32_t)(cv * 32 + cs * 64 + cf * 32));
-    if (cv) bulk_g2s(S + 2, vol_pts + 4 * (size_t)r.vo, (uint32_t)(cv * 32), bar + 2 + b);
-    if (cs) bulk_g2s(S + 2 + 4 * cv, srf_pts + 8 * (size_t)r.so, (uint32_t)(cs * 64), bar + 2 + b);
-    if (cf) bulk_g2s(S + 2 + 4 * cv + 8 * cs, fac_pts + 4 * (size_t)r.fo, (uint32_t)(cf * 32), bar + 2 + b);
+    reinterpret_cast<int *>(S)[0] = r.nch;
+    mbar_expect_tx(bar + 2 + b, (uint32_t)r.bytes);
+    bulk_g2s(S + 2, stream + r.off, (uint32_t)r.bytes, bar + 2 + b);
   };
   if (lane == 0) {
 #pragma unroll
@@ -289,15 +301,16 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
   __syncwarp();
   CDesc2 cd = desc[c0w];
   issue_blocks(cd, 0);
-  // prologue: NB-1 chunks in flight, the record of the next one prefetched into a register
-  CChunk rn = {0, 0, 0, 0};
+  // prologue: NB-1 packets in flight, the record of the next one prefetched into a register
+  CPacket rn = {0, 0, 0};
   if (lane == 0) {
 #pragma unroll
     for (int j = 0; j < NB - 1; ++j)
-      if (k0w + j < k1w) issue_chunk(k0w + j, chunks[k0w + j]);
-    if (k0w + NB - 1 < k1w) rn = chunks[k0w + NB - 1];
+      if (p0w + j < p1w) issue_packet(p0w + j, packets[p0w + j]);
+    if (p0w + NB - 1 < p1w) rn = packets[p0w + NB - 1];
   }
-  int j = k0w;  // next chunk to consume
+  int pj = p0w - 1, left = 0, pos = 0;  // packet being consumed, its chunks left, read position
+  const double *S = RING;
   const double ih = kp.ih, ih2 = kp.ih2;
   int it = 0;
   for (int c = c0w; c < c1w; ++c, ++it) {
@@ -436,22 +449,29 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     double acc[C::ACC];
 #pragma unroll
     for (int i = 0; i < C::ACC; ++i) acc[i] = 0.0;
-    for (int k = 0; k < K; ++k, ++j) {
-      const int b = (j - k0w) % NB;
-      mbar_wait(bar + 2 + b, ((j - k0w) / NB) & 1);
-      // refill: chunk j+NB-1 goes to the slot consumed at j-1
-      if (lane == 0) {
-        issue_chunk(j + NB - 1, rn);
-        if (j + NB < k1w) rn = chunks[j + NB];
+    for (int k = 0; k < K; ++k) {
+      if (left == 0) {  // next packet: wait for it, refill the slot of the previous one
+        ++pj;
+        const int b = (pj - p0w) % NB;
+        mbar_wait(bar + 2 + b, ((pj - p0w) / NB) & 1);
+        if (lane == 0) {
+          issue_packet(pj + NB - 1, rn);
+          if (pj + NB < p1w) rn = packets[pj + NB];
+        }
+        S = RING + b * C::RSLOT;
+        left = reinterpret_cast<const int *>(S)[0];
+        pos = 2;
       }
-      const double *S = RING + b * C::RSLOT;
-      const int cnt = reinterpret_cast<const int *>(S)[0];
+      const int cnt = reinterpret_cast<const int *>(S + pos)[0];
       const int cv = cnt & 0xff, cs = (cnt >> 8) & 0xff, cf = (cnt >> 16) & 0xff;
+      const double *P = S + pos + 2;  // the chunk's rows
+      pos += 2 + 4 * cv + 8 * cs + 4 * cf;
+      --left;
       // kind: 0 volume, 1 interface, 2 cut face, 3 idle lane
       const int kind = lane < cv ? 0 : (lane < cv + cs ? 1 : (lane < cv + cs + cf ? 2 : 3));
       double xi = 0.5, eta = 0.5, zeta = 0.5, W = 0.0, nx = 0.0, ny = 0.0, nz = 0.0;
       if (kind == 0 || kind == 2) {
-        const double *pp = S + 2 + (kind == 0 ? 4 * lane : 4 * cv + 8 * cs + 4 * (lane - cv - cs));
+        const double *pp = P + (kind == 0 ? 4 * lane : 4 * cv + 8 * cs + 4 * (lane - cv - cs));
         const double2 p0 = *reinterpret_cast<const double2 *>(pp);
         const double2 p1 = *reinterpret_cast<const double2 *>(pp + 2);
         xi = p0.x;
@@ -459,7 +479,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
         zeta = p1.x;
         W = p1.y;
       } else if (kind == 1) {
-        const double *pp = S + 2 + 4 * cv + 8 * (lane - cv);
+        const double *pp = P + 4 * cv + 8 * (lane - cv);
         const double2 p0 = *reinterpret_cast<const double2 *>(pp);
         const double2 p1 = *reinterpret_cast<const double2 *>(pp + 2);
         const double2 p2 = *reinterpret_cast<const double2 *>(pp + 4);
@@ -516,22 +536,22 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
         else if (d == 1) face_point<N, 1>(acc, R, JAB, xi, eta, zeta, W, kp);
         else face_point<N, 2>(acc, R, JAB, xi, eta, zeta, W, kp);
       }
-      __syncwarp();  // every lane is done with ring slot b before it is refilled
-      if (lane == 0) fence_proxy_async();
+      __syncwarp();  // every lane is done with the ring slot before it is refilled
+      if (lane == 0 && left == 0) fence_proxy_async();
     }
     // ---- reduce over the warp and write the block (every cut cell block written once)
-    // padded shared-memory transpose, 32 entries per pass: lane l sums entry
-    // 32 pass + l over the 32 lanes (fixed order)
+    // padded shared-memory transpose, RW entries per pass: lane l < RW sums entry
+    // RW pass + l over the 32 lanes (fixed order)
     double *RED = base + C::OFF_RED;
     double *vb = v + (size_t)cd.blk * N3;
     const bool st_on = (gm | sm) != 0;
+    constexpr int RW = C::RW;
 #pragma unroll
-    for (int ps = 0; ps < (C::ACC + 31) / 32; ++ps) {
-      constexpr int RW = C::ACC < 32 ? C::ACC : 32;
+    for (int ps = 0; ps < C::ACC / RW; ++ps) {
 #pragma unroll
-      for (int i = 0; i < RW; ++i) RED[i * 33 + lane] = acc[ps * 32 + i];
+      for (int i = 0; i < RW; ++i) RED[i * 33 + lane] = acc[ps * RW + i];
       __syncwarp();
-      const int l = ps * 32 + lane;
+      const int l = ps * RW + lane;
       if (lane < RW && l < N3) {
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
