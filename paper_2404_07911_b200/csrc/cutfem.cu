@@ -1277,12 +1277,15 @@ int cutfem_debug_timeline(int reset, unsigned long long *out) {
       h[k][1] = 0;
     }
     CU(cudaMemcpyToSymbol(g_tl, h, sizeof(h)));
+    std::vector<unsigned long long> z(8192, 0);
+    CU(cudaMemcpyToSymbol(g_tlw, z.data(), sizeof(unsigned long long) * 8192));
   } else {
     CU(cudaMemcpyFromSymbol(h, g_tl, sizeof(h)));
     for (int k = 0; k < 8; ++k) {
       out[2 * k] = h[k][0];
       out[2 * k + 1] = h[k][1];
     }
+    CU(cudaMemcpyFromSymbol(out + 16, g_tlw, sizeof(unsigned long long) * 8192));
   }
   return 0;
 #else

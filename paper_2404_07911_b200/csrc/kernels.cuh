@@ -31,6 +31,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+__device__ unsigned long long g_tlw[8192];  // k_cutp: per-warp end time
+#define TL_WARP_END(gw) \
+  if ((threadIdx.x & 31) == 0 && (gw) < 8192) g_tlw[gw] = gtimer();
 #define TL_BEGIN(k) \
   if (threadIdx.x == 0) atomicMin(&g_tl[k][0], gtimer());
 #define TL_END(k) \
@@ -38,6 +41,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #else
 #define TL_BEGIN(k)
 #define TL_END(k)
+#define TL_WARP_END(gw)
 #endif
 #ifndef CUTFEM_USE_BULK
 #define CUTFEM_USE_BULK 1
@@ -473,7 +477,30 @@ __global__ void __launch_bounds__(128) k_uncut(const double *__restrict__ u, dou
   }
 }
 
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K)); }
+
 // ============================================================== cut cells
+#ifndef CUT_PREF_MAXN
+#define CUT_PREF_MAXN 7
+#endif
+#ifndef CUT_ROWINT_MINN
+#define CUT_ROWINT_MINN 5
+#endif
+#ifndef CUT_RPT
+#define CUT_RPT 3  // x-rows per thread in the row integration, n = 5, 6
+#endif
+#ifndef CUT_RPT7
+#define CUT_RPT7 3  // n >= 7
+#endif
+#ifndef CUT_SPLIT_MASK
+#define CUT_SPLIT_MASK 0x2ff  // bit n: split the point phase over THREADS / CHUNK threads (not n = 8: measured slower)
+#endif
 template <int N>
 struct CutCfg {
   static constexpr int THREADS = 128;
@@ -486,12 +513,18 @@ struct CutCfg {
   // integration phase: each thread owns RPT x-rows (b, c) of the block (sharing the
   // x-basis loads), TG threads cover the N^2 rows, G groups split the chunk's points
   // (N >= 7; below, one thread per DoF looping over the points is faster)
-  static constexpr bool ROWINT = N >= 7;
-  static constexpr int RPT = ROWINT ? 4 : 1;
+  static constexpr bool ROWINT = N >= CUT_ROWINT_MINN;
+  static constexpr int RPT = ROWINT ? (N >= 7 ? CUT_RPT7 : CUT_RPT) : 1;
   static constexpr int TG = ROWINT ? (NN + RPT - 1) / RPT : THREADS;
   static constexpr int G = ROWINT ? THREADS / TG : 1;
-  // U, NB, T, R (padded blocks) + JA, JB, FC1, FC2 (NN each) + point rows
-  static constexpr int SMEM_D = 4 * Blk<N>::SZ + 4 * NN + CHUNK * ROW;
+  // per-point phase: SPL threads per point, each evaluating CPS of the N z-planes
+  static constexpr int SPL = ((CUT_SPLIT_MASK >> N) & 1) ? THREADS / CHUNK : 1, CPS = (N + SPL - 1) / SPL;
+  // neighbour blocks prefetched (cp.async at entry, overlapping the point work) up
+  // to n = CUT_PREF_MAXN; above, loaded face by face
+  static constexpr bool PREF = N <= CUT_PREF_MAXN;
+  static constexpr int NBN = PREF ? 6 : 1;
+  // U, T, R, NB[NBN] (padded blocks) + JA, JB, FC1, FC2 (NN each) + point rows
+  static constexpr int SMEM_D = (3 + NBN) * Blk<N>::SZ + 4 * NN + CHUNK * ROW;
   static constexpr int SMEM = SMEM_D * 8;
 };
 
@@ -566,10 +599,12 @@ __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int
   constexpr int NN = C::NN, ROW = C::ROW, RPT = C::RPT, TG = C::TG, G = C::G;
   const int tid = threadIdx.x;
   const int grp = tid / TG, rl = tid % TG;
+  constexpr int SPL = C::SPL, CPS = C::CPS;
+  const int pq = tid / SPL, part = tid % SPL;  // point of the chunk, z-plane share
   const double h = kp.h, ih = 1.0 / h, ih2 = ih * ih;
   for (int64_t c0 = pb; c0 < pe; c0 += C::CHUNK) {
-    if (tid < C::CHUNK) {
-      const int64_t q = c0 + tid;
+    if (pq < C::CHUNK) {
+      const int64_t q = c0 + pq;
       double xi = 0.5, eta = 0.5, zeta = 0.5, W = 0.0, nx = 0.0, ny = 0.0, nz = 0.0;
       if (q < pe) {
         if (SURF) {
@@ -594,8 +629,54 @@ __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int
       basis_vd<N>(R, xi, vx, dvx);
       basis_vd<N>(R, eta, vy, dvy);
       basis_vd<N>(R, zeta, vz, dvz);
-      double u0, ux, uy, uz;
-      eval_point<N>(U, vx, dvx, vy, dvy, vz, dvz, u0, ux, uy, uz);
+      // this thread's z-planes c = part * CPS + cc (cc < CPS, c < N)
+      double vzl[CPS], dvzl[CPS];
+#pragma unroll
+      for (int cc = 0; cc < CPS; ++cc) {
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int k = 0; k < SPL; ++k)
+          if (k * CPS + cc < N && part == k) {
+            a = vz[k * CPS + cc];
+            b = dvz[k * CPS + cc];
+          }
+        vzl[cc] = a;
+        dvzl[cc] = b;
+      }
+      double u0 = 0.0, ux = 0.0, uy = 0.0, uz = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < CPS; ++cc) {
+        const int c = part * CPS + cc;
+        if ((N % SPL) != 0 && c >= N) break;
+        double t00 = 0.0, t10 = 0.0, t01 = 0.0;
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+          double s0 = 0.0, s1 = 0.0;
+          const double *row = U + c * Blk<N>::PS + b * Blk<N>::P;
+#pragma unroll
+          for (int a = 0; a < N; ++a) {
+            const double uu = row[a];
+            s0 = fma(vx[a], uu, s0);
+            s1 = fma(dvx[a], uu, s1);
+          }
+          t00 = fma(vy[b], s0, t00);
+          t10 = fma(dvy[b], s0, t10);
+          t01 = fma(vy[b], s1, t01);
+        }
+        u0 = fma(vzl[cc], t00, u0);
+        uz = fma(dvzl[cc], t00, uz);
+        uy = fma(vzl[cc], t10, uy);
+        ux = fma(vzl[cc], t01, ux);
+      }
+      // sum the SPL partial evaluations (xor butterfly: every thread of the point
+      // gets the same bits)
+#pragma unroll
+      for (int o = 1; o < SPL; o <<= 1) {
+        u0 += __shfl_xor_sync(0xffffffffu, u0, o);
+        ux += __shfl_xor_sync(0xffffffffu, ux, o);
+        uy += __shfl_xor_sync(0xffffffffu, uy, o);
+        uz += __shfl_xor_sync(0xffffffffu, uz, o);
+      }
       // B: quadrature-point operation
       double c0v, c1, c2, c3;
       if (SURF) {
@@ -612,26 +693,26 @@ __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int
         c2 = sw * uy;
         c3 = sw * uz;
       }
-      // I (z and y stages per point); the x stage is the row integration below
-      double T0[N], T1[N], T2[N];
+      // I (z and y stages per point, this thread's z-planes); the x stage is the
+      // row integration below
+      double *row = PS + pq * ROW;
 #pragma unroll
-      for (int c = 0; c < N; ++c) {
-        T0[c] = fma(c0v, vz[c], c3 * dvz[c]);
-        T1[c] = c2 * vz[c];
-        T2[c] = c1 * vz[c];
-      }
-      double *row = PS + tid * ROW;
-#pragma unroll
-      for (int c = 0; c < N; ++c)
+      for (int cc = 0; cc < CPS; ++cc) {
+        const int c = part * CPS + cc;
+        if ((N % SPL) != 0 && c >= N) break;
+        const double T0 = fma(c0v, vzl[cc], c3 * dvzl[cc]), T1 = c2 * vzl[cc], T2 = c1 * vzl[cc];
 #pragma unroll
         for (int b = 0; b < N; ++b) {
-          row[b + N * c] = fma(vy[b], T0[c], dvy[b] * T1[c]);
-          row[NN + b + N * c] = vy[b] * T2[c];
+          row[b + N * c] = fma(vy[b], T0, dvy[b] * T1);
+          row[NN + b + N * c] = vy[b] * T2;
         }
+      }
+      if (part == 0) {
 #pragma unroll
-      for (int a = 0; a < N; ++a) {
-        row[2 * NN + a] = vx[a];
-        row[2 * NN + N + a] = dvx[a];
+        for (int a = 0; a < N; ++a) {
+          row[2 * NN + a] = vx[a];
+          row[2 * NN + N + a] = dvx[a];
+        }
       }
     }
     __syncthreads();
@@ -691,11 +772,27 @@ __global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, doubl
   constexpr int NN = B::NN, N3 = B::N3, SZ = B::SZ, TH = C::THREADS;
   const RefTab &R = c_ref[N - 2];
   extern __shared__ double smem[];
-  double *U = smem, *NB = smem + SZ, *T = smem + 2 * SZ, *Rb = smem + 3 * SZ;
-  double *JA = smem + 4 * SZ, *JB = JA + NN, *FC1 = JB + NN, *FC2 = FC1 + NN;
+  double *U = smem, *T = smem + SZ, *Rb = smem + 2 * SZ, *NBs = smem + 3 * SZ;
+  double *JA = smem + (3 + C::NBN) * SZ, *JB = JA + NN, *FC1 = JB + NN, *FC2 = FC1 + NN;
   double *PS = FC2 + NN;
   const int tid = threadIdx.x;
   const CDesc dsc = desc[blockIdx.x];
+  auto face_on = [&](int f, bool &gp, bool &ss, bool &sc) {
+    gp = ((dsc.flags >> f) & 1u) && (kp.mask & TERM_GP);
+    ss = ((dsc.flags >> (6 + f)) & 1u) && (kp.mask & TERM_SIPG);
+    sc = ((dsc.flags >> (12 + f)) & 1u) && (kp.mask & TERM_SIPG);
+    return dsc.nb[f] >= 0 && (gp || ss || sc);
+  };
+  if constexpr (C::PREF) {
+    // the neighbour blocks of every face with work, in flight during the point phases
+    for (int f = 0; f < 6; ++f) {
+      bool gp, ss, sc;
+      if (!face_on(f, gp, ss, sc)) continue;
+      const double *nbp = u + (size_t)dsc.nb[f] * N3;
+      for (int l = tid; l < N3; l += TH) cp_async8(NBs + f * SZ + B::pad(l), nbp + l);
+    }
+    cp_async_commit();
+  }
   {
     const double *ub = u + (size_t)dsc.blk * N3;
     for (int l = tid; l < N3; l += TH) U[B::pad(l)] = __ldg(ub + l);
@@ -740,18 +837,19 @@ __global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, doubl
   __syncthreads();
 
   const double h = kp.h, h2 = h * h;
-  for (int f = 0; f < 6; ++f) {
-    const int nbk = dsc.nb[f];
-    if (nbk < 0) continue;
-    const bool gp = ((dsc.flags >> f) & 1u) && (kp.mask & TERM_GP);
-    const bool ss = ((dsc.flags >> (6 + f)) & 1u) && (kp.mask & TERM_SIPG);
-    const bool sc = ((dsc.flags >> (12 + f)) & 1u) && (kp.mask & TERM_SIPG);
-    if (!(gp || ss || sc)) continue;
-    {
-      const double *nbp = u + (size_t)nbk * N3;
-      for (int l = tid; l < N3; l += TH) NB[B::pad(l)] = __ldg(nbp + l);
-    }
+  if constexpr (C::PREF) {
+    cp_async_wait<0>();
     __syncthreads();
+  }
+  for (int f = 0; f < 6; ++f) {
+    bool gp, ss, sc;
+    if (!face_on(f, gp, ss, sc)) continue;
+    double *NB = C::PREF ? NBs + f * SZ : NBs;
+    if constexpr (!C::PREF) {
+      const double *nbp = u + (size_t)dsc.nb[f] * N3;
+      for (int l = tid; l < N3; l += TH) NB[B::pad(l)] = __ldg(nbp + l);
+      __syncthreads();
+    }
     const int dd = f >> 1, side = f & 1;
     const int fo = side ? N - 1 : 0, fn = side ? 0 : N - 1;
     const double sg = side ? 1.0 : -1.0;
@@ -897,13 +995,6 @@ __global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, doubl
 // The cell block and its six neighbour blocks are fetched with cp.async at
 // kernel entry, overlapping the point work.
 
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int K>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K)); }
 
 // Warp reduce-scatter of L per-lane partial sums (L a power of two <= 64).
 // Afterwards value j of lane l is the warp sum of entry idx(l, j) =

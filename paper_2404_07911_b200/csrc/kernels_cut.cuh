@@ -133,10 +133,13 @@ struct __align__(16) CPacket {
   int32_t nch;    // chunks in the packet
 };
 #ifndef CUTP_PK
-#define CUTP_PK 4096  // packet capacity (bytes)
+#define CUTP_PK 4608  // packet capacity (bytes)
 #endif
 #ifndef CUTP_NB
 #define CUTP_NB 3  // packet ring depth
+#endif
+#ifndef CUTP_RW
+#define CUTP_RW 16  // rows of the reduction transpose buffer
 #endif
 
 // values only (cut-face points need no in-face derivatives)
@@ -224,7 +227,7 @@ struct CutPCfg {
   static constexpr int RSLOT = 2 + PK / 8;
   static constexpr int OFF_WS = OFF_RING + NB * RSLOT;  // w of the structured faces (n^3)
   static constexpr int OFF_RED = OFF_WS + ((N3 + 1) & ~1);  // reduction transpose [RW][33]
-  static constexpr int RW = ACC < 16 ? ACC : 16;                // accumulators per reduction pass
+  static constexpr int RW = ACC < CUTP_RW ? ACC : CUTP_RW;      // accumulators per reduction pass
   static constexpr int WSLOT = OFF_RED + RW * 33;
   static constexpr int SMEM = WARPS * WSLOT * 8;
 };
@@ -568,6 +571,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     if constexpr (!C::BULK) __syncwarp();
     if (has_next) cd = nd;
   }
+  TL_WARP_END(gw);
   TL_END(0);
 }
 

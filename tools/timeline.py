@@ -30,9 +30,14 @@ for rep in range(4):
     op.apply(u, v)
     b.record()
     torch.cuda.synchronize()
-    out = (ctypes.c_ulonglong * 16)()
+    out = (ctypes.c_ulonglong * (16 + 8192))()
     L.cutfem_debug_timeline(0, ctypes.addressof(out))
     t0 = min(out[2 * k] for k in names if out[2 * k] != 2 ** 64 - 1)
     row = {names[k]: (round((out[2 * k] - t0) / 1e3, 1), round((out[2 * k + 1] - t0) / 1e3, 1)) for k in names
            if out[2 * k] != 2 ** 64 - 1}
     print(f"apply {a.elapsed_time(b) * 1e3:.1f} us  (start, end) us: {row}")
+    we = np.array([out[16 + i] for i in range(8192)], dtype=np.float64)
+    we = (we[we > 0] - t0) / 1e3
+    if we.size:
+        print("  k_cutp warp end times (us) pct 0/10/25/50/75/90/99/100:",
+              np.round(np.percentile(we, [0, 10, 25, 50, 75, 90, 99, 100]), 1).tolist(), "n", we.size)
