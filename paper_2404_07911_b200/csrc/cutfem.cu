@@ -86,6 +86,8 @@ struct cutfem_handle {
   int *d_wstart = nullptr;      // per part: warp -> first cell (grid_cutp[part] * WARPS + 1 entries)
   int *d_kstart = nullptr;      // per part: warp -> first packet
   CPacket *d_chunks = nullptr;  // packets of the point-chunk stream, per warp in consumption order
+  bool uncw_first = false;      // n = 5, 6: k_uncw launched before k_cut
+  int uncw_ctas = 0;            // n = 5, 6: k_uncw CTAs per SM (0: occupancy)
   char *d_stream = nullptr;     // the packed stream (chunk headers + point rows)
   int64_t w_off[3] = {0};
   int grid_cutp[3] = {0};
@@ -745,11 +747,28 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
   const int64_t nu = np + ng;
   const bool fork = nc > 0 && nu > 0;
   cudaStream_t cs = fork ? hd->side : st;
-  if (nc > 0) {
-    if (fork) {
-      CU(cudaEventRecord(hd->ev_fork, st));
-      CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
+  // n = 5, 6: the persistent uncut kernel (k_uncw) may go first with a capped grid,
+  // leaving room on every SM for the cut-cell CTAs (env CUTFEM_UNCW_FIRST, CUTFEM_UNCW_CTAS)
+  auto launch_uncw = [&]() -> int {
+    if (!(nu > 0 && (N == 5 || N == 6) && hd->d_tiles)) return 0;
+    constexpr int NU = (N == 5 || N == 6) ? N : 5;
+    const int64_t nt = hd->t_cnt[0][part];
+    if (nt > 0) {
+      const int occ = hd->uncw_ctas > 0 ? std::min(hd->uncw_ctas, hd->occ_tile[0]) : hd->occ_tile[0];
+      const unsigned grid = (unsigned)std::min<int64_t>(nt, (int64_t)occ * hd->sm_count);
+      k_uncw<NU><<<grid, UncwCfg<NU>::THREADS, UncwCfg<NU>::SMEM, st>>>(
+          u, v, reinterpret_cast<const TileRec<TileCfg<NU>::SMAX> *>(hd->d_tiles) + hd->t_off[0][part], (int)nt,
+          *reinterpret_cast<const TileTab<NU> *>(hd->ttab.data()), hd->kp.mask);
+      CU(cudaGetLastError());
     }
+    return 0;
+  };
+  if (fork) {
+    CU(cudaEventRecord(hd->ev_fork, st));
+    CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
+  }
+  if (hd->uncw_first) launch_uncw();
+  if (nc > 0) {
     if (N <= 4) {
       using CW = CutWCfg<(N <= 4 ? N : 4)>;
       const unsigned grid = (unsigned)((nc + CW::WARPS - 1) / CW::WARPS);
@@ -764,15 +783,7 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
     CU(cudaGetLastError());
   }
   if (nu > 0 && (N == 5 || N == 6) && hd->d_tiles) {
-    constexpr int NU = (N == 5 || N == 6) ? N : 5;
-    const int64_t nt = hd->t_cnt[0][part];
-    if (nt > 0) {
-      const unsigned grid = (unsigned)std::min<int64_t>(nt, (int64_t)hd->occ_tile[0] * hd->sm_count);
-      k_uncw<NU><<<grid, UncwCfg<NU>::THREADS, UncwCfg<NU>::SMEM, st>>>(
-          u, v, reinterpret_cast<const TileRec<TileCfg<NU>::SMAX> *>(hd->d_tiles) + hd->t_off[0][part], (int)nt,
-          *reinterpret_cast<const TileTab<NU> *>(hd->ttab.data()), hd->kp.mask);
-      CU(cudaGetLastError());
-    }
+    if (!hd->uncw_first) launch_uncw();
   } else if (nu > 0) {
     if (N <= 5) {
       constexpr int NC = (N <= 5 ? N : 5);
@@ -1164,6 +1175,8 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   if ((rc = upload(hd, &hd->d_srfptr, pb->srf_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_sfptr, pb->sf_ptr, (size_t)(nsf ? nsf + 1 : 0)))) return rc;
   hd->cut_last = std::getenv("CUTFEM_CUT_LAST") != nullptr;
+  hd->uncw_first = std::getenv("CUTFEM_UNCW_FIRST") != nullptr;
+  if (const char *e = std::getenv("CUTFEM_UNCW_CTAS")) hd->uncw_ctas = std::atoi(e);
   if (const char *e = std::getenv("CUTFEM_TILE_PERSIST")) hd->persist = std::atoi(e);
   else hd->persist = 3;
   if (!std::getenv("CUTFEM_NO_TILE") && (rc = dispatch_tiles(hd, pb, ud, cd))) return rc;

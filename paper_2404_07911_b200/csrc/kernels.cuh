@@ -481,6 +481,10 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int K>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K)); }
@@ -488,6 +492,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // ============================================================== cut cells
 #ifndef CUT_PREF_MAXN
 #define CUT_PREF_MAXN 7
+#endif
+#ifndef CUT_PPF_MASK
+#define CUT_PPF_MASK 0x300  // bit n: prefetch the point rows (n = 8, 9: measured faster; 6, 7 slower)
 #endif
 #ifndef CUT_ROWINT_MINN
 #define CUT_ROWINT_MINN 5
@@ -524,7 +531,13 @@ struct CutCfg {
   static constexpr bool PREF = N <= CUT_PREF_MAXN;
   static constexpr int NBN = PREF ? 6 : 1;
   // U, T, R, NB[NBN] (padded blocks) + JA, JB, FC1, FC2 (NN each) + point rows
-  static constexpr int SMEM_D = (3 + NBN) * Blk<N>::SZ + 4 * NN + CHUNK * ROW;
+  // point rows of the next chunk prefetched (cp.async, double buffer of 8 doubles a
+  // point) while the current one is processed
+  static constexpr bool PPF = N >= 5 && ((CUT_PPF_MASK >> N) & 1);
+  static constexpr int PBUF = PPF ? 2 * CHUNK * 8 : 0;
+  static constexpr int OFF_PS = (3 + NBN) * Blk<N>::SZ + 4 * NN;
+  static constexpr int OFF_PB = (OFF_PS + CHUNK * ROW + 1) & ~1;  // 16-byte aligned
+  static constexpr int SMEM_D = OFF_PB + PBUF;
   static constexpr int SMEM = SMEM_D * 8;
 };
 
@@ -602,11 +615,52 @@ __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int
   constexpr int SPL = C::SPL, CPS = C::CPS;
   const int pq = tid / SPL, part = tid % SPL;  // point of the chunk, z-plane share
   const double h = kp.h, ih = 1.0 / h, ih2 = ih * ih;
-  for (int64_t c0 = pb; c0 < pe; c0 += C::CHUNK) {
+  constexpr int RL = SURF ? 8 : 4;  // doubles per point row
+  double *PB = PS - C::OFF_PS + C::OFF_PB;  // [2][CHUNK * 8] prefetch buffers (16-byte aligned)
+  // rows [c, min(c + CHUNK, pe)) into buffer b: 16-byte pieces over the CTA
+  auto prefetch = [&](int64_t c, int b) {
+    if constexpr (C::PPF) {
+      const int cnt = (int)((pe - c) < C::CHUNK ? (pe - c) : C::CHUNK);
+      for (int e = tid; e < cnt * (RL / 2); e += C::THREADS)
+        cp_async16(PB + b * C::CHUNK * 8 + 2 * e, pts + RL * c + 2 * e);
+      cp_async_commit();
+    }
+  };
+  if (pb < pe) prefetch(pb, 0);
+  int it = 0;
+  for (int64_t c0 = pb; c0 < pe; c0 += C::CHUNK, ++it) {
+    if constexpr (C::PPF) {
+      // the next chunk goes to the other buffer (last read before the previous
+      // chunk's integration barrier); wait for this one
+      if (c0 + C::CHUNK < pe) {
+        prefetch(c0 + C::CHUNK, (it + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+    }
     if (pq < C::CHUNK) {
       const int64_t q = c0 + pq;
       double xi = 0.5, eta = 0.5, zeta = 0.5, W = 0.0, nx = 0.0, ny = 0.0, nz = 0.0;
-      if (q < pe) {
+      if (C::PPF && q < pe) {
+        const double *p = PB + (it & 1) * C::CHUNK * 8 + RL * pq;
+        const double2 a = *reinterpret_cast<const double2 *>(p);
+        const double2 b = *reinterpret_cast<const double2 *>(p + 2);
+        xi = a.x;
+        eta = a.y;
+        zeta = b.x;
+        if (SURF) {
+          const double2 c = *reinterpret_cast<const double2 *>(p + 4);
+          const double2 d = *reinterpret_cast<const double2 *>(p + 6);
+          nx = b.y;
+          ny = c.x;
+          nz = c.y;
+          W = d.x;
+        } else {
+          W = b.y;
+        }
+      } else if (q < pe) {
         if (SURF) {
           const double *p = pts + 8 * q;
           xi = __ldg(p);
