@@ -280,6 +280,13 @@ void build_tiletab(double h, double sipg_gamma, const double *gpg, TileTab<N> &t
     }
 }
 
+template <int N>
+int build_ttab(cutfem_handle *hd, const cutfem_problem *pb) {
+  hd->ttab.resize(sizeof(TileTab<N>));
+  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
+  return 0;
+}
+
 // ---- k_tile*: one cell of a tile set: block, face neighbours, face masks
 struct TCell {
   int32_t blk;
@@ -778,7 +785,7 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
     } else {
       k_cut<N><<<(unsigned)nc, CutCfg<N>::THREADS, CutCfg<N>::SMEM, cs>>>(
           u, v, dc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp, hd->d_sfptr, hd->kp,
-          hd->ft);
+          hd->ft, *reinterpret_cast<const TileTab<N> *>(hd->ttab.data()));
     }
     CU(cudaGetLastError());
   }
@@ -1181,6 +1188,20 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   else hd->persist = 3;
   if (!std::getenv("CUTFEM_NO_TILE") && (rc = dispatch_tiles(hd, pb, ud, cd))) return rc;
   if ((rc = upload_tables(p))) return rc;
+  if (hd->ttab.empty()) {  // line operators for k_cut's structured faces (any degree)
+    switch (p + 1) {
+      case 2: rc = build_ttab<2>(hd, pb); break;
+      case 3: rc = build_ttab<3>(hd, pb); break;
+      case 4: rc = build_ttab<4>(hd, pb); break;
+      case 5: rc = build_ttab<5>(hd, pb); break;
+      case 6: rc = build_ttab<6>(hd, pb); break;
+      case 7: rc = build_ttab<7>(hd, pb); break;
+      case 8: rc = build_ttab<8>(hd, pb); break;
+      case 9: rc = build_ttab<9>(hd, pb); break;
+      default: break;
+    }
+    if (rc) return rc;
+  }
   if ((rc = dispatch_attrs(n))) return rc;
   {
     int dev = device, smc = 148;

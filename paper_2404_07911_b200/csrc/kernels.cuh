@@ -76,6 +76,31 @@ __constant__ RefTab c_ref[8];  // index N - 2
 //   Goo[s][m][a] = h sum_j g_j e_j[m] e_j[a], Gon[s][m][a] = h sum_j g_j e_j[m] o_j[a]
 // with e_j = l^(j)(own face), o_j = l^(j)(neighbour face); s = 0 own cell is the
 // minus side (face at xi_d = 1), s = 1 own cell is the plus side.
+// Per-handle line operators (h, penalties folded), all warp-uniform.  Only the
+// lo-face (s = 0) variants are stored: every 1-D operator here is
+// centro-symmetric (GLL nodes and Gauss points are symmetric about 1/2), so the
+// hi face uses the reversed entries:  l'_a(1) = -l'_{n-1-a}(0),
+// cJ_hi[m] = cJ_lo[n-1-m], cA_hi[m] = -cA_lo[n-1-m], G_hi[m][a] = G_lo[n-1-m][n-1-a],
+// and L, M satisfy X[i][j] = X[n-1-i][n-1-j].  Reading only the canonical half
+// keeps ~20 distinct constants live next to the 64-double accumulator.
+template <int N>
+struct TileTab {
+  double L[N * N];    // M^{-1} h K1: volume term along one axis
+  double M[N * N];    // GLL mass M1
+  double d0[N];       // l'_a(0)
+  double cJ[N];       // SIPG (lo face): w_line += cJ [u] + cA (d u_own + d u_nb)
+  double cA[N];
+  double Goo[N * N];  // ghost penalty (lo face), own line:        M^{-1} G_oo
+  double Gon[N * N];  // ghost penalty (lo face), neighbour line: -M^{-1} G_on
+};
+
+// canonical index of a centro-symmetric n x n matrix entry
+template <int N>
+__device__ __forceinline__ constexpr int csym(int k) {
+  return k < N * N - 1 - k ? k : N * N - 1 - k;
+}
+
+
 struct FaceTab {
   double Goo[2][CUTFEM_NMAX * CUTFEM_NMAX];
   double Gon[2][CUTFEM_NMAX * CUTFEM_NMAX];
@@ -493,6 +518,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef CUT_PREF_MAXN
 #define CUT_PREF_MAXN 7
 #endif
+#ifndef CUT_WFACE_MASK
+#define CUT_WFACE_MASK 0x40
+#endif
 #ifndef CUT_PPF_MASK
 #define CUT_PPF_MASK 0x300  // bit n: prefetch the point rows (n = 8, 9: measured faster; 6, 7 slower)
 #endif
@@ -530,6 +558,9 @@ struct CutCfg {
   // to n = CUT_PREF_MAXN; above, loaded face by face
   static constexpr bool PREF = N <= CUT_PREF_MAXN;
   static constexpr int NBN = PREF ? 6 : 1;
+  // structured faces in w-space (one parallel pass + one M (x) M (x) M sweep) instead
+  // of face by face; needs the prefetched neighbours (measured faster at n = 6 only)
+  static constexpr bool WFACE = PREF && ((CUT_WFACE_MASK >> N) & 1);
   // U, T, R, NB[NBN] (padded blocks) + JA, JB, FC1, FC2 (NN each) + point rows
   // point rows of the next chunk prefetched (cp.async, double buffer of 8 doubles a
   // point) while the current one is processed
@@ -820,7 +851,8 @@ __global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, doubl
                                              const double *__restrict__ srf_pts,
                                              const int64_t *__restrict__ srf_ptr,
                                              const double *__restrict__ sf_pts,
-                                             const int64_t *__restrict__ sf_ptr, KParams kp, FaceTab ft) {
+                                             const int64_t *__restrict__ sf_ptr, KParams kp, FaceTab ft,
+                                             TileTab<N> tt) {
   using B = Blk<N>;
   using C = CutCfg<N>;
   constexpr int NN = B::NN, N3 = B::N3, SZ = B::SZ, TH = C::THREADS;
@@ -894,10 +926,99 @@ __global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, doubl
   if constexpr (C::PREF) {
     cp_async_wait<0>();
     __syncthreads();
+    // structured faces (ghost penalty, full-face SIPG) in w-space (as k_cutp): per
+    // (axis, line) item both faces of the axis through M^{-1}-premultiplied line
+    // operators (the hi face in the line-reversed frame with the lo-face
+    // coefficients), one buffer per axis; then v += (M (x) M (x) M) sum_axes w
+    uint32_t gmk = 0, smk = 0;
+#pragma unroll
+    for (int f = 0; f < 6 && C::WFACE; ++f) {
+      bool gp, ss, sc;
+      if (!face_on(f, gp, ss, sc)) continue;
+      gmk |= (uint32_t)gp << f;
+      smk |= (uint32_t)ss << f;
+    }
+    if (gmk | smk) {
+      double *WS = PS;  // [3][SZ] (the point rows are consumed)
+      for (int it = tid; it < 3 * NN; it += TH) {
+        const int D = it / NN, t = it - D * NN;
+        int b0, st;
+        B::line(D, t, b0, st);
+        double uo[N], w[N];
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          uo[m] = U[b0 + m * st];
+          w[m] = 0.0;
+        }
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd) {
+          const int f = 2 * D + sd;
+          const bool g = (gmk >> f) & 1u, sp = (smk >> f) & 1u;
+          if (!(g || sp)) continue;
+          const double *NBf = NBs + f * SZ;
+          double uu[N], un[N], out[N];
+#pragma unroll
+          for (int m = 0; m < N; ++m) {
+            const int pm = sd ? N - 1 - m : m;
+            uu[m] = uo[pm];
+            un[m] = NBf[b0 + pm * st];
+            out[m] = 0.0;
+          }
+          if (g) {
+#pragma unroll
+            for (int m = 0; m < N; ++m) {
+              double x = 0.0;
+#pragma unroll
+              for (int a = 0; a < N; ++a) x = fma(tt.Goo[m * N + a], uu[a], fma(tt.Gon[m * N + a], un[a], x));
+              out[m] = x;
+            }
+          }
+          if (sp) {
+            double A0 = 0.0, A1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < N; ++m) {
+              A0 = fma(tt.d0[m], uu[m], A0);
+              A1 = fma(-tt.d0[N - 1 - m], un[m], A1);
+            }
+            const double J = uu[0] - un[N - 1], A = A0 + A1;
+#pragma unroll
+            for (int m = 0; m < N; ++m) out[m] = fma(tt.cJ[m], J, fma(tt.cA[m], A, out[m]));
+          }
+#pragma unroll
+          for (int m = 0; m < N; ++m) w[sd ? N - 1 - m : m] += out[m];
+        }
+#pragma unroll
+        for (int m = 0; m < N; ++m) WS[D * SZ + b0 + m * st] = w[m];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int D = 0; D < 3; ++D) {
+        for (int t = tid; t < NN; t += TH) {
+          int b0, st;
+          B::line(D, t, b0, st);
+          double x[N];
+#pragma unroll
+          for (int m = 0; m < N; ++m) {
+            const int l = b0 + m * st;
+            x[m] = D == 0 ? (WS[l] + WS[SZ + l]) + WS[2 * SZ + l] : WS[l];
+          }
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            double y = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) y = fma(tt.M[csym<N>(i * N + j)], x[j], y);
+            if (D < 2) WS[b0 + i * st] = y;
+            else Rb[b0 + i * st] += y;
+          }
+        }
+        __syncthreads();
+      }
+    }
   }
   for (int f = 0; f < 6; ++f) {
     bool gp, ss, sc;
     if (!face_on(f, gp, ss, sc)) continue;
+    if (C::WFACE && !sc) continue;  // structured parts done above
     double *NB = C::PREF ? NBs + f * SZ : NBs;
     if constexpr (!C::PREF) {
       const double *nbp = u + (size_t)dsc.nb[f] * N3;
@@ -911,7 +1032,7 @@ __global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, doubl
     const double *dnb = side ? R.d0 : R.d1;
     const double *Goo = ft.Goo[side ? 0 : 1];
     const double *Gon = ft.Gon[side ? 0 : 1];
-    const bool structured = gp || ss;
+    const bool structured = !C::WFACE && (gp || ss);
     for (int t = tid; t < NN; t += TH) {
       int b0, st;
       B::line(dd, t, b0, st);

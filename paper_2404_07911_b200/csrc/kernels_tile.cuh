@@ -64,29 +64,7 @@ struct __align__(16) TileRec {
   int32_t blk[SMAX];
 };
 
-// Per-handle line operators (h, penalties folded), all warp-uniform.  Only the
-// lo-face (s = 0) variants are stored: every 1-D operator here is
-// centro-symmetric (GLL nodes and Gauss points are symmetric about 1/2), so the
-// hi face uses the reversed entries:  l'_a(1) = -l'_{n-1-a}(0),
-// cJ_hi[m] = cJ_lo[n-1-m], cA_hi[m] = -cA_lo[n-1-m], G_hi[m][a] = G_lo[n-1-m][n-1-a],
-// and L, M satisfy X[i][j] = X[n-1-i][n-1-j].  Reading only the canonical half
-// keeps ~20 distinct constants live next to the 64-double accumulator.
-template <int N>
-struct TileTab {
-  double L[N * N];    // M^{-1} h K1: volume term along one axis
-  double M[N * N];    // GLL mass M1
-  double d0[N];       // l'_a(0)
-  double cJ[N];       // SIPG (lo face): w_line += cJ [u] + cA (d u_own + d u_nb)
-  double cA[N];
-  double Goo[N * N];  // ghost penalty (lo face), own line:        M^{-1} G_oo
-  double Gon[N * N];  // ghost penalty (lo face), neighbour line: -M^{-1} G_on
-};
-
-// canonical index of a centro-symmetric n x n matrix entry
-template <int N>
-__device__ __forceinline__ constexpr int csym(int k) {
-  return k < N * N - 1 - k ? k : N * N - 1 - k;
-}
+// TileTab<N> (the per-handle line operators) and csym live in kernels.cuh.
 
 // position m along axis D of line t (t = t0 + N t1 over the two other axes, ascending)
 template <int N, int D>
