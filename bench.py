@@ -261,7 +261,7 @@ def run_ours(args, P, cfg, rank, world, local_rank):
         kname = {"structured": (f"k_tile2<{n_},0>" if n_ == 4 else f"k_tile<{n_},0>") + f" + k_gpw<{n_}>",
                  "unstructured": f"k_cutp<{n_}>"}
     else:
-        kname = {"structured": f"k_uncut{'3' if n_ == 5 else ''}<{n_}>", "unstructured": f"k_cut<{n_}>"}
+        kname = {"structured": f"k_uncw<{n_}>" if n_ in (5, 6) else f"k_uncut<{n_}>", "unstructured": f"k_cut<{n_}>"}
     dom = max(k_ms, key=k_ms.get)
     F_dom = work["F_uncut"] if dom == "structured" else work["F_cut"]
     B_dom = work["B_uncut"] if dom == "structured" else work["B_cut"]
