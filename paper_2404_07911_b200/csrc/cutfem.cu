@@ -87,6 +87,7 @@ struct cutfem_handle {
   int *d_kstart = nullptr;      // per part: warp -> first packet
   CPacket *d_chunks = nullptr;  // packets of the point-chunk stream, per warp in consumption order
   bool uncw_first = false;      // n = 5, 6: k_uncw launched before k_cut
+  bool gpw_cut = false;         // p <= 3: the cut cells' structured faces in k_gpw (after k_cutp)
   int uncw_ctas = 0;            // n = 5, 6: k_uncw CTAs per SM (0: occupancy)
   char *d_stream = nullptr;     // the packed stream (chunk headers + point rows)
   int64_t w_off[3] = {0};
@@ -421,7 +422,9 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       c.gp = d.flags & nbm & 0x3fu;
       c.sipg = (d.flags >> 6) & nbm & 0x3fu;  // structured (full, uncut) faces of the cut cell
       c.vol = false;
-      (void)c;  // cut cells: their structured faces are done inside k_cutp
+      // cut cells: their structured faces go to k_gpw (after k_cutp) when gpw_cut,
+      // else k_cutp does them
+      if (hd->gpw_cut && (c.gp | c.sipg)) set[1][pt - 1].push_back(c);
     }
   }
   // set 0: k_tile* tiles (TileCfg<N>); set 1: k_gpw tiles (smaller, GpwCfg<N>::T).
@@ -466,7 +469,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       e.fb = (int64_t)fac.size() / 4;
       for (int f = 0; f < 6; ++f) {
         e.nb[f] = d.nb[f] >= 0 ? d.nb[f] : -1;
-        if (d.nb[f] >= 0) {
+        if (d.nb[f] >= 0 && !hd->gpw_cut) {
           if (d.flags & (1u << f)) e.smask |= 1u << f;               // ghost penalty (the cell is cut)
           if (d.flags & (1u << (6 + f))) e.smask |= 1u << (8 + f);   // full face inside Omega: SIPG
         }
@@ -727,6 +730,13 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
       k_tile<NT, 0><<<grid, 32, C::SMEM, st>>>(u, v, t0, (int)n0, tt, hd->kp.mask);
     CU(cudaGetLastError());
   }
+  bool joined = false;
+  if (n1 > 0 && hd->gpw_cut && fork && !cut_last) {
+    // k_gpw adds to cut-cell blocks too: wait for k_cutp's v = ...
+    CU(cudaEventRecord(hd->ev_join, hd->side));
+    CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
+    joined = true;
+  }
   if (n1 > 0) {  // uncut cells next to cut cells: + ghost penalty (needs only k_tile*<0>)
     const unsigned grid = (unsigned)(hd->persist & 2 ? std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count) : n1);
     k_gpw<NT><<<grid, GpwCfg<NT>::THREADS, GpwCfg<NT>::SMEM, st>>>(
@@ -734,7 +744,7 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
     CU(cudaGetLastError());
   }
   if (cut_last && (rc = launch_cut())) return rc;
-  if (fork) {
+  if (fork && !joined) {
     CU(cudaEventRecord(hd->ev_join, hd->side));
     CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
   }
@@ -1183,6 +1193,8 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   if ((rc = upload(hd, &hd->d_sfptr, pb->sf_ptr, (size_t)(nsf ? nsf + 1 : 0)))) return rc;
   hd->cut_last = std::getenv("CUTFEM_CUT_LAST") != nullptr;
   hd->uncw_first = std::getenv("CUTFEM_UNCW_FIRST") != nullptr;
+  hd->gpw_cut = std::getenv("CUTFEM_GPW_CUT") != nullptr;
+  if (hd->gpw_cut) hd->cut_last = false;  // k_gpw must follow k_cutp
   if (const char *e = std::getenv("CUTFEM_UNCW_CTAS")) hd->uncw_ctas = std::atoi(e);
   if (const char *e = std::getenv("CUTFEM_TILE_PERSIST")) hd->persist = std::atoi(e);
   else hd->persist = 3;
