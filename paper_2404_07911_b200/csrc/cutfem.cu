@@ -88,6 +88,7 @@ struct cutfem_handle {
   CPacket *d_chunks = nullptr;  // packets of the point-chunk stream, per warp in consumption order
   bool uncw_first = false;      // n = 5, 6: k_uncw launched before k_cut
   bool gpw_cut = false;         // p <= 3: the cut cells' structured faces in k_gpw (after k_cutp)
+  bool cellk = true;            // p = 1, 2: uncut cells through k_cell (env CUTFEM_NO_CELLK: k_tile + k_gpw)
   int uncw_ctas = 0;            // n = 5, 6: k_uncw CTAs per SM (0: occupancy)
   char *d_stream = nullptr;     // the packed stream (chunk headers + point rows)
   int64_t w_off[3] = {0};
@@ -721,6 +722,22 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
   if (!cut_last && (rc = launch_cut())) return rc;
   const TileTab<NT> &tt = *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data());
   const char *tb = reinterpret_cast<const char *>(hd->d_tiles);  // byte offsets per set
+  if constexpr (NT <= 3) if (hd->cellk && (which & 1)) {
+    // p = 1, 2: one thread per uncut cell (plain cells, then the cells next to cut cells)
+    const int64_t np = hd->r_cnt[part][0], ng = hd->r_cnt[part][1];
+    if (np + ng > 0) {
+      k_cell<NT><<<(unsigned)((np + ng + 127) / 128), 128, 0, st>>>(
+          u, v, hd->d_udesc + hd->r_off[part][0], (int)np, hd->d_udesc + hd->r_off[part][1], (int)ng, tt,
+          hd->kp.mask);
+      CU(cudaGetLastError());
+    }
+    if (cut_last && (rc = launch_cut())) return rc;
+    if (fork) {
+      CU(cudaEventRecord(hd->ev_join, hd->side));
+      CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
+    }
+    return 0;
+  }
   if (n0 > 0) {
     const unsigned grid = (unsigned)(hd->persist & 1 ? std::min<int64_t>(n0, (int64_t)hd->occ_tile[0] * hd->sm_count) : n0);
     const auto *t0 = reinterpret_cast<const TileRec<C::SMAX> *>(tb + hd->t_off[0][part]);
@@ -1194,6 +1211,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   hd->cut_last = std::getenv("CUTFEM_CUT_LAST") != nullptr;
   hd->uncw_first = std::getenv("CUTFEM_UNCW_FIRST") != nullptr;
   hd->gpw_cut = std::getenv("CUTFEM_GPW_CUT") != nullptr;
+  hd->cellk = std::getenv("CUTFEM_NO_CELLK") == nullptr && !hd->gpw_cut;
   if (hd->gpw_cut) hd->cut_last = false;  // k_gpw must follow k_cutp
   if (const char *e = std::getenv("CUTFEM_UNCW_CTAS")) hd->uncw_ctas = std::atoi(e);
   if (const char *e = std::getenv("CUTFEM_TILE_PERSIST")) hd->persist = std::atoi(e);

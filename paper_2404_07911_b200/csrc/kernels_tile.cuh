@@ -1038,3 +1038,160 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
     }
   }
 }
+
+// ===================================================================== k_cell
+// k_cell<N> (N = 2, 3): every structured term of the uncut cells (volume, SIPG on
+// all faces, ghost penalty on the faces to cut cells), v = result.  At these
+// degrees a block is 64 / 216 bytes: staging tiles with halos through TMA issues
+// many tiny copies and amplifies the reads ~4x, so here ONE THREAD owns one cell,
+// reads its block and each face neighbour's block straight from global memory
+// (neighbours are shared by nearby threads: L1/L2 hits), keeps u, w and the
+// neighbour block in registers and applies the same w-space operators as
+// k_tile / k_uncw (M^{-1}-premultiplied line operators, then M (x) M (x) M).
+// Cells: desc0[0, n0) then desc1[0, n1) (plain cells, cells next to cut cells).
+#ifndef CELL_G2
+#define CELL_G2 1  // measured: grouping the neighbour loads costs more occupancy than it hides
+#endif
+#ifndef CELL_G3
+#define CELL_G3 1
+#endif
+template <int N>
+__device__ __forceinline__ void load_block(const double *__restrict__ p, double (&x)[N * N * N]) {
+  constexpr int N3 = N * N * N;
+  if constexpr ((N3 % 2) == 0) {
+#pragma unroll
+    for (int k = 0; k < N3; k += 2) {
+      const double2 t = __ldg(reinterpret_cast<const double2 *>(p + k));
+      x[k] = t.x;
+      x[k + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < N3; ++k) x[k] = __ldg(p + k);
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) k_cell(const double *__restrict__ u, double *__restrict__ v,
+                                              const UDesc *__restrict__ desc0, int n0,
+                                              const UDesc *__restrict__ desc1, int n1, TileTab<N> tt,
+                                              uint32_t mask) {
+  constexpr int NN = N * N, N3 = NN * N;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n0 + n1) return;
+  const UDesc d = i < n0 ? desc0[i] : desc1[i - n0];
+  const bool cell_on = (mask & TERM_CELL) != 0, sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
+  double uo[N3], w[N3];
+  load_block<N>(u + (size_t)d.blk * N3, uo);
+#pragma unroll
+  for (int l = 0; l < N3; ++l) w[l] = 0.0;
+  // volume: w += (M^{-1} h K1)_D along every axis
+  if (cell_on) {
+    static_for<0, 3>([&](auto dc) {
+      constexpr int D = decltype(dc)::value;
+#pragma unroll
+      for (int t = 0; t < NN; ++t)
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          double x = w[lix<N, D>(t, a)];
+#pragma unroll
+          for (int b = 0; b < N; ++b) x = fma(tt.L[csym<N>(a * N + b)], uo[lix<N, D>(t, b)], x);
+          w[lix<N, D>(t, a)] = x;
+        }
+    });
+  }
+  // faces: SIPG (every face with an active neighbour) and ghost penalty (faces to cut
+  // cells).  The neighbour blocks of a group of faces (all six at n = 2, the two of an
+  // axis at n = 3) are loaded together so their latencies overlap.
+  constexpr int G = N == 2 ? CELL_G2 : CELL_G3;  // 1, 2, 3 or 6
+  double nbv[G][N3];
+  auto face_need = [&](int F, bool &sp, bool &g) {
+    const int nbk = d.nb[F];
+    sp = sipg_on && nbk >= 0;
+    g = gp_on && nbk >= 0 && ((d.flags >> F) & 1u);
+    return sp || g;
+  };
+  auto load_group = [&](int F0) {
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      bool sp, g;
+      if (face_need(F0 + k, sp, g)) load_block<N>(u + (size_t)d.nb[F0 + k] * N3, nbv[k]);
+    }
+  };
+  static_for<0, 6>([&](auto fc) {
+    constexpr int F = decltype(fc)::value, D = F / 2, SS = F % 2;
+    if constexpr (F % G == 0) load_group(F);
+    bool sp, g;
+    if (!face_need(F, sp, g)) return;
+    const double(&un)[N3] = nbv[F % G];
+#pragma unroll
+    for (int t = 0; t < NN; ++t) {
+      double o[N], n_[N], out[N];
+#pragma unroll
+      for (int m = 0; m < N; ++m) {
+        o[m] = uo[lix<N, D>(t, m)];
+        n_[m] = un[lix<N, D>(t, m)];
+        out[m] = 0.0;
+      }
+      if (g) {
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          double x = 0.0;
+#pragma unroll
+          for (int a = 0; a < N; ++a) {
+            const int k = SS ? (N - 1 - m) * N + (N - 1 - a) : m * N + a;
+            x = fma(tt.Goo[k], o[a], fma(tt.Gon[k], n_[a], x));
+          }
+          out[m] = x;
+        }
+      }
+      if (sp) {
+        double A0 = 0.0, A1 = 0.0;
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          if (SS == 0) {
+            A0 = fma(tt.d0[m], o[m], A0);
+            A1 = fma(-tt.d0[N - 1 - m], n_[m], A1);
+          } else {
+            A0 = fma(-tt.d0[N - 1 - m], o[m], A0);
+            A1 = fma(tt.d0[m], n_[m], A1);
+          }
+        }
+        const double J = SS ? (o[N - 1] - n_[0]) : (o[0] - n_[N - 1]);
+        const double A = A0 + A1;
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          if (SS == 0) out[m] = fma(tt.cJ[m], J, fma(tt.cA[m], A, out[m]));
+          else out[m] = fma(tt.cJ[N - 1 - m], J, fma(-tt.cA[N - 1 - m], A, out[m]));
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < N; ++m) w[lix<N, D>(t, m)] += out[m];
+    }
+  });
+  // v = (M (x) M (x) M) w
+  static_for<0, 3>([&](auto dc) {
+    constexpr int D = decltype(dc)::value;
+#pragma unroll
+    for (int t = 0; t < NN; ++t) {
+      double x[N];
+#pragma unroll
+      for (int m = 0; m < N; ++m) x[m] = w[lix<N, D>(t, m)];
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        double y = 0.0;
+#pragma unroll
+        for (int b = 0; b < N; ++b) y = fma(tt.M[csym<N>(a * N + b)], x[b], y);
+        w[lix<N, D>(t, a)] = y;
+      }
+    }
+  });
+  double *vb = v + (size_t)d.blk * N3;
+  if constexpr ((N3 % 2) == 0) {
+#pragma unroll
+    for (int k = 0; k < N3; k += 2) *reinterpret_cast<double2 *>(vb + k) = make_double2(w[k], w[k + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < N3; ++k) vb[k] = w[k];
+  }
+}
