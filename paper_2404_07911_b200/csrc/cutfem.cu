@@ -530,34 +530,51 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         for (int64_t i : lists[w]) {
           const CDesc2 &e = c2[i];
           c2o[pos++] = e;
-          // the chunks of this cell: [volume | interface] points in chunks of 32, then the
-          // cut-face points axis by axis (a chunk never mixes a face point with another
-          // kind or another face axis: the warp then runs one code path per chunk)
+          // the chunks of this cell.  n <= CUTP_UNIFIED_MAXN: every point kind in one stream;
+          // else [volume | interface] points in chunks of 32, then the cut-face points axis
+          // by axis (a chunk never mixes a face point with another kind or face axis: one
+          // code path per chunk, which pays at n = 4 where registers are tight)
           const int nv = (hd->mask & CUTFEM_TERM_CELL) ? e.nv : 0, ns = (hd->mask & CUTFEM_TERM_NITSCHE) ? e.ns : 0;
           const bool fon = (hd->mask & CUTFEM_TERM_SIPG) != 0;
           const size_t k0 = chunk.size();
-          for (int q0 = 0; q0 < nv + ns; q0 += 32) {
-            const int cv = std::max(0, std::min(32, nv - q0));
-            const int qs = std::max(0, q0 - nv), cs = std::max(0, std::min(32 - cv, ns - qs));
-            CChunk r;
-            r.vo = (int32_t)(e.vb + q0);
-            r.so = (int32_t)(e.sb + qs);
-            r.fo = (int32_t)e.fb;
-            r.cnt = cv | (cs << 8);
-            chunk.push_back(r);
-          }
-          int64_t fo = e.fb;
-          for (int ax = 0; ax < 3 && fon; ++ax) {
-            const int na = fax[i][ax];
-            for (int q0 = 0; q0 < na; q0 += 32) {
+          if constexpr (CutPCfg<N>::UNIFIED) {
+            // one stream: volume, interface, cut-face points (any axis) in chunks of 32
+            const int nf = fon ? e.nf : 0;
+            for (int q0 = 0; q0 < nv + ns + nf; q0 += 32) {
+              const int cv = std::max(0, std::min(32, nv - q0));
+              const int qs = std::max(0, q0 - nv), cs = std::max(0, std::min(32 - cv, ns - qs));
+              const int qf = std::max(0, q0 - nv - ns), cf = std::max(0, std::min(32 - cv - cs, nf - qf));
               CChunk r;
-              r.vo = (int32_t)e.vb;
-              r.so = (int32_t)e.sb;
-              r.fo = (int32_t)(fo + q0);
-              r.cnt = std::min(32, na - q0) << 16;
+              r.vo = (int32_t)(e.vb + std::min(q0, nv));
+              r.so = (int32_t)(e.sb + qs);
+              r.fo = (int32_t)(e.fb + qf);
+              r.cnt = cv | (cs << 8) | (cf << 16);
               chunk.push_back(r);
             }
-            fo += na;
+          } else {
+            for (int q0 = 0; q0 < nv + ns; q0 += 32) {
+              const int cv = std::max(0, std::min(32, nv - q0));
+              const int qs = std::max(0, q0 - nv), cs = std::max(0, std::min(32 - cv, ns - qs));
+              CChunk r;
+              r.vo = (int32_t)(e.vb + q0);
+              r.so = (int32_t)(e.sb + qs);
+              r.fo = (int32_t)e.fb;
+              r.cnt = cv | (cs << 8);
+              chunk.push_back(r);
+            }
+            int64_t fo = e.fb;
+            for (int ax = 0; ax < 3 && fon; ++ax) {
+              const int na = fax[i][ax];
+              for (int q0 = 0; q0 < na; q0 += 32) {
+                CChunk r;
+                r.vo = (int32_t)e.vb;
+                r.so = (int32_t)e.sb;
+                r.fo = (int32_t)(fo + q0);
+                r.cnt = std::min(32, na - q0) << 16;
+                chunk.push_back(r);
+              }
+              fo += na;
+            }
           }
           c2o[pos - 1].nchunk = (int32_t)(chunk.size() - k0);
         }

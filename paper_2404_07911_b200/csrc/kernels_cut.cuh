@@ -138,6 +138,12 @@ struct __align__(16) CPacket {
 #ifndef CUTP_NB
 #define CUTP_NB 3  // packet ring depth
 #endif
+#ifndef CUTP_UNIFIED_MAXN
+#define CUTP_UNIFIED_MAXN 3  // n <= this: a chunk mixes every point kind and face axis
+#endif
+#ifndef CUTP_BFLY_MAXACC
+#define CUTP_BFLY_MAXACC 32  // accumulators <= this: shuffle reduce-scatter instead of the transpose
+#endif
 #ifndef CUTP_RW
 #define CUTP_RW 16  // rows of the reduction transpose buffer
 #endif
@@ -212,6 +218,59 @@ __device__ __forceinline__ void face_point(double (&acc)[ACC], const RefTab &R, 
     }
 }
 
+// The same cut-face point update for a runtime face axis d (chunks mixing axes):
+// the rank-1 update acc[c][b][a] += X_a Y_b Z_c with the normal factor T on axis d
+// and the in-face bases on the others (selected, not branched).
+template <int N, int ACC>
+__device__ __forceinline__ void face_point_rt(double (&acc)[ACC], const RefTab &R, const double *JAB, double xi,
+                                              double eta, double zeta, double W, const KParams &kp) {
+  constexpr int NN = N * N;
+  const int d = (xi == 0.0 || xi == 1.0) ? 0 : ((eta == 0.0 || eta == 1.0) ? 1 : 2);
+  const double xd = d == 0 ? xi : (d == 1 ? eta : zeta);
+  const int sd = xd == 1.0 ? 1 : 0;
+  double ls[N], lt[N];
+  basis_v_sym<N>(R, d == 0 ? eta : xi, ls);
+  basis_v_sym<N>(R, d == 2 ? eta : zeta, lt);
+  const double *JA = JAB + (2 * d + sd) * 2 * NN, *JB = JA + NN;
+  double J = 0.0, A = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      r0 = fma(ls[i], JA[i + N * j], r0);
+      r1 = fma(ls[i], JB[i + N * j], r1);
+    }
+    J = fma(lt[j], r0, J);
+    A = fma(lt[j], r1, A);
+  }
+  const double sg = sd ? kp.i2h : -kp.i2h;
+  const double k1 = W * fma(kp.sigma, J, -sg * A), k2 = -W * sg * J;
+  double T[N];
+#pragma unroll
+  for (int m = 0; m < N; ++m) T[m] = k2 * (sd ? R.d1[m] : R.d0[m]);
+  if (sd) T[N - 1] += k1;
+  else T[0] += k1;
+  double X[N], Y[N], Z[N];
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    X[m] = d == 0 ? T[m] : ls[m];
+    Y[m] = d == 0 ? ls[m] : (d == 1 ? T[m] : lt[m]);
+    Z[m] = d == 2 ? T[m] : lt[m];
+  }
+#pragma unroll
+  for (int c = 0; c < N; ++c)
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      const double yz = Y[b] * Z[c];
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        double &r = acc[(c * N + b) * N + a];
+        r = fma(X[a], yz, r);
+      }
+    }
+}
+
 template <int N>
 struct CutPCfg {
   static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
@@ -220,6 +279,10 @@ struct CutPCfg {
   static constexpr int PK = CUTP_PK;  // packet capacity in bytes (>= the largest chunk, 16 + 32 * 64)
   static constexpr int NN = N * N, N3 = N * N * N, N3P = (N3 + 1) & ~1;
   static constexpr int ACC = N == 4 ? 64 : (N == 3 ? 32 : 8);  // padded n^3 (power of two)
+  // one chunk stream per cell mixing volume, interface and cut-face points (any face
+  // axis: runtime-axis face update); else chunks are kind- and axis-homogeneous
+  static constexpr bool UNIFIED = N <= CUTP_UNIFIED_MAXN;
+  static constexpr bool BFLY = ACC <= CUTP_BFLY_MAXACC;
   // bars(2 + NB) | UB[2][7][N3P] | JAB[6][2][NN] | ring[NB][2 + PK/8] (nch + packet)
   static constexpr int OFF_UB = (2 + NB + 1) & ~1;
   static constexpr int OFF_JAB = OFF_UB + 2 * 7 * N3P;
@@ -534,10 +597,14 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
         }
       } else if (kind == 2) {
         // cut-face point: the face is the coordinate that is exactly 0 or 1
-        const int d = (xi == 0.0 || xi == 1.0) ? 0 : ((eta == 0.0 || eta == 1.0) ? 1 : 2);
-        if (d == 0) face_point<N, 0>(acc, R, JAB, xi, eta, zeta, W, kp);
-        else if (d == 1) face_point<N, 1>(acc, R, JAB, xi, eta, zeta, W, kp);
-        else face_point<N, 2>(acc, R, JAB, xi, eta, zeta, W, kp);
+        if constexpr (C::UNIFIED) {
+          face_point_rt<N>(acc, R, JAB, xi, eta, zeta, W, kp);
+        } else {
+          const int d = (xi == 0.0 || xi == 1.0) ? 0 : ((eta == 0.0 || eta == 1.0) ? 1 : 2);
+          if (d == 0) face_point<N, 0>(acc, R, JAB, xi, eta, zeta, W, kp);
+          else if (d == 1) face_point<N, 1>(acc, R, JAB, xi, eta, zeta, W, kp);
+          else face_point<N, 2>(acc, R, JAB, xi, eta, zeta, W, kp);
+        }
       }
       __syncwarp();  // every lane is done with the ring slot before it is refilled
       if (lane == 0 && left == 0) fence_proxy_async();
@@ -549,8 +616,19 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     double *vb = v + (size_t)cd.blk * N3;
     const bool st_on = (gm | sm) != 0;
     constexpr int RW = C::RW;
+    if constexpr (C::BFLY) {
+      // shuffle reduce-scatter (fixed order), then the writer lanes store
+      butterfly<C::ACC>(acc, lane);
+      if (BF<C::ACC>::writer(lane)) {
 #pragma unroll
-    for (int ps = 0; ps < C::ACC / RW; ++ps) {
+        for (int jj = 0; jj < BF<C::ACC>::LF; ++jj) {
+          const int l = BF<C::ACC>::idx(lane, jj);
+          if (l < N3) vb[l] = acc[jj] + (st_on ? WS[l] : 0.0);
+        }
+      }
+    }
+#pragma unroll
+    for (int ps = 0; ps < (C::BFLY ? 0 : C::ACC / RW); ++ps) {
 #pragma unroll
       for (int i = 0; i < RW; ++i) RED[i * 33 + lane] = acc[ps * RW + i];
       __syncwarp();
