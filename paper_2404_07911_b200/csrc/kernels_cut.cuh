@@ -291,7 +291,7 @@ struct CutPCfg {
   static constexpr int OFF_WS = OFF_RING + NB * RSLOT;  // w of the structured faces (n^3)
   static constexpr int OFF_RED = OFF_WS + ((N3 + 1) & ~1);  // reduction transpose [RW][33]
   static constexpr int RW = ACC < CUTP_RW ? ACC : CUTP_RW;      // accumulators per reduction pass
-  static constexpr int WSLOT = OFF_RED + RW * 33;
+  static constexpr int WSLOT = OFF_RED + (BFLY ? 0 : RW * 33);
   static constexpr int SMEM = WARPS * WSLOT * 8;
 };
 
