@@ -518,8 +518,20 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef CUT_PREF_MAXN
 #define CUT_PREF_MAXN 7
 #endif
+// CTAs per SM the register allocation of k_cut<n> must allow (ptxas's own choice
+// without a bound gave these at n = 5..9; an explicit 1 lets it take up to 255
+// registers and was measured 15 % slower at n = 5, 7)
+#ifndef CUT_MINB5
+#define CUT_MINB5 4
+#endif
+#ifndef CUT_MINB6
+#define CUT_MINB6 3
+#endif
+#ifndef CUT_MINB7
+#define CUT_MINB7 3
+#endif
 #ifndef CUT_WFACE_MASK
-#define CUT_WFACE_MASK 0x40
+#define CUT_WFACE_MASK 0xe0
 #endif
 #ifndef CUT_PPF_MASK
 #define CUT_PPF_MASK 0x300  // bit n: prefetch the point rows (n = 8, 9: measured faster; 6, 7 slower)
@@ -539,6 +551,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <int N>
 struct CutCfg {
   static constexpr int THREADS = 128;
+  static constexpr int MINB = N <= 4 ? 1 : (N == 5 ? CUT_MINB5 : (N == 6 ? CUT_MINB6 : (N == 7 ? CUT_MINB7 : 2)));
   static constexpr int NN = N * N, N3 = N * N * N;
   static constexpr int ROW0 = 2 * NN + 2 * N;
   static constexpr int ROW = (ROW0 % 2 == 0) ? ROW0 + 1 : ROW0;  // odd stride: no bank conflicts
@@ -559,7 +572,7 @@ struct CutCfg {
   static constexpr bool PREF = N <= CUT_PREF_MAXN;
   static constexpr int NBN = PREF ? 6 : 1;
   // structured faces in w-space (one parallel pass + one M (x) M (x) M sweep) instead
-  // of face by face; needs the prefetched neighbours (measured faster at n = 6 only)
+  // of face by face; needs the prefetched neighbours (measured faster at n = 5, 6, 7)
   static constexpr bool WFACE = PREF && ((CUT_WFACE_MASK >> N) & 1);
   // U, T, R, NB[NBN] (padded blocks) + JA, JB, FC1, FC2 (NN each) + point rows
   // point rows of the next chunk prefetched (cp.async, double buffer of 8 doubles a
@@ -844,7 +857,7 @@ __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int
 }
 
 template <int N>
-__global__ void __launch_bounds__(128) k_cut(const double *__restrict__ u, double *__restrict__ v,
+__global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__restrict__ u, double *__restrict__ v,
                                              const CDesc *__restrict__ desc, int ncut,
                                              const double *__restrict__ vol_pts,
                                              const int64_t *__restrict__ vol_ptr,
