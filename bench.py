@@ -320,6 +320,7 @@ def run_ours(args, P, cfg, rank, world, local_rank):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step,
             "ms_per_step_stats": {"min": float(ms.min()), "median": float(np.median(ms)), "max": float(ms.max()),
+                                  "iqr": [float(np.percentile(ms, 25)), float(np.percentile(ms, 75))],
                                   "argmax": int(np.argmax(ms)), "n_above_1.2x_median": int((ms > 1.2 * np.median(ms)).sum())},
             "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
