@@ -90,6 +90,7 @@ struct cutfem_handle {
   bool gpw_cut = false;         // p <= 3: the cut cells' structured faces in k_gpw (after k_cutp)
   bool cellk = true;            // p = 1, 2: uncut cells through k_cell (env CUTFEM_NO_CELLK: k_tile + k_gpw)
   int uncw_ctas = 0;            // n = 5, 6: k_uncw CTAs per SM (0: occupancy)
+  int uncw_hi = 1 << 8;         // bit n (7..9): uncut cells through k_uncw (env CUTFEM_UNCW_HI=mask)
   char *d_stream = nullptr;     // the packed stream (chunk headers + point rows)
   int64_t w_off[3] = {0};
   int grid_cutp[3] = {0};
@@ -700,6 +701,11 @@ int dispatch_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vecto
     case 4: return setup_tiles<4>(hd, pb, ud, cd);
     case 5: return setup_uncw<5>(hd, pb, ud);
     case 6: return setup_uncw<6>(hd, pb, ud);
+    // n = 7..9: k_uncw where measured faster than k_uncut (bit n of uncw_hi; default n = 8:
+    // n = 7 neutral, n = 9 slower — 140 KB of tile data, one CTA per SM)
+    case 7: return (hd->uncw_hi >> 7) & 1 ? setup_uncw<7>(hd, pb, ud) : 0;
+    case 8: return (hd->uncw_hi >> 8) & 1 ? setup_uncw<8>(hd, pb, ud) : 0;
+    case 9: return (hd->uncw_hi >> 9) & 1 ? setup_uncw<9>(hd, pb, ud) : 0;
   }
   return 0;
 }
@@ -801,8 +807,8 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
   // n = 5, 6: the persistent uncut kernel (k_uncw) may go first with a capped grid,
   // leaving room on every SM for the cut-cell CTAs (env CUTFEM_UNCW_FIRST, CUTFEM_UNCW_CTAS)
   auto launch_uncw = [&]() -> int {
-    if (!(nu > 0 && (N == 5 || N == 6) && hd->d_tiles)) return 0;
-    constexpr int NU = (N == 5 || N == 6) ? N : 5;
+    if (!(nu > 0 && N >= 5 && hd->d_tiles)) return 0;
+    constexpr int NU = N >= 5 ? N : 5;
     const int64_t nt = hd->t_cnt[0][part];
     if (nt > 0) {
       const int occ = hd->uncw_ctas > 0 ? std::min(hd->uncw_ctas, hd->occ_tile[0]) : hd->occ_tile[0];
@@ -833,7 +839,7 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
     }
     CU(cudaGetLastError());
   }
-  if (nu > 0 && (N == 5 || N == 6) && hd->d_tiles) {
+  if (nu > 0 && N >= 5 && hd->d_tiles) {
     if (!hd->uncw_first) launch_uncw();
   } else if (nu > 0) {
     if (N <= 5) {
@@ -1231,6 +1237,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   hd->cellk = std::getenv("CUTFEM_NO_CELLK") == nullptr && !hd->gpw_cut;
   if (hd->gpw_cut) hd->cut_last = false;  // k_gpw must follow k_cutp
   if (const char *e = std::getenv("CUTFEM_UNCW_CTAS")) hd->uncw_ctas = std::atoi(e);
+  if (const char *e = std::getenv("CUTFEM_UNCW_HI")) hd->uncw_hi = (int)std::strtol(e, nullptr, 0);
   if (const char *e = std::getenv("CUTFEM_TILE_PERSIST")) hd->persist = std::atoi(e);
   else hd->persist = 3;
   if (!std::getenv("CUTFEM_NO_TILE") && (rc = dispatch_tiles(hd, pb, ud, cd))) return rc;

@@ -46,13 +46,14 @@ struct TileCfgX {
   // slot stride (doubles): consecutive slots on different banks for 8- / 16-byte reads
   static constexpr int ST = N == 2 ? 10 : (N == 3 ? 27 : (N == 4 ? 66 : (BULK ? N3 + 2 : N3)));
   static constexpr int TC = TCELLS;  // cells per tile
-  // slots per tile: the brick + its face halo (2x4x4: 32 + 64, 2x2x4: 16 + 40, 2x2x2: 8 + 24)
-  static constexpr int SMAX = TC == 32 ? (N <= 3 ? 128 : 100) : (TC == 16 ? 60 : 36);
+  // slots per tile: the brick + its face halo (2x4x4: 32 + 64, 2x2x4: 16 + 40,
+  // 2x2x2: 8 + 24, 1x2x2: 4 + 16)
+  static constexpr int SMAX = TC == 32 ? (N <= 3 ? 128 : 100) : (TC == 16 ? 60 : (TC == 8 ? 36 : 20));
   static constexpr int SMEM = 16 + SMAX * ST * 8;
-  static constexpr int BX = 2, BY = TC == 32 ? 4 : 2, BZ = TC == 8 ? 2 : 4;
+  static constexpr int BX = TC == 4 ? 1 : 2, BY = TC == 32 ? 4 : 2, BZ = (TC == 8 || TC == 4) ? 2 : 4;
 };
 template <int N>
-struct TileCfg : TileCfgX<N, (N <= 4 ? 32 : (N == 5 ? 16 : 8))> {};
+struct TileCfg : TileCfgX<N, (N <= 4 ? 32 : (N == 5 ? 16 : (N == 6 ? 8 : 4)))> {};
 
 // One warp-tile.  lane_nb[l] = {slot of faces 0..3 (bytes), slot of faces 4,5
 // (bytes 0,1) | ghost-penalty face bits << 16}; slot 255 = no neighbour.  Lane l
@@ -867,7 +868,7 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
 
 
 // ===================================================================== k_uncw
-// k_uncw<N> (N = 5, 6): uncut cells at high degree, every structured term (volume,
+// k_uncw<N> (N = 5..9): uncut cells at high degree, every structured term (volume,
 // SIPG on all faces, ghost penalty on faces to cut cells), v = result.  The same
 // w-space arithmetic as k_tile2, organised like k_gpw (runtime line loops, w in
 // shared memory, small code): TPC threads per cell take every TPC-th line; the
