@@ -34,7 +34,7 @@ def test_single_slab_equals_plain(cf, cutgen_mod, p):
     assert torch.equal(v0, v1)
 
 
-@pytest.mark.parametrize("p,nparts", [(2, 2), (3, 3), (1, 4)])
+@pytest.mark.parametrize("p,nparts", [(2, 2), (3, 3), (1, 4), (5, 2), (7, 2)])
 def test_slabs_with_emulated_halo(cf, cutgen_mod, p, nparts):
     P = cutgen_mod.generate(cutgen_mod.SPHERE, 12, -1.0, 1.0, p)
     nd = (p + 1) ** 3
