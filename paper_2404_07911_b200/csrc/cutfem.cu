@@ -91,6 +91,7 @@ struct cutfem_handle {
   bool cellk = true;            // p = 1, 2: uncut cells through k_cell (env CUTFEM_NO_CELLK: k_tile + k_gpw)
   int uncw_ctas = 0;            // n = 5, 6: k_uncw CTAs per SM (0: occupancy)
   int uncw_hi = 1 << 8;         // bit n (7..9): uncut cells through k_uncw (env CUTFEM_UNCW_HI=mask)
+  bool vlines = true;           // k_cutp: volume points in lines where they form lines (env CUTFEM_NO_VLINES)
   char *d_stream = nullptr;     // the packed stream (chunk headers + point rows)
   int64_t w_off[3] = {0};
   int grid_cutp[3] = {0};
@@ -384,6 +385,30 @@ void build_tiles(const std::vector<TCell> &cells, const cutfem_problem *pb, std:
   if (!tiles.empty()) std::memcpy(out.data(), tiles.data(), out.size());
 }
 
+// A cut cell's volume points in LINES: consecutive groups of n points that share
+// two reference coordinates exactly (dimension-reduction quadrature), all along one
+// axis.  Returns the axis (0..2) or -1 (the cell then streams single points).
+static int vol_line_axis(const double *vp, int64_t nv, int n) {
+  if (nv <= 0 || nv % n != 0 || n < 2) return -1;
+  int ax = -1;
+  for (int64_t g = 0; g < nv; g += n) {
+    const double *a = vp + 4 * g;
+    for (int t = 1; t < n; ++t) {
+      const double *b = vp + 4 * (g + t);
+      int diff = -1, nd = 0;
+      for (int d = 0; d < 3; ++d)
+        if (a[d] != b[d]) {
+          diff = d;
+          ++nd;
+        }
+      if (nd != 1) return -1;
+      if (ax < 0) ax = diff;
+      if (diff != ax) return -1;
+    }
+  }
+  return ax;
+}
+
 template <int N>
 int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<UDesc> &ud,
                 const std::vector<CDesc> &cd) {
@@ -512,7 +537,18 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       hd->w_off[pt] = (int64_t)ws.size();
       const int W = grid * WP;
       std::vector<int64_t> idx(n);
-      auto cost = [&](const CDesc2 &e) { return (double)((e.nv + e.ns + e.nf + 31) / 32) + 1.5; };
+      // cost of a cell in point-chunk units: its chunks + a fixed per-cell part; volume
+      // points in lines cost ~2.8 point chunks per 32 lines (128 points) at n = 4
+      std::vector<char> isline(c2.size(), 0);
+      for (int64_t i = 0; i < n; ++i) {
+        const CDesc2 &e = c2[o + i];
+        isline[o + i] = hd->vlines && N >= 3 && e.nv > 0 && vol_line_axis(pb->vol_pts + 4 * e.vb, e.nv, N) >= 0;
+      }
+      auto cost = [&](const CDesc2 &e) {
+        const int64_t i = &e - c2.data();
+        if (isline[i]) return 2.8 * ((e.nv / N + 31) / 32) + (double)((e.ns + e.nf + 31) / 32) + 1.5;
+        return (double)((e.nv + e.ns + e.nf + 31) / 32) + 1.5;
+      };
       for (int64_t i = 0; i < n; ++i) idx[i] = o + i;
       std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return cost(c2[a]) > cost(c2[b]); });
       std::vector<std::vector<int64_t>> lists(W);
@@ -535,9 +571,27 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
           // else [volume | interface] points in chunks of 32, then the cut-face points axis
           // by axis (a chunk never mixes a face point with another kind or face axis: one
           // code path per chunk, which pays at n = 4 where registers are tight)
-          const int nv = (hd->mask & CUTFEM_TERM_CELL) ? e.nv : 0, ns = (hd->mask & CUTFEM_TERM_NITSCHE) ? e.ns : 0;
+          int nv = (hd->mask & CUTFEM_TERM_CELL) ? e.nv : 0;
+          const int ns = (hd->mask & CUTFEM_TERM_NITSCHE) ? e.ns : 0;
           const bool fon = (hd->mask & CUTFEM_TERM_SIPG) != 0;
           const size_t k0 = chunk.size();
+          // volume points in lines: chunks of <= 32 lines (sign bit, axis << 24), then the
+          // cell's other points as below with no volume points left
+          const int lax = (hd->vlines && N >= 3 && nv > 0) ? vol_line_axis(pb->vol_pts + 4 * e.vb, nv, N) : -1;
+          int nlc = 0;  // line chunks of the cell (packed into nchunk's high half)
+          if (lax >= 0) {
+            const int nl = nv / N;
+            for (int l0 = 0; l0 < nl; l0 += 32) {
+              CChunk r;
+              r.vo = (int32_t)(e.vb + (int64_t)l0 * N);
+              r.so = (int32_t)e.sb;
+              r.fo = (int32_t)e.fb;
+              r.cnt = (int32_t)(0x80000000u | ((uint32_t)lax << 24) | (uint32_t)std::min(32, nl - l0));
+              chunk.push_back(r);
+              ++nlc;
+            }
+            nv = 0;
+          }
           if constexpr (CutPCfg<N>::UNIFIED) {
             // one stream: volume, interface, cut-face points (any axis) in chunks of 32
             const int nf = fon ? e.nf : 0;
@@ -577,7 +631,8 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
               fo += na;
             }
           }
-          c2o[pos - 1].nchunk = (int32_t)(chunk.size() - k0);
+          if (chunk.size() - k0 > 0xffff) return fail(CUTFEM_EUNSUPPORTED, "k_cutp: > 65535 point chunks in a cell");
+          c2o[pos - 1].nchunk = (int32_t)((chunk.size() - k0) | ((size_t)nlc << 16));
         }
       }
       ws.push_back((int)(pos - o));
@@ -597,8 +652,9 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       CPacket cur = {(int64_t)strm.size() * 8, 0, 0};
       for (int k = ks[w]; k < ks[w + 1]; ++k) {
         const CChunk &r = chunk[k];
-        const int cv = r.cnt & 0xff, cs = (r.cnt >> 8) & 0xff, cf = (r.cnt >> 16) & 0xff;
-        const int bytes = 16 + 32 * cv + 64 * cs + 32 * cf;
+        const bool line = r.cnt < 0;
+        const int cv = r.cnt & 0xff, cs = line ? 0 : (r.cnt >> 8) & 0xff, cf = line ? 0 : (r.cnt >> 16) & 0xff;
+        const int bytes = line ? 16 + (16 + 16 * N) * cv : 16 + 32 * cv + 64 * cs + 32 * cf;
         if (cur.nch > 0 && cur.bytes + bytes > CutPCfg<N>::PK) {
           pk.push_back(cur);
           cur = {(int64_t)strm.size() * 8, 0, 0};
@@ -606,6 +662,22 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         double hdr[2] = {0.0, 0.0};
         std::memcpy(hdr, &r.cnt, sizeof(int32_t));
         strm.insert(strm.end(), hdr, hdr + 2);
+        if (line) {
+          // per line: the two base coordinates (ascending axes), then (coordinate, W) per point
+          const int ax = (r.cnt >> 24) & 3, b1 = ax == 0 ? 1 : 0, b2 = ax == 2 ? 1 : 2;
+          for (int l = 0; l < cv; ++l) {
+            const double *x = pb->vol_pts + 4 * ((size_t)r.vo + (size_t)l * N);
+            strm.push_back(x[b1]);
+            strm.push_back(x[b2]);
+            for (int t = 0; t < N; ++t) {
+              strm.push_back(x[4 * t + ax]);
+              strm.push_back(x[4 * t + 3]);
+            }
+          }
+          cur.bytes += bytes;
+          ++cur.nch;
+          continue;
+        }
         strm.insert(strm.end(), pb->vol_pts + 4 * (size_t)r.vo, pb->vol_pts + 4 * ((size_t)r.vo + cv));
         for (int q = 0; q < cs; ++q) {
           const double *x = pb->srf_pts + 7 * ((size_t)r.so + q);
@@ -1238,6 +1310,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   if (hd->gpw_cut) hd->cut_last = false;  // k_gpw must follow k_cutp
   if (const char *e = std::getenv("CUTFEM_UNCW_CTAS")) hd->uncw_ctas = std::atoi(e);
   if (const char *e = std::getenv("CUTFEM_UNCW_HI")) hd->uncw_hi = (int)std::strtol(e, nullptr, 0);
+  hd->vlines = std::getenv("CUTFEM_NO_VLINES") == nullptr;
   if (const char *e = std::getenv("CUTFEM_TILE_PERSIST")) hd->persist = std::atoi(e);
   else hd->persist = 3;
   if (!std::getenv("CUTFEM_NO_TILE") && (rc = dispatch_tiles(hd, pb, ud, cd))) return rc;

@@ -38,7 +38,8 @@ struct __align__(16) CDesc2 {
   int64_t vb, sb, fb;  // first volume / interface / cut-face point of the cell
   int32_t nv, ns, nf;
   uint32_t smask;    // bits 0-5: ghost-penalty faces, bits 8-13: full-face SIPG faces
-  int32_t nchunk;    // point chunks of the cell in the plan (a new chunk starts at the
+  int32_t nchunk;    // chunks of the cell in the plan, | (volume-line chunks, the first ones) << 16
+                     // (a new point chunk starts at the
                      // volume/interface -> face boundary and at every face-axis boundary)
 };
 
@@ -271,6 +272,87 @@ __device__ __forceinline__ void face_point_rt(double (&acc)[ACC], const RefTab &
     }
 }
 
+// Volume points that come in LINES (dimension-reduction quadrature: along
+// each line of the height axis AX the q = n Gauss points share the two base
+// coordinates).  The base-plane part of the contraction is then done once per
+// line instead of once per point (the paper's partial-sum reuse, P:874-878,
+// extended across the points of a line):
+//   P_i = sum_jk u(i,j,k) l1_j l2_k,  Q1_i = sum u l1'_j l2_k,  Q2_i = sum u l1_j l2'_k
+//   per point t: u, d_AX u, d_B1 u, d_B2 u from 4 n-term sums over i, and the test
+//   coefficients accumulated into R0_i = sum_t c_AX la'_i, R1_i = sum_t c_B1 la_i,
+//   R2_i = sum_t c_B2 la_i
+//   acc(i,j,k) += R0_i l1_j l2_k + R1_i l1'_j l2_k + R2_i l1_j l2'_k
+// (i along AX, j along the lower base axis B1, k along the upper B2).  Record:
+// [b1, b2, (t, W) x n].  About a third of the per-point FP64 work at n = 4.
+template <int N, int AX>
+__device__ __forceinline__ constexpr int lpos(int i, int j, int k) {
+  // i along AX, j along B1 < B2, k along B2 -> l = x + N y + N^2 z
+  return AX == 0 ? (i + N * j + N * N * k) : (AX == 1 ? (j + N * i + N * N * k) : (j + N * k + N * N * i));
+}
+template <int N, int AX, int ACC>
+__device__ __forceinline__ void vol_line(double (&acc)[ACC], const RefTab &R, const double *U, const double *rec,
+                                         double ih2) {
+  double v1[N], d1[N], v2[N], d2[N];
+  basis_vd_sym<N>(R, rec[0], v1, d1);
+  basis_vd_sym<N>(R, rec[1], v2, d2);
+  double Pp[N], Q1[N], Q2[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double p = 0.0, q1 = 0.0, q2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double uu = U[lpos<N, AX>(i, j, k)];
+        s0 = fma(v1[j], uu, s0);
+        s1 = fma(d1[j], uu, s1);
+      }
+      p = fma(v2[k], s0, p);
+      q1 = fma(v2[k], s1, q1);
+      q2 = fma(d2[k], s0, q2);
+    }
+    Pp[i] = p;
+    Q1[i] = q1;
+    Q2[i] = q2;
+  }
+  double R0[N], R1[N], R2[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) R0[i] = R1[i] = R2[i] = 0.0;
+#pragma unroll
+  for (int t = 0; t < N; ++t) {
+    const double2 tw = *reinterpret_cast<const double2 *>(rec + 2 + 2 * t);
+    double va[N], da[N];
+    basis_vd_sym<N>(R, tw.x, va, da);
+    double uA = 0.0, uB1 = 0.0, uB2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      uA = fma(da[i], Pp[i], uA);
+      uB1 = fma(va[i], Q1[i], uB1);
+      uB2 = fma(va[i], Q2[i], uB2);
+    }
+    const double sw = tw.y * ih2;
+    const double cA = sw * uA, cB1 = sw * uB1, cB2 = sw * uB2;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R0[i] = fma(cA, da[i], R0[i]);
+      R1[i] = fma(cB1, va[i], R1[i]);
+      R2[i] = fma(cB2, va[i], R2[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const double T0 = fma(R0[i], v2[k], R2[i] * d2[k]), T1 = R1[i] * v2[k];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double &r = acc[lpos<N, AX>(i, j, k)];
+        r = fma(v1[j], T0, fma(d1[j], T1, r));
+      }
+    }
+}
+
 template <int N>
 struct CutPCfg {
   static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
@@ -386,7 +468,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     if (has_next) nd = desc[c + 1];
     int nv, ns, nf;
     counts(cd, nv, ns, nf);
-    const int K = cd.nchunk;
+    const int K = cd.nchunk & 0xffff, KL = cd.nchunk >> 16;  // chunks; the first KL are volume lines
     const uint32_t fm = fmask_of(cd);
     // ---- this cell's blocks
     if constexpr (C::BULK) {
@@ -515,24 +597,43 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     double acc[C::ACC];
 #pragma unroll
     for (int i = 0; i < C::ACC; ++i) acc[i] = 0.0;
-    for (int k = 0; k < K; ++k) {
-      if (left == 0) {  // next packet: wait for it, refill the slot of the previous one
-        ++pj;
-        const int b = (pj - p0w) % NB;
-        mbar_wait(bar + 2 + b, ((pj - p0w) / NB) & 1);
-        if (lane == 0) {
-          issue_packet(pj + NB - 1, rn);
-          if (pj + NB < p1w) rn = packets[pj + NB];
-        }
-        S = RING + b * C::RSLOT;
-        left = reinterpret_cast<const int *>(S)[0];
-        pos = 2;
+    auto next_packet = [&]() {  // wait for the next packet, refill the slot of the previous one
+      ++pj;
+      const int b = (pj - p0w) % NB;
+      mbar_wait(bar + 2 + b, ((pj - p0w) / NB) & 1);
+      if (lane == 0) {
+        issue_packet(pj + NB - 1, rn);
+        if (pj + NB < p1w) rn = packets[pj + NB];
       }
+      S = RING + b * C::RSLOT;
+      left = reinterpret_cast<const int *>(S)[0];
+      pos = 2;
+    };
+    // volume LINES first (their own loop: the point loop below keeps its code
+    // generation): chunks of cv lines along axis (cnt >> 24) & 3, records of 2 + 2N doubles
+    for (int k = 0; k < KL; ++k) {
+      if (left == 0) next_packet();
+      const int cnt = reinterpret_cast<const int *>(S + pos)[0];
+      const int cv = cnt & 0xff, ax = (cnt >> 24) & 3;
+      const double *P = S + pos + 2;
+      --left;
+      pos += 2 + (2 + 2 * N) * cv;
+      if (lane < cv) {
+        const double *rec = P + (2 + 2 * N) * lane;
+        if (ax == 0) vol_line<N, 0>(acc, R, U, rec, ih2);
+        else if (ax == 1) vol_line<N, 1>(acc, R, U, rec, ih2);
+        else vol_line<N, 2>(acc, R, U, rec, ih2);
+      }
+      __syncwarp();
+      if (lane == 0 && left == 0) fence_proxy_async();
+    }
+    for (int k = KL; k < K; ++k) {
+      if (left == 0) next_packet();
       const int cnt = reinterpret_cast<const int *>(S + pos)[0];
       const int cv = cnt & 0xff, cs = (cnt >> 8) & 0xff, cf = (cnt >> 16) & 0xff;
       const double *P = S + pos + 2;  // the chunk's rows
-      pos += 2 + 4 * cv + 8 * cs + 4 * cf;
       --left;
+      pos += 2 + 4 * cv + 8 * cs + 4 * cf;
       // kind: 0 volume, 1 interface, 2 cut face, 3 idle lane
       const int kind = lane < cv ? 0 : (lane < cv + cs ? 1 : (lane < cv + cs + cf ? 2 : 3));
       double xi = 0.5, eta = 0.5, zeta = 0.5, W = 0.0, nx = 0.0, ny = 0.0, nz = 0.0;
