@@ -1224,6 +1224,11 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
           cost += (pb->sf_ptr[s + 1] - pb->sf_ptr[s]) / 2;
         }
       }
+      // k_cut (n >= 5): volume points in lines -> flag bit 26, axis in bits 24-25
+      if (n >= 5 && !std::getenv("CUTFEM_NO_VLINES")) {
+        const int lax = vol_line_axis(pb->vol_pts + 4 * c.vb, c.nv, n);
+        if (lax >= 0) c.flags |= (1u << 26) | ((uint32_t)lax << 24);
+      }
       cd.push_back(c);
       ccost.push_back(cost + (bnd ? (int64_t)1 << 40 : 0));  // boundary cells sort last (key), heavy first
       cbnd.push_back(bnd ? 1 : 0);

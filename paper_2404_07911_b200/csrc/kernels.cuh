@@ -530,6 +530,10 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef CUT_MINB7
 #define CUT_MINB7 3
 #endif
+#ifndef CUT_LB_UNROLL
+#define CUT_LB_UNROLL 0  // unroll factor of the line base contraction's outer loop (0: per degree,
+                         // full up to n = 7, none above: measured)
+#endif
 #ifndef CUT_WFACE_MASK
 #define CUT_WFACE_MASK 0xe0
 #endif
@@ -856,6 +860,204 @@ __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int
   }
 }
 
+// Volume points in LINES (dimension-reduction quadrature: the n Gauss points of a
+// line of the height axis ax share the two base coordinates; the cell's points are
+// stored line by line).  Per line (one thread): the base-plane contraction
+//   P_i = sum_jk u l1_j l2_k,  Q1_i = sum u l1'_j l2_k,  Q2_i = sum u l1_j l2'_k
+// once, then per point only n-term sums for u, grad u and the test coefficients
+//   R0_i += c_ax la'_i,  R1_i += c_B1 la_i,  R2_i += c_B2 la_i
+// (i along ax, j along B1 < B2, k along B2; the paper's partial-sum reuse, P:874-878,
+// extended across the points of a line).  The line's contribution
+//   R0_i l1_j l2_k + R1_i l1'_j l2_k + R2_i l1_j l2'_k
+// is written as rows in the x-stage form  X0[a] S0[bc] + X1[a] S1[bc] (+ X2[a] S2[bc]
+// when the lines run along x), so the row-blocked integration runs once per LINE.
+template <int N, int AX, int H>
+__device__ __forceinline__ void line_base(const double *U, int i0, const double (&v1)[N], const double (&d1)[N],
+                                          const double (&v2)[N], const double (&d2)[N], double (&Pp)[H],
+                                          double (&Q1)[H], double (&Q2)[H]) {
+  using B = Blk<N>;
+  constexpr int LBU = CUT_LB_UNROLL > 0 ? CUT_LB_UNROLL : (N <= 7 ? H : 1);
+#pragma unroll LBU
+  for (int ii = 0; ii < H; ++ii) {
+    const int i = i0 + ii < N ? i0 + ii : N - 1;  // (odd n: the upper half's last slot is a dummy)
+    double p = 0.0, q1 = 0.0, q2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double uu = AX == 0 ? U[B::at(i, j, k)] : (AX == 1 ? U[B::at(j, i, k)] : U[B::at(j, k, i)]);
+        s0 = fma(v1[j], uu, s0);
+        s1 = fma(d1[j], uu, s1);
+      }
+      p = fma(v2[k], s0, p);
+      q1 = fma(v2[k], s1, q1);
+      q2 = fma(d2[k], s0, q2);
+    }
+    Pp[ii] = p;
+    Q1[ii] = q1;
+    Q2[ii] = q2;
+  }
+}
+
+// Lines are split over a thread pair along i (the line axis): each thread holds
+// the base sums and test coefficients of its half of the i range; the n-term sums
+// over i of a point are combined by one __shfl_xor (same bits on both threads).
+template <int N>
+__device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int64_t pb, int64_t pe, int ax,
+                                            const double *U, double *PS, double (&acc)[CutCfg<N>::RPT][N],
+                                            const KParams &kp, const RefTab &R) {
+  using C = CutCfg<N>;
+  constexpr int NN = C::NN, RPT = C::RPT, TG = C::TG, G = C::G;
+  constexpr int RL0 = 3 * NN + 3 * N, RL = (RL0 % 2 == 0) ? RL0 + 1 : RL0;  // row: S0 S1 S2 X0 X1 X2
+  constexpr int CL0 = (C::CHUNK * C::ROW) / RL, CL = CL0 < C::THREADS / 2 ? CL0 : C::THREADS / 2;  // lines/chunk
+  constexpr int H = (N + 1) / 2;  // i values per thread
+  const int tid = threadIdx.x, grp = tid / TG, rl = tid % TG;
+  const int lq = tid >> 1, part = tid & 1, i0 = part * H;
+  const double ih = 1.0 / kp.h, ih2 = ih * ih;
+  const int64_t nl = (pe - pb) / N;
+  for (int64_t l0 = 0; l0 < nl; l0 += CL) {
+    const int cnt = (int)((nl - l0) < CL ? (nl - l0) : CL);
+    {  // every thread takes part in the shuffles (idle pairs work on a dummy line)
+      const bool live = lq < cnt;
+      const double *p = pts + 4 * (pb + (l0 + (live ? lq : 0)) * N);
+      const double b1 = ax == 0 ? p[1] : p[0], b2 = ax == 2 ? p[1] : p[2];
+      double Pp[H], Q1[H], Q2[H];
+      {  // the base bases are recomputed for the rows below (not kept live over the points)
+        double v1[N], d1[N], v2[N], d2[N];
+        basis_vd<N>(R, b1, v1, d1);
+        basis_vd<N>(R, b2, v2, d2);
+        if (ax == 0) line_base<N, 0, H>(U, i0, v1, d1, v2, d2, Pp, Q1, Q2);
+        else if (ax == 1) line_base<N, 1, H>(U, i0, v1, d1, v2, d2, Pp, Q1, Q2);
+        else line_base<N, 2, H>(U, i0, v1, d1, v2, d2, Pp, Q1, Q2);
+      }
+      double R0[H], R1[H], R2[H];
+#pragma unroll
+      for (int ii = 0; ii < H; ++ii) R0[ii] = R1[ii] = R2[ii] = 0.0;
+#pragma unroll 1
+      for (int t = 0; t < N; ++t) {
+        const double tc = p[4 * t + ax], W = live ? p[4 * t + 3] : 0.0;
+        double va[N], da[N];
+        basis_vd<N>(R, tc, va, da);
+        double vh[H], dh[H];  // this thread's half (i0 + ii), dummy slot zero
+#pragma unroll
+        for (int ii = 0; ii < H; ++ii) {
+          double x = 0.0, y = 0.0;
+#pragma unroll
+          for (int m = 0; m < N; ++m)
+            if (m == i0 + ii) {
+              x = va[m];
+              y = da[m];
+            }
+          vh[ii] = x;
+          dh[ii] = y;
+        }
+        double uA = 0.0, uB1 = 0.0, uB2 = 0.0;
+#pragma unroll
+        for (int ii = 0; ii < H; ++ii) {
+          uA = fma(dh[ii], Pp[ii], uA);
+          uB1 = fma(vh[ii], Q1[ii], uB1);
+          uB2 = fma(vh[ii], Q2[ii], uB2);
+        }
+        uA += __shfl_xor_sync(0xffffffffu, uA, 1);
+        uB1 += __shfl_xor_sync(0xffffffffu, uB1, 1);
+        uB2 += __shfl_xor_sync(0xffffffffu, uB2, 1);
+        const double sw = W * ih2;
+        const double cA = sw * uA, cB1 = sw * uB1, cB2 = sw * uB2;
+#pragma unroll
+        for (int ii = 0; ii < H; ++ii) {
+          R0[ii] = fma(cA, dh[ii], R0[ii]);
+          R1[ii] = fma(cB1, vh[ii], R1[ii]);
+          R2[ii] = fma(cB2, vh[ii], R2[ii]);
+        }
+      }
+      if (live) {
+        double v1[N], d1[N], v2[N], d2[N];
+        basis_vd<N>(R, b1, v1, d1);
+        basis_vd<N>(R, b2, v2, d2);
+        double *row = PS + lq * RL;
+        if (ax == 0) {  // i = a: X = R (own a), S[b + N c] = l1_b l2_c, l1'_b l2_c, l1_b l2'_c (c parity)
+#pragma unroll
+          for (int c = 0; c < N; ++c) {
+            if ((c & 1) != part) continue;
+#pragma unroll
+            for (int b = 0; b < N; ++b) {
+              row[b + N * c] = v1[b] * v2[c];
+              row[NN + b + N * c] = d1[b] * v2[c];
+              row[2 * NN + b + N * c] = v1[b] * d2[c];
+            }
+          }
+#pragma unroll
+          for (int ii = 0; ii < H; ++ii) {
+            const int a = i0 + ii;
+            if (a < N) {
+              row[3 * NN + a] = R0[ii];
+              row[3 * NN + N + a] = R1[ii];
+              row[3 * NN + 2 * N + a] = R2[ii];
+            }
+          }
+        } else {  // j = a: X0 = l1, X1 = l1'; own i = b (ax = y) or c (ax = z)
+#pragma unroll
+          for (int ii = 0; ii < H; ++ii) {
+            const int i = i0 + ii;
+            if (i >= N) continue;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              const int bc = ax == 1 ? i + N * k : k + N * i;
+              row[bc] = fma(R0[ii], v2[k], R2[ii] * d2[k]);
+              row[NN + bc] = R1[ii] * v2[k];
+            }
+          }
+          if (part == 0) {
+#pragma unroll
+            for (int a = 0; a < N; ++a) {
+              row[3 * NN + a] = v1[a];
+              row[3 * NN + N + a] = d1[a];
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (grp < G) {
+      for (int qq = grp; qq < cnt; qq += G) {
+        const double *row = PS + qq * RL;
+        double x0[N], x1[N];
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          x0[a] = row[3 * NN + a];
+          x1[a] = row[3 * NN + N + a];
+        }
+        if (ax == 0) {
+          double x2[N];
+#pragma unroll
+          for (int a = 0; a < N; ++a) x2[a] = row[3 * NN + 2 * N + a];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int bc = rl * RPT + r;
+            if (bc < NN) {
+              const double s0 = row[bc], s1 = row[NN + bc], s2 = row[2 * NN + bc];
+#pragma unroll
+              for (int a = 0; a < N; ++a) acc[r][a] = fma(x0[a], s0, fma(x1[a], s1, fma(x2[a], s2, acc[r][a])));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int bc = rl * RPT + r;
+            if (bc < NN) {
+              const double s0 = row[bc], s1 = row[NN + bc];
+#pragma unroll
+              for (int a = 0; a < N; ++a) acc[r][a] = fma(x0[a], s0, fma(x1[a], s1, acc[r][a]));
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__restrict__ u, double *__restrict__ v,
                                              const CDesc *__restrict__ desc, int ncut,
@@ -903,7 +1105,17 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
 #pragma unroll
     for (int a = 0; a < N; ++a) acc[r][a] = 0.0;
   if (kp.mask & TERM_CELL)
-    point_chunks<N, false>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], U, PS, acc, kp, R);
+  {
+    if constexpr (C::ROWINT) {
+      if ((dsc.flags >> 26) & 1u)  // volume points in lines along axis (flags >> 24) & 3
+        line_chunks<N>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], (int)((dsc.flags >> 24) & 3u), U, PS, acc,
+                       kp, R);
+      else
+        point_chunks<N, false>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], U, PS, acc, kp, R);
+    } else {
+      point_chunks<N, false>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], U, PS, acc, kp, R);
+    }
+  }
   if (kp.mask & TERM_NITSCHE)
     point_chunks<N, true>(srf_pts, srf_ptr[dsc.cut], srf_ptr[dsc.cut + 1], U, PS, acc, kp, R);
   if constexpr (!C::ROWINT) {
