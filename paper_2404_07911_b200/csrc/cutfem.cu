@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <array>
+#include <map>
+#include <unordered_map>
 #include <queue>
 #include <cmath>
 #include <cstdio>
@@ -20,6 +22,7 @@
 #include <cstring>
 #include <string>
 #include <unordered_map>
+#include <map>
 #include <vector>
 
 #include "../../include/cutfem.h"
@@ -92,6 +95,7 @@ struct cutfem_handle {
   int uncw_ctas = 0;            // n = 5, 6: k_uncw CTAs per SM (0: occupancy)
   int uncw_hi = 1 << 8;         // bit n (7..9): uncut cells through k_uncw (env CUTFEM_UNCW_HI=mask)
   bool vlines = true;           // k_cutp: volume points in lines where they form lines (env CUTFEM_NO_VLINES)
+  bool slines = true;           // k_cutp: interface points on the volume lines (env CUTFEM_NO_SLINES)
   char *d_stream = nullptr;     // the packed stream (chunk headers + point rows)
   int64_t w_off[3] = {0};
   int grid_cutp[3] = {0};
@@ -409,6 +413,26 @@ static int vol_line_axis(const double *vp, int64_t nv, int n) {
   return ax;
 }
 
+// The interface points of a line cell that lie on its volume lines (same two base
+// coordinates, at most one per line): line index per interface point, or empty if
+// any point is off the lines (the cell then streams its interface points singly).
+static std::vector<int> srf_on_lines(const double *vp, int64_t nv, const double *sp, int64_t ns, int n, int ax) {
+  std::vector<int> li;
+  if (ns <= 0) return li;
+  const int b1 = ax == 0 ? 1 : 0, b2 = ax == 2 ? 1 : 2;
+  std::map<std::pair<double, double>, int> key;
+  for (int64_t l = 0; l < nv / n; ++l) key[{vp[4 * l * n + b1], vp[4 * l * n + b2]}] = (int)l;
+  std::vector<char> used(nv / n, 0);
+  li.resize(ns);
+  for (int64_t q = 0; q < ns; ++q) {
+    auto it = key.find({sp[7 * q + b1], sp[7 * q + b2]});
+    if (it == key.end() || used[it->second]) return {};
+    used[it->second] = 1;
+    li[q] = it->second;
+  }
+  return li;
+}
+
 template <int N>
 int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<UDesc> &ud,
                 const std::vector<CDesc> &cd) {
@@ -572,7 +596,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
           // by axis (a chunk never mixes a face point with another kind or face axis: one
           // code path per chunk, which pays at n = 4 where registers are tight)
           int nv = (hd->mask & CUTFEM_TERM_CELL) ? e.nv : 0;
-          const int ns = (hd->mask & CUTFEM_TERM_NITSCHE) ? e.ns : 0;
+          int ns = (hd->mask & CUTFEM_TERM_NITSCHE) ? e.ns : 0;
           const bool fon = (hd->mask & CUTFEM_TERM_SIPG) != 0;
           const size_t k0 = chunk.size();
           // volume points in lines: chunks of <= 32 lines (sign bit, axis << 24), then the
@@ -581,16 +605,22 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
           int nlc = 0;  // line chunks of the cell (packed into nchunk's high half)
           if (lax >= 0) {
             const int nl = nv / N;
+            // the interface points ride on the lines when they all sit on distinct lines
+            // (needs both the cell and the Nitsche term: a record carries both)
+            const bool son = ns > 0 && nv > 0 && hd->slines &&
+                             !srf_on_lines(pb->vol_pts + 4 * e.vb, nv, pb->srf_pts + 7 * e.sb, ns, N, lax).empty();
             for (int l0 = 0; l0 < nl; l0 += 32) {
               CChunk r;
               r.vo = (int32_t)(e.vb + (int64_t)l0 * N);
               r.so = (int32_t)e.sb;
               r.fo = (int32_t)e.fb;
-              r.cnt = (int32_t)(0x80000000u | ((uint32_t)lax << 24) | (uint32_t)std::min(32, nl - l0));
+              r.cnt = (int32_t)(0x80000000u | (son ? 1u << 29 : 0u) | ((uint32_t)lax << 24) |
+                                (uint32_t)std::min(32, nl - l0));
               chunk.push_back(r);
               ++nlc;
             }
             nv = 0;
+            if (son) ns = 0;
           }
           if constexpr (CutPCfg<N>::UNIFIED) {
             // one stream: volume, interface, cut-face points (any axis) in chunks of 32
@@ -644,6 +674,9 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     // packets of <= CUTP_PK bytes, one bulk copy each
     std::vector<double> strm;
     std::vector<CPacket> pk;
+    std::map<int64_t, size_t> cell_of_vb;  // first volume point -> cut cell (line chunks)
+    for (size_t i = 0; i < c2.size(); ++i)
+      if (c2[i].nv > 0) cell_of_vb[c2[i].vb] = i;
     std::vector<int> ps;
     ps.reserve(ks.size());
     for (size_t w = 0; w + 1 < ks.size(); ++w) {
@@ -652,9 +685,9 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       CPacket cur = {(int64_t)strm.size() * 8, 0, 0};
       for (int k = ks[w]; k < ks[w + 1]; ++k) {
         const CChunk &r = chunk[k];
-        const bool line = r.cnt < 0;
+        const bool line = r.cnt < 0, lsrf = line && ((r.cnt >> 29) & 1);
         const int cv = r.cnt & 0xff, cs = line ? 0 : (r.cnt >> 8) & 0xff, cf = line ? 0 : (r.cnt >> 16) & 0xff;
-        const int bytes = line ? 16 + (16 + 16 * N) * cv : 16 + 32 * cv + 64 * cs + 32 * cf;
+        const int bytes = line ? 16 + (16 + 16 * N + (lsrf ? 48 : 0)) * cv : 16 + 32 * cv + 64 * cs + 32 * cf;
         if (cur.nch > 0 && cur.bytes + bytes > CutPCfg<N>::PK) {
           pk.push_back(cur);
           cur = {(int64_t)strm.size() * 8, 0, 0};
@@ -665,6 +698,19 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         if (line) {
           // per line: the two base coordinates (ascending axes), then (coordinate, W) per point
           const int ax = (r.cnt >> 24) & 3, b1 = ax == 0 ? 1 : 0, b2 = ax == 2 ? 1 : 2;
+          // the cell's lines and (lsrf) which interface point sits on each
+          std::vector<int> on;  // interface point per line of this chunk, -1 none
+          if (lsrf) {
+            // the cut cell of this chunk: its first line chunk starts at the cell's vb
+            auto it = cell_of_vb.upper_bound(r.vo);
+            --it;
+            const CDesc2 &e = c2[it->second];
+            const std::vector<int> li = srf_on_lines(pb->vol_pts + 4 * e.vb, e.nv, pb->srf_pts + 7 * e.sb, e.ns, N, ax);
+            const int l0 = (int)((r.vo - e.vb) / N);
+            on.assign(cv, -1);
+            for (size_t q = 0; q < li.size(); ++q)
+              if (li[q] >= l0 && li[q] < l0 + cv) on[li[q] - l0] = (int)(e.sb + (int64_t)q);
+          }
           for (int l = 0; l < cv; ++l) {
             const double *x = pb->vol_pts + 4 * ((size_t)r.vo + (size_t)l * N);
             strm.push_back(x[b1]);
@@ -672,6 +718,18 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
             for (int t = 0; t < N; ++t) {
               strm.push_back(x[4 * t + ax]);
               strm.push_back(x[4 * t + 3]);
+            }
+            if (lsrf) {
+              double rs6[6] = {0, 0, 0, 0, 0, 0};
+              if (on[l] >= 0) {
+                const double *y = pb->srf_pts + 7 * (size_t)on[l];  // xi eta zeta nx ny nz W
+                rs6[0] = y[ax];
+                rs6[1] = y[6];
+                rs6[2] = y[3 + ax];
+                rs6[3] = y[3 + b1];
+                rs6[4] = y[3 + b2];
+              }
+              strm.insert(strm.end(), rs6, rs6 + 6);
             }
           }
           cur.bytes += bytes;
@@ -1316,6 +1374,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   if (const char *e = std::getenv("CUTFEM_UNCW_CTAS")) hd->uncw_ctas = std::atoi(e);
   if (const char *e = std::getenv("CUTFEM_UNCW_HI")) hd->uncw_hi = (int)std::strtol(e, nullptr, 0);
   hd->vlines = std::getenv("CUTFEM_NO_VLINES") == nullptr;
+  hd->slines = std::getenv("CUTFEM_NO_SLINES") == nullptr;
   if (const char *e = std::getenv("CUTFEM_TILE_PERSIST")) hd->persist = std::atoi(e);
   else hd->persist = 3;
   if (!std::getenv("CUTFEM_NO_TILE") && (rc = dispatch_tiles(hd, pb, ud, cd))) return rc;

@@ -289,9 +289,10 @@ __device__ __forceinline__ constexpr int lpos(int i, int j, int k) {
   // i along AX, j along B1 < B2, k along B2 -> l = x + N y + N^2 z
   return AX == 0 ? (i + N * j + N * N * k) : (AX == 1 ? (j + N * i + N * N * k) : (j + N * k + N * N * i));
 }
-template <int N, int AX, int ACC>
+template <int N, int AX, bool SRF, int ACC>
 __device__ __forceinline__ void vol_line(double (&acc)[ACC], const RefTab &R, const double *U, const double *rec,
-                                         double ih2) {
+                                         const KParams &kp) {
+  const double ih2 = kp.ih2;
   double v1[N], d1[N], v2[N], d2[N];
   basis_vd_sym<N>(R, rec[0], v1, d1);
   basis_vd_sym<N>(R, rec[1], v2, d2);
@@ -338,6 +339,34 @@ __device__ __forceinline__ void vol_line(double (&acc)[ACC], const RefTab &R, co
       R0[i] = fma(cA, da[i], R0[i]);
       R1[i] = fma(cB1, va[i], R1[i]);
       R2[i] = fma(cB2, va[i], R2[i]);
+    }
+  }
+  if constexpr (SRF) {
+    // the line's interface (Nitsche) point, if any (W = 0 otherwise): rec[2 + 2N ..] =
+    // t, W, n_ax, n_B1, n_B2 (the unit normal in the line's axes); value term folded into R0
+    const double2 tw = *reinterpret_cast<const double2 *>(rec + 2 + 2 * N);
+    const double2 nn = *reinterpret_cast<const double2 *>(rec + 4 + 2 * N);
+    const double n2 = rec[6 + 2 * N];
+    if (tw.y != 0.0) {
+      double va[N], da[N];
+      basis_vd_sym<N>(R, tw.x, va, da);
+      double u0 = 0.0, uA = 0.0, uB1 = 0.0, uB2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        u0 = fma(va[i], Pp[i], u0);
+        uA = fma(da[i], Pp[i], uA);
+        uB1 = fma(va[i], Q1[i], uB1);
+        uB2 = fma(va[i], Q2[i], uB2);
+      }
+      const double un = (nn.x * uA + nn.y * uB1 + n2 * uB2) * kp.ih;  // physical normal derivative
+      const double c0 = tw.y * (kp.tau * u0 - un), g = -tw.y * u0 * kp.ih;
+      const double cA = g * nn.x, cB1 = g * nn.y, cB2 = g * n2;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        R0[i] = fma(cA, da[i], fma(c0, va[i], R0[i]));
+        R1[i] = fma(cB1, va[i], R1[i]);
+        R2[i] = fma(cB2, va[i], R2[i]);
+      }
     }
   }
 #pragma unroll
@@ -615,14 +644,22 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
       if (left == 0) next_packet();
       const int cnt = reinterpret_cast<const int *>(S + pos)[0];
       const int cv = cnt & 0xff, ax = (cnt >> 24) & 3;
+      const bool srf = (cnt >> 29) & 1;  // records carry the line's interface point
+      const int rs = 2 + 2 * N + (srf ? 6 : 0);
       const double *P = S + pos + 2;
       --left;
-      pos += 2 + (2 + 2 * N) * cv;
+      pos += 2 + rs * cv;
       if (lane < cv) {
-        const double *rec = P + (2 + 2 * N) * lane;
-        if (ax == 0) vol_line<N, 0>(acc, R, U, rec, ih2);
-        else if (ax == 1) vol_line<N, 1>(acc, R, U, rec, ih2);
-        else vol_line<N, 2>(acc, R, U, rec, ih2);
+        const double *rec = P + rs * lane;
+        if (srf) {
+          if (ax == 0) vol_line<N, 0, true>(acc, R, U, rec, kp);
+          else if (ax == 1) vol_line<N, 1, true>(acc, R, U, rec, kp);
+          else vol_line<N, 2, true>(acc, R, U, rec, kp);
+        } else {
+          if (ax == 0) vol_line<N, 0, false>(acc, R, U, rec, kp);
+          else if (ax == 1) vol_line<N, 1, false>(acc, R, U, rec, kp);
+          else vol_line<N, 2, false>(acc, R, U, rec, kp);
+        }
       }
       __syncwarp();
       if (lane == 0 && left == 0) fence_proxy_async();
