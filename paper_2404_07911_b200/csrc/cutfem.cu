@@ -104,6 +104,7 @@ struct cutfem_handle {
   CDesc *d_cdesc = nullptr;
   double *d_vol = nullptr, *d_srf = nullptr, *d_sfp = nullptr;
   int64_t *d_volptr = nullptr, *d_srfptr = nullptr, *d_sfptr = nullptr;
+  int32_t *d_line_srf = nullptr;  // k_cut line cells: interface point on each line (-1 none)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // host path buffers
@@ -965,7 +966,7 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
     } else {
       k_cut<N><<<(unsigned)nc, CutCfg<N>::THREADS, CutCfg<N>::SMEM, cs>>>(
           u, v, dc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp, hd->d_sfptr, hd->kp,
-          hd->ft, *reinterpret_cast<const TileTab<N> *>(hd->ttab.data()));
+          hd->ft, *reinterpret_cast<const TileTab<N> *>(hd->ttab.data()), hd->d_line_srf);
     }
     CU(cudaGetLastError());
   }
@@ -1111,6 +1112,7 @@ void free_handle(cutfem_handle *hd) {
   cudaFree(hd->d_srf);
   cudaFree(hd->d_sfp);
   cudaFree(hd->d_volptr);
+  cudaFree(hd->d_line_srf);
   cudaFree(hd->d_srfptr);
   cudaFree(hd->d_sfptr);
   cudaFree(hd->d_u);
@@ -1227,6 +1229,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   // descriptors
   std::vector<UDesc> ud;
   std::vector<CDesc> cd;
+  std::vector<int32_t> line_srf;  // k_cut: interface point per volume line of the line cells
   std::vector<int64_t> ccost;
   if (n_compute < 0) n_compute = na;
   hd->n_own = n_compute;
@@ -1282,10 +1285,23 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
           cost += (pb->sf_ptr[s + 1] - pb->sf_ptr[s]) / 2;
         }
       }
-      // k_cut (n >= 5): volume points in lines -> flag bit 26, axis in bits 24-25
+      // k_cut (n >= 5): volume points in lines -> flag bit 26, axis in bits 24-25; the
+      // interface points on the lines -> bit 27, per-line index list from c.pad
       if (n >= 5 && !std::getenv("CUTFEM_NO_VLINES")) {
         const int lax = vol_line_axis(pb->vol_pts + 4 * c.vb, c.nv, n);
-        if (lax >= 0) c.flags |= (1u << 26) | ((uint32_t)lax << 24);
+        if (lax >= 0) {
+          c.flags |= (1u << 26) | ((uint32_t)lax << 24);
+          const std::vector<int> li = std::getenv("CUTFEM_NO_SLINES")
+                                          ? std::vector<int>()
+                                          : srf_on_lines(pb->vol_pts + 4 * c.vb, c.nv, pb->srf_pts + 7 * c.sb, c.ns, n, lax);
+          if (!li.empty()) {
+            c.flags |= 1u << 27;
+            c.pad = (int32_t)line_srf.size();
+            const size_t l0 = line_srf.size();
+            line_srf.resize(l0 + c.nv / n, -1);
+            for (size_t q = 0; q < li.size(); ++q) line_srf[l0 + li[q]] = (int32_t)(c.sb + (int64_t)q);
+          }
+        }
       }
       cd.push_back(c);
       ccost.push_back(cost + (bnd ? (int64_t)1 << 40 : 0));  // boundary cells sort last (key), heavy first
@@ -1364,6 +1380,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
     if ((rc = upload(hd, &hd->d_sfp, f4.data(), f4.size()))) return rc;
   }
   if ((rc = upload(hd, &hd->d_volptr, pb->vol_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
+  if (!line_srf.empty() && (rc = upload(hd, &hd->d_line_srf, line_srf.data(), line_srf.size()))) return rc;
   if ((rc = upload(hd, &hd->d_srfptr, pb->srf_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_sfptr, pb->sf_ptr, (size_t)(nsf ? nsf + 1 : 0)))) return rc;
   hd->cut_last = std::getenv("CUTFEM_CUT_LAST") != nullptr;

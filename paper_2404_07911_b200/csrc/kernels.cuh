@@ -906,7 +906,8 @@ __device__ __forceinline__ void line_base(const double *U, int i0, const double 
 template <int N>
 __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int64_t pb, int64_t pe, int ax,
                                             const double *U, double *PS, double (&acc)[CutCfg<N>::RPT][N],
-                                            const KParams &kp, const RefTab &R) {
+                                            const KParams &kp, const RefTab &R, const int *__restrict__ lsrf,
+                                            const double *__restrict__ srf_pts) {
   using C = CutCfg<N>;
   constexpr int NN = C::NN, RPT = C::RPT, TG = C::TG, G = C::G;
   constexpr int RL0 = 3 * NN + 3 * N, RL = (RL0 % 2 == 0) ? RL0 + 1 : RL0;  // row: S0 S1 S2 X0 X1 X2
@@ -967,6 +968,50 @@ __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int6
 #pragma unroll
         for (int ii = 0; ii < H; ++ii) {
           R0[ii] = fma(cA, dh[ii], R0[ii]);
+          R1[ii] = fma(cB1, vh[ii], R1[ii]);
+          R2[ii] = fma(cB2, vh[ii], R2[ii]);
+        }
+      }
+      if (lsrf) {
+        // the line's interface (Nitsche) point, if any; every pair runs this (W = 0 when
+        // absent) so the shuffles stay convergent; value term folded into R0
+        const int q = live ? lsrf[l0 + lq] : -1;
+        const double *y = srf_pts + 8 * (int64_t)(q >= 0 ? q : 0);
+        const double tc = y[ax], W = q >= 0 ? y[6] : 0.0;
+        const double nA = y[3 + ax], nB1 = y[3 + (ax == 0 ? 1 : 0)], nB2 = y[3 + (ax == 2 ? 1 : 2)];
+        double va[N], da[N];
+        basis_vd<N>(R, tc, va, da);
+        double vh[H], dh[H];
+#pragma unroll
+        for (int ii = 0; ii < H; ++ii) {
+          double x = 0.0, z = 0.0;
+#pragma unroll
+          for (int m = 0; m < N; ++m)
+            if (m == i0 + ii) {
+              x = va[m];
+              z = da[m];
+            }
+          vh[ii] = x;
+          dh[ii] = z;
+        }
+        double u0 = 0.0, uA = 0.0, uB1 = 0.0, uB2 = 0.0;
+#pragma unroll
+        for (int ii = 0; ii < H; ++ii) {
+          u0 = fma(vh[ii], Pp[ii], u0);
+          uA = fma(dh[ii], Pp[ii], uA);
+          uB1 = fma(vh[ii], Q1[ii], uB1);
+          uB2 = fma(vh[ii], Q2[ii], uB2);
+        }
+        u0 += __shfl_xor_sync(0xffffffffu, u0, 1);
+        uA += __shfl_xor_sync(0xffffffffu, uA, 1);
+        uB1 += __shfl_xor_sync(0xffffffffu, uB1, 1);
+        uB2 += __shfl_xor_sync(0xffffffffu, uB2, 1);
+        const double un = (nA * uA + nB1 * uB1 + nB2 * uB2) * ih;  // physical normal derivative
+        const double c0 = W * (kp.tau * u0 - un), g = -W * u0 * ih;
+        const double cA = g * nA, cB1 = g * nB1, cB2 = g * nB2;
+#pragma unroll
+        for (int ii = 0; ii < H; ++ii) {
+          R0[ii] = fma(cA, dh[ii], fma(c0, vh[ii], R0[ii]));
           R1[ii] = fma(cB1, vh[ii], R1[ii]);
           R2[ii] = fma(cB2, vh[ii], R2[ii]);
         }
@@ -1067,7 +1112,7 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
                                              const int64_t *__restrict__ srf_ptr,
                                              const double *__restrict__ sf_pts,
                                              const int64_t *__restrict__ sf_ptr, KParams kp, FaceTab ft,
-                                             TileTab<N> tt) {
+                                             TileTab<N> tt, const int *__restrict__ line_srf) {
   using B = Blk<N>;
   using C = CutCfg<N>;
   constexpr int NN = B::NN, N3 = B::N3, SZ = B::SZ, TH = C::THREADS;
@@ -1109,14 +1154,15 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
     if constexpr (C::ROWINT) {
       if ((dsc.flags >> 26) & 1u)  // volume points in lines along axis (flags >> 24) & 3
         line_chunks<N>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], (int)((dsc.flags >> 24) & 3u), U, PS, acc,
-                       kp, R);
+                       kp, R, ((dsc.flags >> 27) & 1u) && (kp.mask & TERM_NITSCHE) ? line_srf + dsc.pad : nullptr,
+                       srf_pts);
       else
         point_chunks<N, false>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], U, PS, acc, kp, R);
     } else {
       point_chunks<N, false>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], U, PS, acc, kp, R);
     }
   }
-  if (kp.mask & TERM_NITSCHE)
+  if ((kp.mask & TERM_NITSCHE) && !(C::ROWINT && ((dsc.flags >> 27) & 1u) && (kp.mask & TERM_CELL)))
     point_chunks<N, true>(srf_pts, srf_ptr[dsc.cut], srf_ptr[dsc.cut + 1], U, PS, acc, kp, R);
   if constexpr (!C::ROWINT) {
     static_assert(C::KPT <= N, "acc[0] holds the thread's DoFs");
