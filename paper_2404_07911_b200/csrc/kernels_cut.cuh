@@ -145,6 +145,9 @@ struct __align__(16) CPacket {
 #ifndef CUTP_BFLY_MAXACC
 #define CUTP_BFLY_MAXACC 32  // accumulators <= this: shuffle reduce-scatter instead of the transpose
 #endif
+#ifndef CUTP_HYB
+#define CUTP_HYB 1
+#endif
 #ifndef CUTP_RW
 #define CUTP_RW 16  // rows of the reduction transpose buffer
 #endif
@@ -394,6 +397,8 @@ struct CutPCfg {
   // axis: runtime-axis face update); else chunks are kind- and axis-homogeneous
   static constexpr bool UNIFIED = N <= CUTP_UNIFIED_MAXN;
   static constexpr bool BFLY = ACC <= CUTP_BFLY_MAXACC;
+  // 64 accumulators: one butterfly level (xor 16) + a 16-lane shared-memory transpose
+  static constexpr bool HYB = !BFLY && ACC == 64 && CUTP_HYB;
   // bars(2 + NB) | UB[2][7][N3P] | JAB[6][2][NN] | ring[NB][2 + PK/8] (nch + packet)
   static constexpr int OFF_UB = (2 + NB + 1) & ~1;
   static constexpr int OFF_JAB = OFF_UB + 2 * 7 * N3P;
@@ -402,7 +407,7 @@ struct CutPCfg {
   static constexpr int OFF_WS = OFF_RING + NB * RSLOT;  // w of the structured faces (n^3)
   static constexpr int OFF_RED = OFF_WS + ((N3 + 1) & ~1);  // reduction transpose [RW][33]
   static constexpr int RW = ACC < CUTP_RW ? ACC : CUTP_RW;      // accumulators per reduction pass
-  static constexpr int WSLOT = OFF_RED + (BFLY ? 0 : RW * 33);
+  static constexpr int WSLOT = OFF_RED + (BFLY ? 0 : (HYB ? 32 * 17 : RW * 33));
   static constexpr int SMEM = WARPS * WSLOT * 8;
 };
 
@@ -765,8 +770,39 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
         }
       }
     }
+    if constexpr (C::HYB) {
+      // lanes l, l^16 exchange halves (xor 16): half h = lane >> 4 then holds entries
+      // 32 h + i summed over the pair; two passes transpose 16 of them over the 16 lanes
+      // of each half through shared memory, lane l summing entry 32 (l >> 4) + 16 ps + (l & 15)
+      const bool up = (lane & 16) != 0;
+      double a32[32];
 #pragma unroll
-    for (int ps = 0; ps < (C::BFLY ? 0 : C::ACC / RW); ++ps) {
+      for (int i = 0; i < 32; ++i) {
+        const double send = up ? acc[i] : acc[i + 32];
+        const double keep = up ? acc[i + 32] : acc[i];
+        a32[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+      const int h = lane >> 4, l16 = lane & 15;
+#pragma unroll
+      for (int ps = 0; ps < 2; ++ps) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) RED[(h * 16 + i) * 17 + l16] = a32[ps * 16 + i];
+        __syncwarp();
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) {
+          s0 += RED[lane * 17 + k];
+          s1 += RED[lane * 17 + k + 1];
+          s2 += RED[lane * 17 + k + 2];
+          s3 += RED[lane * 17 + k + 3];
+        }
+        const int e = 32 * h + 16 * ps + l16;
+        vb[e] = ((s0 + s1) + (s2 + s3)) + (st_on ? WS[e] : 0.0);
+        __syncwarp();
+      }
+    }
+#pragma unroll
+    for (int ps = 0; ps < ((C::BFLY || C::HYB) ? 0 : C::ACC / RW); ++ps) {
 #pragma unroll
       for (int i = 0; i < RW; ++i) RED[i * 33 + lane] = acc[ps * RW + i];
       __syncwarp();
