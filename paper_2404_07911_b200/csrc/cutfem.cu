@@ -96,6 +96,8 @@ struct cutfem_handle {
   int uncw_hi = 1 << 8;         // bit n (7..9): uncut cells through k_uncw (env CUTFEM_UNCW_HI=mask)
   bool vlines = true;           // k_cutp: volume points in lines where they form lines (env CUTFEM_NO_VLINES)
   bool slines = true;           // k_cutp: interface points on the volume lines (env CUTFEM_NO_SLINES)
+  bool flines = false;          // k_cutp: cut-face points in lines (env CUTFEM_FLINES=1; measured slower:
+                                // ~10 face lines per cell over 3 normal axes leave most lanes idle)
   char *d_stream = nullptr;     // the packed stream (chunk headers + point rows)
   int64_t w_off[3] = {0};
   int grid_cutp[3] = {0};
@@ -509,6 +511,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     std::vector<CDesc2> c2(cd.size());
     std::vector<double> fac;
     std::vector<std::array<int32_t, 3>> fax(cd.size(), std::array<int32_t, 3>{0, 0, 0});  // face points per axis
+    std::vector<std::array<int32_t, 6>> fcn(cd.size(), std::array<int32_t, 6>{0, 0, 0, 0, 0, 0});  // per face
     for (size_t i = 0; i < cd.size(); ++i) {
       const CDesc &d = cd[i];
       CDesc2 &e = c2[i];
@@ -539,7 +542,51 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       }
       e.nf = (int32_t)((int64_t)fac.size() / 4 - e.fb);
       for (int f = 0; f < 6; ++f)
-        if ((e.fmask >> f) & 1u) fax[i][f >> 1] += (int32_t)(pb->sf_ptr[d.sf[f] + 1] - pb->sf_ptr[d.sf[f]]);
+        if ((e.fmask >> f) & 1u) {
+          fcn[i][f] = (int32_t)(pb->sf_ptr[d.sf[f] + 1] - pb->sf_ptr[d.sf[f]]);
+          fax[i][f >> 1] += fcn[i][f];
+        }
+    }
+    // cut-face points in LINES (2-D dimension reduction on the face): per cell, every face's
+    // points in groups of N consecutive rows with the normal coordinate and one in-face
+    // coordinate shared exactly; fl_s / fl_m hold the fixed coordinate and sd + 2 tl per
+    // line, keyed by the line's first row
+    std::vector<char> fline(cd.size(), 0);
+    std::vector<double> fl_s(fac.size() / 4, 0.0), fl_m(fac.size() / 4, 0.0);
+    for (size_t i = 0; i < cd.size() && hd->flines; ++i) {
+      const CDesc2 &e = c2[i];
+      if (e.nf <= 0) continue;
+      bool ok = true;
+      int64_t row = e.fb;
+      for (int f = 0; f < 6 && ok; ++f) {
+        const int cnt = fcn[i][f];
+        if (cnt == 0) continue;
+        if (cnt % N != 0) {
+          ok = false;
+          break;
+        }
+        const int dd = f >> 1, e1 = dd == 0 ? 1 : 0, e2 = dd == 2 ? 1 : 2;
+        for (int g = 0; g < cnt && ok; g += N) {
+          const double *a = &fac[4 * (row + g)];
+          int var = -1;
+          for (int t = 1; t < N; ++t) {
+            const double *b = &fac[4 * (row + g + t)];
+            const bool s1 = a[e1] == b[e1], s2 = a[e2] == b[e2];
+            const int v = (s1 && !s2) ? e2 : ((s2 && !s1) ? e1 : -1);
+            if (v < 0 || (var >= 0 && v != var) || a[dd] != b[dd]) {
+              ok = false;
+              break;
+            }
+            var = v;
+          }
+          if (!ok) break;
+          const int tl = var == e2 ? 1 : 0;
+          fl_s[row + g] = tl ? a[e1] : a[e2];
+          fl_m[row + g] = (double)((f & 1) + 2 * tl);
+        }
+        row += cnt;
+      }
+      fline[i] = ok ? 1 : 0;
     }
     CU(cudaFuncSetAttribute(k_cutp<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutPCfg<N>::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_cutp, k_cutp<N>, 32 * CutPCfg<N>::WARPS,
@@ -571,8 +618,9 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       }
       auto cost = [&](const CDesc2 &e) {
         const int64_t i = &e - c2.data();
-        if (isline[i]) return 2.8 * ((e.nv / N + 31) / 32) + (double)((e.ns + e.nf + 31) / 32) + 1.5;
-        return (double)((e.nv + e.ns + e.nf + 31) / 32) + 1.5;
+        const int nf = fline[i] ? e.nf / 2 : e.nf;  // face lines cost about half a point chunk per 32 points
+        if (isline[i]) return 2.8 * ((e.nv / N + 31) / 32) + (double)((e.ns + nf + 31) / 32) + 1.5;
+        return (double)((e.nv + e.ns + nf + 31) / 32) + 1.5;
       };
       for (int64_t i = 0; i < n; ++i) idx[i] = o + i;
       std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return cost(c2[a]) > cost(c2[b]); });
@@ -623,9 +671,29 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
             nv = 0;
             if (son) ns = 0;
           }
+          // cut-face lines, normal axis by axis (faces 2D, 2D+1 are consecutive rows)
+          int nfc = 0;
+          bool fdone = false;
+          if (fon && fline[i]) {
+            int64_t row = e.fb;
+            for (int dd = 0; dd < 3; ++dd) {
+              const int nl = (fcn[i][2 * dd] + fcn[i][2 * dd + 1]) / N;
+              for (int l0 = 0; l0 < nl; l0 += 32) {
+                CChunk r;
+                r.vo = (int32_t)e.vb;
+                r.so = (int32_t)e.sb;
+                r.fo = (int32_t)(row + (int64_t)l0 * N);
+                r.cnt = (int32_t)((1u << 30) | ((uint32_t)dd << 24) | (uint32_t)std::min(32, nl - l0));
+                chunk.push_back(r);
+                ++nfc;
+              }
+              row += (int64_t)nl * N;
+            }
+            fdone = true;
+          }
           if constexpr (CutPCfg<N>::UNIFIED) {
             // one stream: volume, interface, cut-face points (any axis) in chunks of 32
-            const int nf = fon ? e.nf : 0;
+            const int nf = (fon && !fdone) ? e.nf : 0;
             for (int q0 = 0; q0 < nv + ns + nf; q0 += 32) {
               const int cv = std::max(0, std::min(32, nv - q0));
               const int qs = std::max(0, q0 - nv), cs = std::max(0, std::min(32 - cv, ns - qs));
@@ -649,7 +717,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
               chunk.push_back(r);
             }
             int64_t fo = e.fb;
-            for (int ax = 0; ax < 3 && fon; ++ax) {
+            for (int ax = 0; ax < 3 && fon && !fdone; ++ax) {
               const int na = fax[i][ax];
               for (int q0 = 0; q0 < na; q0 += 32) {
                 CChunk r;
@@ -662,8 +730,9 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
               fo += na;
             }
           }
-          if (chunk.size() - k0 > 0xffff) return fail(CUTFEM_EUNSUPPORTED, "k_cutp: > 65535 point chunks in a cell");
-          c2o[pos - 1].nchunk = (int32_t)((chunk.size() - k0) | ((size_t)nlc << 16));
+          if (chunk.size() - k0 > 0xffff || nlc > 0xff || nfc > 0xff)
+            return fail(CUTFEM_EUNSUPPORTED, "k_cutp: too many point chunks in a cell");
+          c2o[pos - 1].nchunk = (int32_t)((uint32_t)(chunk.size() - k0) | ((uint32_t)nlc << 16) | ((uint32_t)nfc << 24));
         }
       }
       ws.push_back((int)(pos - o));
@@ -686,6 +755,31 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       CPacket cur = {(int64_t)strm.size() * 8, 0, 0};
       for (int k = ks[w]; k < ks[w + 1]; ++k) {
         const CChunk &r = chunk[k];
+        const bool fln = r.cnt >= 0 && ((r.cnt >> 30) & 1);  // cut-face lines
+        if (fln) {
+          const int nl = r.cnt & 0xff, dd = (r.cnt >> 24) & 3, e1 = dd == 0 ? 1 : 0, e2 = dd == 2 ? 1 : 2;
+          const int fbytes = 16 + (16 + 16 * N) * nl;
+          if (cur.nch > 0 && cur.bytes + fbytes > CutPCfg<N>::PK) {
+            pk.push_back(cur);
+            cur = {(int64_t)strm.size() * 8, 0, 0};
+          }
+          double hdr[2] = {0.0, 0.0};
+          std::memcpy(hdr, &r.cnt, sizeof(int32_t));
+          strm.insert(strm.end(), hdr, hdr + 2);
+          for (int l = 0; l < nl; ++l) {
+            const int64_t row = r.fo + (int64_t)l * N;
+            const int tl = ((int)fl_m[row]) >> 1;
+            strm.push_back(fl_s[row]);
+            strm.push_back(fl_m[row]);
+            for (int t = 0; t < N; ++t) {
+              strm.push_back(fac[4 * (row + t) + (tl ? e2 : e1)]);
+              strm.push_back(fac[4 * (row + t) + 3]);
+            }
+          }
+          cur.bytes += fbytes;
+          ++cur.nch;
+          continue;
+        }
         const bool line = r.cnt < 0, lsrf = line && ((r.cnt >> 29) & 1);
         const int cv = r.cnt & 0xff, cs = line ? 0 : (r.cnt >> 8) & 0xff, cf = line ? 0 : (r.cnt >> 16) & 0xff;
         const int bytes = line ? 16 + (16 + 16 * N + (lsrf ? 48 : 0)) * cv : 16 + 32 * cv + 64 * cs + 32 * cf;
@@ -1392,6 +1486,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   if (const char *e = std::getenv("CUTFEM_UNCW_HI")) hd->uncw_hi = (int)std::strtol(e, nullptr, 0);
   hd->vlines = std::getenv("CUTFEM_NO_VLINES") == nullptr;
   hd->slines = std::getenv("CUTFEM_NO_SLINES") == nullptr;
+  hd->flines = std::getenv("CUTFEM_FLINES") != nullptr;
   if (const char *e = std::getenv("CUTFEM_TILE_PERSIST")) hd->persist = std::atoi(e);
   else hd->persist = 3;
   if (!std::getenv("CUTFEM_NO_TILE") && (rc = dispatch_tiles(hd, pb, ud, cd))) return rc;

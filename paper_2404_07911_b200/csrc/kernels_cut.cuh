@@ -385,6 +385,91 @@ __device__ __forceinline__ void vol_line(double (&acc)[ACC], const RefTab &R, co
     }
 }
 
+// Cut-face points in LINES (the 2-D dimension-reduction rule on the face: n points
+// along one in-face axis at a fixed other in-face coordinate s).  Record:
+// [s, sd + 2 tl, (t, W) x n]: sd the side (0 lo face, 1 hi face of the normal axis D),
+// tl = 0 if the line runs along the lower in-face axis e1 (s on e2), 1 if along e2.
+// Per line: the trace interpolation reduced along s once (r_k = sum_m l_m(s) J[..]),
+// per point n-term sums for [u] and {d u} and M[m][k] += T_m l_k(t); then one
+// n^3 expansion acc(m on D, s-index, k on the line axis) += l(s) M.
+template <int N, int D, int ACC>
+__device__ __forceinline__ void face_line(double (&acc)[ACC], const RefTab &R, const double *JAB, const double *rec,
+                                          const KParams &kp) {
+  constexpr int NN = N * N, E1 = D == 0 ? 1 : 0, E2 = D == 2 ? 1 : 2;
+  const int meta = (int)rec[1], sd = meta & 1, tl = meta >> 1;
+  double ls[N];
+  basis_v_sym<N>(R, rec[0], ls);
+  const double *JA = JAB + (2 * D + sd) * 2 * NN, *JB = JA + NN;
+  double rJ[N], rA[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double x = 0.0, y = 0.0;
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      const int idx = tl ? (m + N * k) : (k + N * m);
+      x = fma(ls[m], JA[idx], x);
+      y = fma(ls[m], JB[idx], y);
+    }
+    rJ[k] = x;
+    rA[k] = y;
+  }
+  const double sg = sd ? kp.i2h : -kp.i2h;
+  double M[N][N];
+#pragma unroll
+  for (int m = 0; m < N; ++m)
+#pragma unroll
+    for (int k = 0; k < N; ++k) M[m][k] = 0.0;
+#pragma unroll
+  for (int t = 0; t < N; ++t) {
+    const double2 tw = *reinterpret_cast<const double2 *>(rec + 2 + 2 * t);
+    double lt[N];
+    basis_v_sym<N>(R, tw.x, lt);
+    double J = 0.0, A = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      J = fma(lt[k], rJ[k], J);
+      A = fma(lt[k], rA[k], A);
+    }
+    const double k1 = tw.y * fma(kp.sigma, J, -sg * A), k2 = -tw.y * sg * J;
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      double T = k2 * (sd ? R.d1[m] : R.d0[m]);
+      if (m == (sd ? N - 1 : 0)) T += k1;
+#pragma unroll
+      for (int k = 0; k < N; ++k) M[m][k] = fma(T, lt[k], M[m][k]);
+    }
+  }
+  // acc(position with D-index m, s-axis index i, line-axis index k) += ls_i M[m][k]
+  auto pos = [](int mD, int m1, int m2) {  // (D, e1, e2) coordinates -> l = x + N y + N^2 z
+    int c[3];
+    c[D] = mD;
+    c[E1] = m1;
+    c[E2] = m2;
+    return c[0] + N * c[1] + NN * c[2];
+  };
+  if (tl) {
+#pragma unroll
+    for (int m = 0; m < N; ++m)
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double &r = acc[pos(m, i, k)];
+          r = fma(ls[i], M[m][k], r);
+        }
+  } else {
+#pragma unroll
+    for (int m = 0; m < N; ++m)
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double &r = acc[pos(m, k, i)];
+          r = fma(ls[i], M[m][k], r);
+        }
+  }
+}
+
 template <int N>
 struct CutPCfg {
   static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
@@ -502,7 +587,9 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     if (has_next) nd = desc[c + 1];
     int nv, ns, nf;
     counts(cd, nv, ns, nf);
-    const int K = cd.nchunk & 0xffff, KL = cd.nchunk >> 16;  // chunks; the first KL are volume lines
+    // chunks of the cell: the first KL are volume lines, the next KF cut-face lines
+    const int K = (int)((uint32_t)cd.nchunk & 0xffffu), KL = (int)(((uint32_t)cd.nchunk >> 16) & 0xffu),
+              KF = (int)((uint32_t)cd.nchunk >> 24);
     const uint32_t fm = fmask_of(cd);
     // ---- this cell's blocks
     if constexpr (C::BULK) {
@@ -669,7 +756,25 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
       __syncwarp();
       if (lane == 0 && left == 0) fence_proxy_async();
     }
-    for (int k = KL; k < K; ++k) {
+    // cut-face LINES (their own loop too): chunks of cv lines on faces of normal axis
+    // (cnt >> 24) & 3, records of 2 + 2N doubles
+    for (int k = KL; k < KL + KF; ++k) {
+      if (left == 0) next_packet();
+      const int cnt = reinterpret_cast<const int *>(S + pos)[0];
+      const int cv = cnt & 0xff, dn = (cnt >> 24) & 3;
+      const double *P = S + pos + 2;
+      --left;
+      pos += 2 + (2 + 2 * N) * cv;
+      if (lane < cv) {
+        const double *rec = P + (2 + 2 * N) * lane;
+        if (dn == 0) face_line<N, 0>(acc, R, JAB, rec, kp);
+        else if (dn == 1) face_line<N, 1>(acc, R, JAB, rec, kp);
+        else face_line<N, 2>(acc, R, JAB, rec, kp);
+      }
+      __syncwarp();
+      if (lane == 0 && left == 0) fence_proxy_async();
+    }
+    for (int k = KL + KF; k < K; ++k) {
       if (left == 0) next_packet();
       const int cnt = reinterpret_cast<const int *>(S + pos)[0];
       const int cv = cnt & 0xff, cs = (cnt >> 8) & 0xff, cf = (cnt >> 16) & 0xff;
