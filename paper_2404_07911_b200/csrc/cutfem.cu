@@ -674,7 +674,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
           // cut-face lines, normal axis by axis (faces 2D, 2D+1 are consecutive rows)
           int nfc = 0;
           bool fdone = false;
-          if (fon && fline[i]) {
+          if (N >= 3 && fon && fline[i]) {
             int64_t row = e.fb;
             for (int dd = 0; dd < 3; ++dd) {
               const int nl = (fcn[i][2 * dd] + fcn[i][2 * dd + 1]) / N;

@@ -588,8 +588,9 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     int nv, ns, nf;
     counts(cd, nv, ns, nf);
     // chunks of the cell: the first KL are volume lines, the next KF cut-face lines
-    const int K = (int)((uint32_t)cd.nchunk & 0xffffu), KL = (int)(((uint32_t)cd.nchunk >> 16) & 0xffu),
-              KF = (int)((uint32_t)cd.nchunk >> 24);
+    // (lines never occur at n = 2: the host plans none, and the loops are compiled out)
+    const int K = (int)((uint32_t)cd.nchunk & 0xffffu), KL = N >= 3 ? (int)(((uint32_t)cd.nchunk >> 16) & 0xffu) : 0,
+              KF = N >= 3 ? (int)((uint32_t)cd.nchunk >> 24) : 0;
     const uint32_t fm = fmask_of(cd);
     // ---- this cell's blocks
     if constexpr (C::BULK) {
@@ -732,7 +733,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     };
     // volume LINES first (their own loop: the point loop below keeps its code
     // generation): chunks of cv lines along axis (cnt >> 24) & 3, records of 2 + 2N doubles
-    for (int k = 0; k < KL; ++k) {
+    for (int k = 0; k < (N >= 3 ? KL : 0); ++k) {
       if (left == 0) next_packet();
       const int cnt = reinterpret_cast<const int *>(S + pos)[0];
       const int cv = cnt & 0xff, ax = (cnt >> 24) & 3;
@@ -758,7 +759,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     }
     // cut-face LINES (their own loop too): chunks of cv lines on faces of normal axis
     // (cnt >> 24) & 3, records of 2 + 2N doubles
-    for (int k = KL; k < KL + KF; ++k) {
+    for (int k = KL; k < (N >= 3 ? KL + KF : KL); ++k) {
       if (left == 0) next_packet();
       const int cnt = reinterpret_cast<const int *>(S + pos)[0];
       const int cv = cnt & 0xff, dn = (cnt >> 24) & 3;
