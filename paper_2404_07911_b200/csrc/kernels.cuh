@@ -585,7 +585,13 @@ struct CutCfg {
   static constexpr int PBUF = PPF ? 2 * CHUNK * 8 : 0;
   static constexpr int OFF_PS = (3 + NBN) * Blk<N>::SZ + 4 * NN;
   static constexpr int OFF_PB = (OFF_PS + CHUNK * ROW + 1) & ~1;  // 16-byte aligned
-  static constexpr int SMEM_D = OFF_PB + PBUF;
+  // volume lines (ROWINT degrees): rows of 3 NN + 3 N doubles, CL lines per chunk, whose
+  // points [xi, eta, zeta, W] are staged in shared memory (LB) once per chunk
+  static constexpr int LRL0 = 3 * NN + 3 * N, LRL = (LRL0 % 2 == 0) ? LRL0 + 1 : LRL0;
+  static constexpr int LCL0 = (CHUNK * ROW) / LRL, LCL = LCL0 < THREADS / 2 ? LCL0 : THREADS / 2;
+  static constexpr int LBUF = ROWINT ? LCL * N * 4 : 0;
+  static constexpr int OFF_LB = OFF_PB + PBUF;  // even: 16-byte aligned
+  static constexpr int SMEM_D = OFF_LB + LBUF;
   static constexpr int SMEM = SMEM_D * 8;
 };
 
@@ -910,18 +916,25 @@ __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int6
                                             const double *__restrict__ srf_pts) {
   using C = CutCfg<N>;
   constexpr int NN = C::NN, RPT = C::RPT, TG = C::TG, G = C::G;
-  constexpr int RL0 = 3 * NN + 3 * N, RL = (RL0 % 2 == 0) ? RL0 + 1 : RL0;  // row: S0 S1 S2 X0 X1 X2
-  constexpr int CL0 = (C::CHUNK * C::ROW) / RL, CL = CL0 < C::THREADS / 2 ? CL0 : C::THREADS / 2;  // lines/chunk
+  constexpr int RL = C::LRL, CL = C::LCL;  // row: S0 S1 S2 X0 X1 X2; lines per chunk
   constexpr int H = (N + 1) / 2;  // i values per thread
+  double *LB = PS - C::OFF_PS + C::OFF_LB;  // the chunk's line points (CL N rows of 4 doubles)
   const int tid = threadIdx.x, grp = tid / TG, rl = tid % TG;
   const int lq = tid >> 1, part = tid & 1, i0 = part * H;
   const double ih = 1.0 / kp.h, ih2 = ih * ih;
   const int64_t nl = (pe - pb) / N;
   for (int64_t l0 = 0; l0 < nl; l0 += CL) {
     const int cnt = (int)((nl - l0) < CL ? (nl - l0) : CL);
+    {  // stage the chunk's points (16-byte pieces; the previous chunk is done with LB)
+      const double *src = pts + 4 * (pb + l0 * N);
+      for (int e = tid; e < cnt * N * 2; e += C::THREADS) cp_async16(LB + 2 * e, src + 2 * e);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+    }
     {  // every thread takes part in the shuffles (idle pairs work on a dummy line)
       const bool live = lq < cnt;
-      const double *p = pts + 4 * (pb + (l0 + (live ? lq : 0)) * N);
+      const double *p = LB + 4 * ((live ? lq : 0) * N);
       const double b1 = ax == 0 ? p[1] : p[0], b2 = ax == 2 ? p[1] : p[2];
       double Pp[H], Q1[H], Q2[H];
       {  // the base bases are recomputed for the rows below (not kept live over the points)
