@@ -717,6 +717,17 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
               chunk.push_back(r);
             }
             int64_t fo = e.fb;
+            if (CutPCfg<N>::FMIX && fon && !fdone) {  // every face axis in one stream
+              for (int q0 = 0; q0 < e.nf; q0 += 32) {
+                CChunk r;
+                r.vo = (int32_t)e.vb;
+                r.so = (int32_t)e.sb;
+                r.fo = (int32_t)(e.fb + q0);
+                r.cnt = std::min(32, e.nf - q0) << 16;
+                chunk.push_back(r);
+              }
+              fdone = true;
+            }
             for (int ax = 0; ax < 3 && fon && !fdone; ++ax) {
               const int na = fax[i][ax];
               for (int q0 = 0; q0 < na; q0 += 32) {

@@ -145,6 +145,9 @@ struct __align__(16) CPacket {
 #ifndef CUTP_BFLY_MAXACC
 #define CUTP_BFLY_MAXACC 32  // accumulators <= this: shuffle reduce-scatter instead of the transpose
 #endif
+#ifndef CUTP_FMIX
+#define CUTP_FMIX 1
+#endif
 #ifndef CUTP_HYB
 #define CUTP_HYB 1
 #endif
@@ -481,6 +484,9 @@ struct CutPCfg {
   // one chunk stream per cell mixing volume, interface and cut-face points (any face
   // axis: runtime-axis face update); else chunks are kind- and axis-homogeneous
   static constexpr bool UNIFIED = N <= CUTP_UNIFIED_MAXN;
+  // not unified: the cut-face points of a cell still form ONE stream over all face axes
+  // (runtime-axis update) instead of one per axis
+  static constexpr bool FMIX = !UNIFIED && CUTP_FMIX;
   static constexpr bool BFLY = ACC <= CUTP_BFLY_MAXACC;
   // 64 accumulators: one butterfly level (xor 16) + a 16-lane shared-memory transpose
   static constexpr bool HYB = !BFLY && ACC == 64 && CUTP_HYB;
@@ -846,7 +852,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
         }
       } else if (kind == 2) {
         // cut-face point: the face is the coordinate that is exactly 0 or 1
-        if constexpr (C::UNIFIED) {
+        if constexpr (C::UNIFIED || C::FMIX) {
           face_point_rt<N>(acc, R, JAB, xi, eta, zeta, W, kp);
         } else {
           const int d = (xi == 0.0 || xi == 1.0) ? 0 : ((eta == 0.0 || eta == 1.0) ? 1 : 2);
