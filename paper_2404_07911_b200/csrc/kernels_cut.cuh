@@ -633,12 +633,12 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     //      w <- (M (x) M (x) M) w; added to the point sums at the end (lanes 0..15 = lines)
     const uint32_t gm = gmask_of(cd), sm = smask_of(cd);
     if (gm | sm) {
-      for (int l = lane; l < N3; l += 32) WS[l] = 0.0;
-      __syncwarp();
       // per axis: lanes 0..15 the lo face in the own frame, lanes 16..31 the hi face in
       // the line-reversed frame (same lo-face coefficients: all operators are
-      // centro-symmetric); the hi half's rows are folded into the lo half by a shuffle
+      // centro-symmetric); the hi half's rows are folded into the lo half by a shuffle.
+      // The three axes are computed first (independent chains), then accumulated into w.
       const int hs = lane >> 4, t = lane & 15;
+      double oa[3][N];
       static_for<0, 3>([&](auto dc) {
         constexpr int D = dc.value;
         constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
@@ -683,9 +683,24 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
           double o2[N];
 #pragma unroll
           for (int m = 0; m < N; ++m) o2[m] = __shfl_xor_sync(0xffffffffu, out[m], 16);
-          if (hs == 0 && t < NN) {
 #pragma unroll
-            for (int m = 0; m < N; ++m) WS[b0 + m * str] += out[m] + o2[N - 1 - m];
+          for (int m = 0; m < N; ++m) oa[D][m] = out[m] + o2[N - 1 - m];
+        } else {
+#pragma unroll
+          for (int m = 0; m < N; ++m) oa[D][m] = 0.0;
+        }
+      });
+      // w = sum over the axes (axis 0's lines cover every position once: plain store first)
+      static_for<0, 3>([&](auto dc) {
+        constexpr int D = dc.value;
+        constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
+        if (hs == 0 && t < NN) {
+          const int tt0 = t % N, tt1 = t / N;
+          const int b0 = D == 0 ? N * tt0 + NN * tt1 : (D == 1 ? tt0 + NN * tt1 : tt0 + N * tt1);
+#pragma unroll
+          for (int m = 0; m < N; ++m) {
+            if (D == 0) WS[b0 + m * str] = oa[D][m];
+            else WS[b0 + m * str] += oa[D][m];
           }
         }
         __syncwarp();
