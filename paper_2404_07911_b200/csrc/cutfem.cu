@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <array>
+#include <type_traits>
 #include <map>
 #include <unordered_map>
 #include <queue>
@@ -481,16 +482,17 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       if (hd->gpw_cut && (c.gp | c.sipg)) set[1][pt - 1].push_back(c);
     }
   }
-  // set 0: k_tile* tiles (TileCfg<N>); set 1: k_gpw tiles (smaller, GpwCfg<N>::T).
-  // Offsets are in BYTES (the record sizes differ).
+  // set 0: k_tile* tiles (TileCfg<N>; k_tile2 at n = 4: Tile2Cfg<4>::T); set 1: k_gpw
+  // tiles (smaller, GpwCfg<N>::T).  Offsets are in BYTES (the record sizes differ).
   using CG = typename GpwCfg<N>::T;
+  using CK = typename std::conditional<N == 4, typename Tile2Cfg<4>::T, C>::type;
   std::vector<char> all;
   for (int k = 0; k < 2; ++k) {
-    const int64_t rs = k == 0 ? (int64_t)sizeof(TileRec<C::SMAX>) : (int64_t)sizeof(TileRec<CG::SMAX>);
+    const int64_t rs = k == 0 ? (int64_t)sizeof(TileRec<CK::SMAX>) : (int64_t)sizeof(TileRec<CG::SMAX>);
     std::vector<char> b0, b1;
     if (k == 0) {
-      build_tiles<C>(set[k][0], pb, b0);
-      build_tiles<C>(set[k][1], pb, b1);
+      build_tiles<CK>(set[k][0], pb, b0);
+      build_tiles<CK>(set[k][1], pb, b1);
     } else {
       build_tiles<CG>(set[k][0], pb, b0);
       build_tiles<CG>(set[k][1], pb, b1);
@@ -999,11 +1001,13 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
   }
   if (n0 > 0) {
     const unsigned grid = (unsigned)(hd->persist & 1 ? std::min<int64_t>(n0, (int64_t)hd->occ_tile[0] * hd->sm_count) : n0);
-    const auto *t0 = reinterpret_cast<const TileRec<C::SMAX> *>(tb + hd->t_off[0][part]);
-    if constexpr (NT == 4)
+    if constexpr (NT == 4) {
+      const auto *t0 = reinterpret_cast<const TileRec<Tile2Cfg<NT>::SMAX> *>(tb + hd->t_off[0][part]);
       k_tile2<NT, 0><<<grid, Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, t0, (int)n0, tt, hd->kp.mask);
-    else
+    } else {
+      const auto *t0 = reinterpret_cast<const TileRec<C::SMAX> *>(tb + hd->t_off[0][part]);
       k_tile<NT, 0><<<grid, 32, C::SMEM, st>>>(u, v, t0, (int)n0, tt, hd->kp.mask);
+    }
     CU(cudaGetLastError());
   }
   bool joined = false;

@@ -37,6 +37,9 @@
 #ifndef T1MINB
 #define T1MINB 1
 #endif
+#ifndef K1_TC
+#define K1_TC 32  // cells per k_tile2 tile (16 measured: structured 40 -> 42 us, apply 109 -> 150 us at C2)
+#endif
 
 // Tiles of TCELLS cells (a brick of the background grid) + their face-neighbour halo.
 template <int N, int TCELLS>
@@ -337,10 +340,12 @@ __global__ void __launch_bounds__(32, T1MINB) k_tile(const double *__restrict__ 
 // reads 8 different slots (16-byte reads, slot stride 33 x 16 B: conflict free).
 template <int N>
 struct Tile2Cfg {
+  // K1_TC cells per tile (32: a 2x4x4 brick, 2 warps; 16: 2x2x4, one warp), 2 threads per cell
+  using T = TileCfgX<N, K1_TC>;
   static constexpr int P = N / 2, NN = N * N, N3 = N * NN, NP = NN * P;
-  static constexpr int ST = TileCfg<N>::ST, SMAX = TileCfg<N>::SMAX;
-  static constexpr int SMEM = TileCfg<N>::SMEM;
-  static constexpr int THREADS = 64;
+  static constexpr int ST = T::ST, SMAX = T::SMAX;
+  static constexpr int SMEM = T::SMEM;
+  static constexpr int THREADS = 2 * K1_TC;
 };
 
 // x or y (D = 0, 1) terms of plane cc (pointers already at the plane)
