@@ -454,11 +454,13 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
           c.nb[f] = d.nb[f];
           if (d.nb[f] >= 0) nbm |= 1u << f;
         }
-        c.gp = 0;
+        // K1_GP (n = 4): the ghost penalty of cells next to cut cells rides in k_tile2
+        constexpr bool k1gp = N == 4 && K1_GP;
+        c.gp = k1gp ? (d.flags & nbm & 0x3fu) : 0u;
         c.sipg = nbm;  // faces of an uncut cell are inside the domain: full SIPG
         c.vol = true;
         set[0][pt - 1].push_back(c);
-        if (d.flags & nbm & 0x3fu) {
+        if (!k1gp && (d.flags & nbm & 0x3fu)) {
           c.gp = d.flags & nbm & 0x3fu;
           c.sipg = 0;
           c.vol = false;

@@ -37,6 +37,10 @@
 #ifndef T1MINB
 #define T1MINB 1
 #endif
+#ifndef K1_GP
+#define K1_GP 0  // k_tile2<4,0> adds the uncut cells' ghost penalty itself (no k_gpw for them);
+                 // measured: structured 40 -> 70 us at C2 (spills), so k_gpw stays
+#endif
 #ifndef K1_TC
 #define K1_TC 32  // cells per k_tile2 tile (16 measured: structured 40 -> 42 us, apply 109 -> 150 us at C2)
 #endif
@@ -555,11 +559,17 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
           z_line<N>(w, t, u0, a0, ev, el, act, tt);
           z_line<N>(w, t + 1, u1, a1, ev, el, act, tt);
         }
-      } else {
-        // ghost penalty + structured SIPG, face by face (skipped when no lane of the warp has it)
+      }
+    }
+    // ghost penalty (+ structured SIPG in MODE 1), face by face, skipped when no lane of
+    // the warp has it.  MODE 0 with K1_GP: the uncut cells' ghost penalty is added here
+    // from the tile already in shared memory (no separate k_gpw pass); every lane of the
+    // warp takes part (the votes), lanes without the face contribute zero.
+    if constexpr (MODE != 0 || K1_GP) {
+      {
         static_for<0, 6>([&](auto fc) {
           constexpr int F = decltype(fc)::value, D = F / 2, SS = F % 2;
-          const bool g = (gpb >> F) & 1u, sp = (spb >> F) & 1u;
+          const bool g = (gpb >> F) & 1u, sp = MODE != 0 && ((spb >> F) & 1u);
           const bool anyg = __any_sync(0xffffffffu, g), anys = __any_sync(0xffffffffu, sp);
           if (!(anyg || anys)) return;
           const double eg = g ? 1.0 : 0.0, es = sp ? 1.0 : 0.0;
