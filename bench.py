@@ -50,14 +50,49 @@ def workload_desc(P, cfg):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clocks / throttle reasons sampled DURING the timed region: in-process NVML
+    polling (cheap queries, no process start-up on the box while timing), else an
+    `nvidia-smi -lms 100` subprocess."""
 
     def __init__(self, uuid: str | None):
         self.uuid = uuid
         self.proc = None
         self.lines = []
+        self.kind = None
+        self._stop = threading.Event()
+
+    def _nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        if self.uuid:
+            h = pynvml.nvmlDeviceGetHandleByUUID(self.uuid)
+        else:
+            h = pynvml.nvmlDeviceGetHandleByIndex(0)
+        get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+        def poll():
+            while not self._stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    bits = get_reasons(h)
+                    self.lines.append(f"{sm}, {mx}, {pw}, {hex(bits)}")
+                except Exception:
+                    pass
+                self._stop.wait(0.02)
+        self.th = threading.Thread(target=poll, daemon=True)
+        self.th.start()
+        self.kind = "nvml"
 
     def __enter__(self):
+        try:
+            self._nvml()
+            time.sleep(0.05)
+            return self
+        except Exception:
+            pass
         cmd = ["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
                "--format=csv,noheader,nounits", "-lms", "100"]
         if self.uuid:
@@ -66,6 +101,7 @@ class ClockSampler:
             self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
+            self.kind = "nvidia-smi"
         except Exception:
             self.proc = None
         time.sleep(0.25)
@@ -76,6 +112,10 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if self.kind == "nvml":
+            time.sleep(0.03)
+            self._stop.set()
+            self.th.join(timeout=1)
         if self.proc:
             time.sleep(0.15)
             self.proc.terminate()
@@ -103,7 +143,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "sampler": self.kind}
 
 
 def load_peaks():
