@@ -478,7 +478,9 @@ struct CutPCfg {
   static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
   static constexpr int WARPS = CUTP_WARPS;
   static constexpr int NB = CUTP_NB;  // packet ring depth (NB-1 packets in flight while one is consumed)
-  static constexpr int PK = CUTP_PK;  // packet capacity in bytes (>= the largest chunk, 16 + 32 * 64)
+  static constexpr int PK = CUTP_PK;  // packet capacity in bytes (>= the largest chunk)
+  // largest chunks: 32 interface rows (64 B), 32 volume lines with their interface point
+  static_assert(PK >= 16 + 32 * 64 && PK >= 16 + 32 * 8 * (2 + 2 * N + 6), "CUTP_PK below the largest chunk");
   static constexpr int NN = N * N, N3 = N * N * N, N3P = (N3 + 1) & ~1;
   static constexpr int ACC = N == 4 ? 64 : (N == 3 ? 32 : 8);  // padded n^3 (power of two)
   // one chunk stream per cell mixing volume, interface and cut-face points (any face
