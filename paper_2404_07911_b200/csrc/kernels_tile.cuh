@@ -37,6 +37,10 @@
 #ifndef T1MINB
 #define T1MINB 1
 #endif
+#ifndef TILE8_SMAX
+#define TILE8_SMAX 36  // slots of an 8-cell tile (a full 2x2x2 brick needs 32; merged partial bricks
+                       // more; 32 measured: k_uncw<6> 3 CTAs/SM instead of 2, same time)
+#endif
 #ifndef K1_GP
 #define K1_GP 0  // k_tile2<4,0> adds the uncut cells' ghost penalty itself (no k_gpw for them);
                  // measured: structured 40 -> 70 us at C2 (spills), so k_gpw stays
@@ -55,7 +59,7 @@ struct TileCfgX {
   static constexpr int TC = TCELLS;  // cells per tile
   // slots per tile: the brick + its face halo (2x4x4: 32 + 64, 2x2x4: 16 + 40,
   // 2x2x2: 8 + 24, 1x2x2: 4 + 16)
-  static constexpr int SMAX = TC == 32 ? (N <= 3 ? 128 : 100) : (TC == 16 ? 60 : (TC == 8 ? 36 : 20));
+  static constexpr int SMAX = TC == 32 ? (N <= 3 ? 128 : 100) : (TC == 16 ? 60 : (TC == 8 ? TILE8_SMAX : 20));
   static constexpr int SMEM = 16 + SMAX * ST * 8;
   static constexpr int BX = TC == 4 ? 1 : 2, BY = TC == 32 ? 4 : 2, BZ = (TC == 8 || TC == 4) ? 2 : 4;
 };
