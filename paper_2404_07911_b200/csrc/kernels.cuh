@@ -1418,28 +1418,44 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
         }
         __syncthreads();
       }
-      if (tid < NN) {
-        FC1[tid] = f1;
-        FC2[tid] = f2;
-      }
-      __syncthreads();
-    }
-    for (int t = tid; t < NN; t += TH) {
-      int b0, st;
-      B::line(dd, t, b0, st);
-      if (structured) {
+      if constexpr (C::WFACE) {
+        // thread t accumulated line t's coefficients itself (NN <= THREADS): apply them
+        // directly (no FC round trip; lines of one axis are disjoint)
+        if (tid < NN) {
+          int b0, st;
+          B::line(dd, tid, b0, st);
 #pragma unroll
-        for (int m = 0; m < N; ++m) Rb[b0 + m * st] += T[b0 + m * st];
-      }
-      if (sc) {
-        const double fa = FC1[t], fb = FC2[t];
-#pragma unroll
-        for (int m = 0; m < N; ++m) Rb[b0 + m * st] = fma(dow[m], fb, Rb[b0 + m * st]);
-        Rb[b0 + fo * st] += fa;
+          for (int m = 0; m < N; ++m) Rb[b0 + m * st] = fma(dow[m], f2, Rb[b0 + m * st]);
+          Rb[b0 + fo * st] += f1;
+        }
+      } else {
+        if (tid < NN) {
+          FC1[tid] = f1;
+          FC2[tid] = f2;
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
+    if constexpr (!C::WFACE) {
+      for (int t = tid; t < NN; t += TH) {
+        int b0, st;
+        B::line(dd, t, b0, st);
+        if (structured) {
+#pragma unroll
+          for (int m = 0; m < N; ++m) Rb[b0 + m * st] += T[b0 + m * st];
+        }
+        if (sc) {
+          const double fa = FC1[t], fb = FC2[t];
+#pragma unroll
+          for (int m = 0; m < N; ++m) Rb[b0 + m * st] = fma(dow[m], fb, Rb[b0 + m * st]);
+          Rb[b0 + fo * st] += fa;
+        }
+      }
+    }
+    // (w-space path: the next face's Rb updates come after its own trace barrier)
+    if constexpr (!C::WFACE) __syncthreads();
   }
+  if constexpr (C::WFACE) __syncthreads();  // every Rb update done
   double *vb = v + (size_t)dsc.blk * N3;
   for (int l = tid; l < N3; l += TH) vb[l] = Rb[B::pad(l)];
 }
