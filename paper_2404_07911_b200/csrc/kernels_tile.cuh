@@ -41,6 +41,9 @@
 #define TILE8_SMAX 36  // slots of an 8-cell tile (a full 2x2x2 brick needs 32; merged partial bricks
                        // more; 32 measured: k_uncw<6> 3 CTAs/SM instead of 2, same time)
 #endif
+#ifndef GPW_TC4
+#define GPW_TC4 8  // cells per k_gpw tile at n = 4 (4 measured neutral at C2)
+#endif
 #ifndef K1_GP
 #define K1_GP 0  // k_tile2<4,0> adds the uncut cells' ghost penalty itself (no k_gpw for them);
                  // measured: structured 40 -> 70 us at C2 (spills), so k_gpw stays
@@ -701,7 +704,7 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
 template <int N>
 struct GpwCfg {
   // small tiles: ~one tile per CTA is in flight, so shorter tiles mean a shorter kernel
-  static constexpr int TC = N == 4 ? 8 : (N == 3 ? 16 : 32);
+  static constexpr int TC = N == 4 ? GPW_TC4 : (N == 3 ? 16 : 32);
   using T = TileCfgX<N, TC>;
   static constexpr bool BULK = T::BULK;
   static constexpr int N3 = N * N * N, ST = T::ST, SMAX = T::SMAX;
