@@ -989,7 +989,7 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
     // p = 1, 2: one thread per uncut cell (plain cells, then the cells next to cut cells)
     const int64_t np = hd->r_cnt[part][0], ng = hd->r_cnt[part][1];
     if (np + ng > 0) {
-      k_cell<NT><<<(unsigned)((np + ng + 127) / 128), 128, 0, st>>>(
+      k_cell<NT><<<(unsigned)(((np + ng) * CELL_TPC + 127) / 128), 128, 0, st>>>(
           u, v, hd->d_udesc + hd->r_off[part][0], (int)np, hd->d_udesc + hd->r_off[part][1], (int)ng, tt,
           hd->kp.mask);
       CU(cudaGetLastError());

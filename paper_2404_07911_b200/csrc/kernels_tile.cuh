@@ -1072,6 +1072,9 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
 // neighbour block in registers and applies the same w-space operators as
 // k_tile / k_uncw (M^{-1}-premultiplied line operators, then M (x) M (x) M).
 // Cells: desc0[0, n0) then desc1[0, n1) (plain cells, cells next to cut cells).
+#ifndef CELL_TPC
+#define CELL_TPC 1  // threads per uncut cell in k_cell (1 or 2; 2 measured slower: p=1 80 -> 90 us)
+#endif
 #ifndef CELL_G2
 #define CELL_G2 1  // measured: grouping the neighbour loads costs more occupancy than it hides
 #endif
@@ -1099,10 +1102,14 @@ __global__ void __launch_bounds__(128) k_cell(const double *__restrict__ u, doub
                                               const UDesc *__restrict__ desc0, int n0,
                                               const UDesc *__restrict__ desc1, int n1, TileTab<N> tt,
                                               uint32_t mask) {
-  constexpr int NN = N * N, N3 = NN * N;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n0 + n1) return;
-  const UDesc d = i < n0 ? desc0[i] : desc1[i - n0];
+  constexpr int NN = N * N, N3 = NN * N, TPC = CELL_TPC;
+  // CELL_TPC = 2: a cell on a thread pair, faces 0-2 / 3-5 (halving each thread's chain of
+  // dependent neighbour loads), w summed by one __shfl_xor per value
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, i = gt / TPC, part = gt % TPC;
+  if (TPC == 1 && i >= n0 + n1) return;
+  const bool valid = i < n0 + n1;  // (TPC = 2: every thread stays for the shuffles)
+  const int ic = valid ? i : 0;
+  const UDesc d = ic < n0 ? desc0[ic] : desc1[ic - n0];
   const bool cell_on = (mask & TERM_CELL) != 0, sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
   double uo[N3], w[N3];
   load_block<N>(u + (size_t)d.blk * N3, uo);
@@ -1112,6 +1119,7 @@ __global__ void __launch_bounds__(128) k_cell(const double *__restrict__ u, doub
   if (cell_on) {
     static_for<0, 3>([&](auto dc) {
       constexpr int D = decltype(dc)::value;
+      if (TPC == 2 && (D == 2) != (part == 1)) return;  // pair: axes 0, 1 / axis 2
 #pragma unroll
       for (int t = 0; t < NN; ++t)
 #pragma unroll
@@ -1143,6 +1151,7 @@ __global__ void __launch_bounds__(128) k_cell(const double *__restrict__ u, doub
   };
   static_for<0, 6>([&](auto fc) {
     constexpr int F = decltype(fc)::value, D = F / 2, SS = F % 2;
+    if (TPC == 2 && (F >= 3) != (part == 1)) return;  // pair: faces 0-2 / 3-5
     if constexpr (F % G == 0) load_group(F);
     bool sp, g;
     if (!face_need(F, sp, g)) return;
@@ -1192,6 +1201,10 @@ __global__ void __launch_bounds__(128) k_cell(const double *__restrict__ u, doub
       for (int m = 0; m < N; ++m) w[lix<N, D>(t, m)] += out[m];
     }
   });
+  if constexpr (TPC == 2) {
+#pragma unroll
+    for (int l = 0; l < N3; ++l) w[l] += __shfl_xor_sync(0xffffffffu, w[l], 1);
+  }
   // v = (M (x) M (x) M) w
   static_for<0, 3>([&](auto dc) {
     constexpr int D = decltype(dc)::value;
@@ -1209,12 +1222,16 @@ __global__ void __launch_bounds__(128) k_cell(const double *__restrict__ u, doub
       }
     }
   });
+  if (!valid) return;
   double *vb = v + (size_t)d.blk * N3;
+  constexpr int H = TPC == 2 ? ((N3 / 2 + 1) & ~1) : N3;  // the pair splits the store (even cut)
   if constexpr ((N3 % 2) == 0) {
 #pragma unroll
-    for (int k = 0; k < N3; k += 2) *reinterpret_cast<double2 *>(vb + k) = make_double2(w[k], w[k + 1]);
+    for (int k = 0; k < N3; k += 2)
+      if (TPC == 1 || (k < H) == (part == 0)) *reinterpret_cast<double2 *>(vb + k) = make_double2(w[k], w[k + 1]);
   } else {
 #pragma unroll
-    for (int k = 0; k < N3; ++k) vb[k] = w[k];
+    for (int k = 0; k < N3; ++k)
+      if (TPC == 1 || (k < H) == (part == 0)) vb[k] = w[k];
   }
 }
