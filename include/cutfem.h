@@ -105,7 +105,9 @@ typedef struct {
 int cutfem_setup(const cutfem_problem *pb, int device, cutfem_handle **out);
 
 /* v = A u.  u_dev, v_dev: DEVICE pointers to n_active*(p+1)^3 doubles
- * (caller-owned, 8-byte aligned, must not alias).  v is fully overwritten.
+ * (caller-owned, 16-byte aligned -- blocks move by bulk copies and 16-byte
+ * vector accesses; a misaligned pointer returns CUTFEM_EINVAL -- and must not
+ * alias).  v is fully overwritten.
  * Stream-ordered on `cuda_stream` (a cudaStream_t, NULL = legacy default);
  * no host synchronisation.  One apply in flight per handle. */
 int cutfem_apply(cutfem_handle *hd, const double *u_dev, double *v_dev, void *cuda_stream);
@@ -118,7 +120,9 @@ int cutfem_apply(cutfem_handle *hd, const double *u_dev, double *v_dev, void *cu
 int cutfem_apply_kernel(cutfem_handle *hd, int which, const double *u_dev, double *v_dev, void *cuda_stream);
 
 /* Same operator with HOST buffers: copies u host->device, applies, copies
- * v device->host, synchronises the stream (the end-to-end path). */
+ * v device->host, synchronises the stream (the end-to-end path).  u_host: the
+ * n_dofs owned values; the library's device copy of u has room for the ghost
+ * blocks of a distributed handle (n_ext_dofs), which the halo exchange fills. */
 int cutfem_apply_host(cutfem_handle *hd, const double *u_host, double *v_host, void *cuda_stream);
 
 /* Sparse-matrix comparison path (P:224-227 eq:matrixbasedop).
@@ -181,6 +185,7 @@ int cutfem_dist_info(const cutfem_handle *hd, int64_t *n_own_blocks, int64_t *n_
  * cutfem_cg: unpreconditioned conjugate gradients on A x = b (the iterative
  * solver the operator evaluation serves), x0 = x_dev (in/out, the
  * owned blocks; a distributed handle needs room for the ghost blocks too).
+ * b_dev and x_dev must be 16-byte aligned and must not alias (CUTFEM_EINVAL).
  * Runs exactly `iters` iterations, or stops early once ||r|| <= tol ||b|| when
  * tol > 0.  All vector work (dots, axpys) runs in the library's kernels with the
  * CG scalars kept on the device; dot products are reduced deterministically

@@ -24,8 +24,9 @@ __device__ __forceinline__ double block_sum(double x, double *sh) {
   return sh[0];
 }
 
-// partial[b] = sum over this block's grid-stride range of a_i * b_i (n even: every
-// block has n^3 >= 8 entries; 16-byte accesses)
+// partial[b] = sum over this block's grid-stride range of a_i * b_i (16-byte
+// accesses over the pairs; an odd n -- odd p with an odd cell count -- leaves one
+// tail entry, added by thread 0 of block 0)
 __global__ void __launch_bounds__(CG_THREADS) k_dot(const double *__restrict__ a, const double *__restrict__ b,
                                                     int64_t n, double *__restrict__ partial) {
   __shared__ double sh[CG_THREADS];
@@ -35,6 +36,7 @@ __global__ void __launch_bounds__(CG_THREADS) k_dot(const double *__restrict__ a
     const double2 x = a2[i], y = b2[i];
     s = fma(x.x, y.x, fma(x.y, y.y, s));
   }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) s = fma(a[n - 1], b[n - 1], s);
   s = block_sum(s, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
@@ -66,6 +68,12 @@ __global__ void __launch_bounds__(CG_THREADS) k_cg_xr(double *__restrict__ x, do
     r2[i] = ri;
     s = fma(ri.x, ri.x, fma(ri.y, ri.y, s));
   }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd n: the tail entry
+    x[n - 1] = fma(alpha, p[n - 1], x[n - 1]);
+    const double rt = fma(-alpha, q[n - 1], r[n - 1]);
+    r[n - 1] = rt;
+    s = fma(rt, rt, s);
+  }
   s = block_sum(s, sh);
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
@@ -80,6 +88,7 @@ __global__ void __launch_bounds__(CG_THREADS) k_cg_p(double *__restrict__ p, con
     const double2 pi = p2[i], ri = r2[i];
     p2[i] = make_double2(fma(beta, pi.x, ri.x), fma(beta, pi.y, ri.y));
   }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = fma(beta, p[n - 1], r[n - 1]);
 }
 
 // r = b - q, p = r, partial sums of |r|^2
@@ -228,6 +237,8 @@ int cutfem_cg(cutfem_handle *hd, const double *b_dev, double *x_dev, int iters, 
   if (!hd) return fail(CUTFEM_EINVAL, "null handle");
   if (iters < 0) return fail(CUTFEM_EINVAL, "iters < 0");
   if (hd->stats.n_dofs > 0 && (!b_dev || !x_dev)) return fail(CUTFEM_EINVAL, "null vector");
+  if (((uintptr_t)b_dev | (uintptr_t)x_dev) & 15) return fail(CUTFEM_EINVAL, "vectors must be 16-byte aligned");
+  if (b_dev == x_dev && hd->stats.n_dofs > 0) return fail(CUTFEM_EINVAL, "b and x must not alias");
   CU(cudaSetDevice(hd->device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const int64_t n = hd->stats.n_dofs, next = hd->stats.n_ext_dofs;

@@ -70,8 +70,6 @@ struct cutfem_handle {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_comm = nullptr, ev_comm_fork = nullptr;
   int sm_count = 148;
-  int occ_plain = 1, occ_gen = 1;  // resident CTAs per SM of the persistent structured kernels
-  int occ_cut = 1;                 // ... and of the persistent unstructured kernel
   uint32_t mask = CUTFEM_TERM_ALL;
   KParams kp;
   FaceTab ft;
@@ -82,23 +80,12 @@ struct cutfem_handle {
   void *d_tiles = nullptr;
   int64_t t_off[3][3] = {{0}}, t_cnt[3][3] = {{0}};
   int occ_tile[3] = {1, 1, 1};
-  bool cut_last = false;  // launch k_cutp after the uncut-cell kernels (env CUTFEM_CUT_LAST)
-  int persist = 1;  // tile kernels: persistent grid (1) or one tile per CTA (0); env CUTFEM_TILE_PERSIST
   std::vector<char> ttab;  // TileTab<N> bytes
   CDesc2 *d_cdesc2 = nullptr;  // k_cutp: cut cells grouped per warp (LPT), their cut-face points
   double *d_fac = nullptr;
   int *d_wstart = nullptr;      // per part: warp -> first cell (grid_cutp[part] * WARPS + 1 entries)
   int *d_kstart = nullptr;      // per part: warp -> first packet
   CPacket *d_chunks = nullptr;  // packets of the point-chunk stream, per warp in consumption order
-  bool uncw_first = false;      // n = 5, 6: k_uncw launched before k_cut
-  bool gpw_cut = false;         // p <= 3: the cut cells' structured faces in k_gpw (after k_cutp)
-  bool cellk = true;            // p = 1, 2: uncut cells through k_cell (env CUTFEM_NO_CELLK: k_tile + k_gpw)
-  int uncw_ctas = 0;            // n = 5, 6: k_uncw CTAs per SM (0: occupancy)
-  int uncw_hi = 1 << 8;         // bit n (7..9): uncut cells through k_uncw (env CUTFEM_UNCW_HI=mask)
-  bool vlines = true;           // k_cutp: volume points in lines where they form lines (env CUTFEM_NO_VLINES)
-  bool slines = true;           // k_cutp: interface points on the volume lines (env CUTFEM_NO_SLINES)
-  bool flines = false;          // k_cutp: cut-face points in lines (env CUTFEM_FLINES=1; measured slower:
-                                // ~10 face lines per cell over 3 normal axes leave most lanes idle)
   char *d_stream = nullptr;     // the packed stream (chunk headers + point rows)
   int64_t w_off[3] = {0};
   int grid_cutp[3] = {0};
@@ -479,9 +466,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       c.gp = d.flags & nbm & 0x3fu;
       c.sipg = (d.flags >> 6) & nbm & 0x3fu;  // structured (full, uncut) faces of the cut cell
       c.vol = false;
-      // cut cells: their structured faces go to k_gpw (after k_cutp) when gpw_cut,
-      // else k_cutp does them
-      if (hd->gpw_cut && (c.gp | c.sipg)) set[1][pt - 1].push_back(c);
+      // (cut cells: k_cutp does their structured faces itself)
     }
   }
   // set 0: k_tile* tiles (TileCfg<N>; k_tile2 at n = 4: Tile2Cfg<4>::T); set 1: k_gpw
@@ -489,7 +474,8 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
   using CG = typename GpwCfg<N>::T;
   using CK = typename std::conditional<N == 4, typename Tile2Cfg<4>::T, C>::type;
   std::vector<char> all;
-  for (int k = 0; k < 2; ++k) {
+  // (n <= 3: the uncut cells run k_cell from their descriptors; no tiles)
+  for (int k = 0; k < (N == 4 ? 2 : 0); ++k) {
     const int64_t rs = k == 0 ? (int64_t)sizeof(TileRec<CK::SMAX>) : (int64_t)sizeof(TileRec<CG::SMAX>);
     std::vector<char> b0, b1;
     if (k == 0) {
@@ -514,8 +500,6 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     // coordinates [xi, eta, zeta, W] (normal coordinate exactly 0 or 1)
     std::vector<CDesc2> c2(cd.size());
     std::vector<double> fac;
-    std::vector<std::array<int32_t, 3>> fax(cd.size(), std::array<int32_t, 3>{0, 0, 0});  // face points per axis
-    std::vector<std::array<int32_t, 6>> fcn(cd.size(), std::array<int32_t, 6>{0, 0, 0, 0, 0, 0});  // per face
     for (size_t i = 0; i < cd.size(); ++i) {
       const CDesc &d = cd[i];
       CDesc2 &e = c2[i];
@@ -528,7 +512,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       e.fb = (int64_t)fac.size() / 4;
       for (int f = 0; f < 6; ++f) {
         e.nb[f] = d.nb[f] >= 0 ? d.nb[f] : -1;
-        if (d.nb[f] >= 0 && !hd->gpw_cut) {
+        if (d.nb[f] >= 0) {
           if (d.flags & (1u << f)) e.smask |= 1u << f;               // ghost penalty (the cell is cut)
           if (d.flags & (1u << (6 + f))) e.smask |= 1u << (8 + f);   // full face inside Omega: SIPG
         }
@@ -545,60 +529,11 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         }
       }
       e.nf = (int32_t)((int64_t)fac.size() / 4 - e.fb);
-      for (int f = 0; f < 6; ++f)
-        if ((e.fmask >> f) & 1u) {
-          fcn[i][f] = (int32_t)(pb->sf_ptr[d.sf[f] + 1] - pb->sf_ptr[d.sf[f]]);
-          fax[i][f >> 1] += fcn[i][f];
-        }
-    }
-    // cut-face points in LINES (2-D dimension reduction on the face): per cell, every face's
-    // points in groups of N consecutive rows with the normal coordinate and one in-face
-    // coordinate shared exactly; fl_s / fl_m hold the fixed coordinate and sd + 2 tl per
-    // line, keyed by the line's first row
-    std::vector<char> fline(cd.size(), 0);
-    std::vector<double> fl_s(fac.size() / 4, 0.0), fl_m(fac.size() / 4, 0.0);
-    for (size_t i = 0; i < cd.size() && hd->flines; ++i) {
-      const CDesc2 &e = c2[i];
-      if (e.nf <= 0) continue;
-      bool ok = true;
-      int64_t row = e.fb;
-      for (int f = 0; f < 6 && ok; ++f) {
-        const int cnt = fcn[i][f];
-        if (cnt == 0) continue;
-        if (cnt % N != 0) {
-          ok = false;
-          break;
-        }
-        const int dd = f >> 1, e1 = dd == 0 ? 1 : 0, e2 = dd == 2 ? 1 : 2;
-        for (int g = 0; g < cnt && ok; g += N) {
-          const double *a = &fac[4 * (row + g)];
-          int var = -1;
-          for (int t = 1; t < N; ++t) {
-            const double *b = &fac[4 * (row + g + t)];
-            const bool s1 = a[e1] == b[e1], s2 = a[e2] == b[e2];
-            const int v = (s1 && !s2) ? e2 : ((s2 && !s1) ? e1 : -1);
-            if (v < 0 || (var >= 0 && v != var) || a[dd] != b[dd]) {
-              ok = false;
-              break;
-            }
-            var = v;
-          }
-          if (!ok) break;
-          const int tl = var == e2 ? 1 : 0;
-          fl_s[row + g] = tl ? a[e1] : a[e2];
-          fl_m[row + g] = (double)((f & 1) + 2 * tl);
-        }
-        row += cnt;
-      }
-      fline[i] = ok ? 1 : 0;
     }
     CU(cudaFuncSetAttribute(k_cutp<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutPCfg<N>::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_cutp, k_cutp<N>, 32 * CutPCfg<N>::WARPS,
                                                      CutPCfg<N>::SMEM));
     hd->occ_cutp = std::max(1, hd->occ_cutp);
-    // CTAs of k_cutp per SM (env CUTFEM_CUTP_CTAS): fewer leaves room for the
-    // concurrent uncut-cell kernel on every SM
-    if (const char *e = std::getenv("CUTFEM_CUTP_CTAS")) hd->occ_cutp = std::max(1, std::min(hd->occ_cutp, std::atoi(e)));
     // per part: longest-processing-time assignment of the cells to the warps of
     // the launch (cost ~ point chunks + a fixed per-cell part), cells of a warp
     // stored contiguously, heaviest first
@@ -618,11 +553,11 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       std::vector<char> isline(c2.size(), 0);
       for (int64_t i = 0; i < n; ++i) {
         const CDesc2 &e = c2[o + i];
-        isline[o + i] = hd->vlines && N >= 3 && e.nv > 0 && vol_line_axis(pb->vol_pts + 4 * e.vb, e.nv, N) >= 0;
+        isline[o + i] = N >= 3 && e.nv > 0 && vol_line_axis(pb->vol_pts + 4 * e.vb, e.nv, N) >= 0;
       }
       auto cost = [&](const CDesc2 &e) {
         const int64_t i = &e - c2.data();
-        const int nf = fline[i] ? e.nf / 2 : e.nf;  // face lines cost about half a point chunk per 32 points
+        const int nf = e.nf;
         if (isline[i]) return 2.8 * ((e.nv / N + 31) / 32) + (double)((e.ns + nf + 31) / 32) + 1.5;
         return (double)((e.nv + e.ns + nf + 31) / 32) + 1.5;
       };
@@ -654,13 +589,13 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
           const size_t k0 = chunk.size();
           // volume points in lines: chunks of <= 32 lines (sign bit, axis << 24), then the
           // cell's other points as below with no volume points left
-          const int lax = (hd->vlines && N >= 3 && nv > 0) ? vol_line_axis(pb->vol_pts + 4 * e.vb, nv, N) : -1;
+          const int lax = (N >= 3 && nv > 0) ? vol_line_axis(pb->vol_pts + 4 * e.vb, nv, N) : -1;
           int nlc = 0;  // line chunks of the cell (packed into nchunk's high half)
           if (lax >= 0) {
             const int nl = nv / N;
             // the interface points ride on the lines when they all sit on distinct lines
             // (needs both the cell and the Nitsche term: a record carries both)
-            const bool son = ns > 0 && nv > 0 && hd->slines &&
+            const bool son = ns > 0 && nv > 0 &&
                              !srf_on_lines(pb->vol_pts + 4 * e.vb, nv, pb->srf_pts + 7 * e.sb, ns, N, lax).empty();
             for (int l0 = 0; l0 < nl; l0 += 32) {
               CChunk r;
@@ -675,26 +610,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
             nv = 0;
             if (son) ns = 0;
           }
-          // cut-face lines, normal axis by axis (faces 2D, 2D+1 are consecutive rows)
-          int nfc = 0;
-          bool fdone = false;
-          if (N >= 3 && fon && fline[i]) {
-            int64_t row = e.fb;
-            for (int dd = 0; dd < 3; ++dd) {
-              const int nl = (fcn[i][2 * dd] + fcn[i][2 * dd + 1]) / N;
-              for (int l0 = 0; l0 < nl; l0 += 32) {
-                CChunk r;
-                r.vo = (int32_t)e.vb;
-                r.so = (int32_t)e.sb;
-                r.fo = (int32_t)(row + (int64_t)l0 * N);
-                r.cnt = (int32_t)((1u << 30) | ((uint32_t)dd << 24) | (uint32_t)std::min(32, nl - l0));
-                chunk.push_back(r);
-                ++nfc;
-              }
-              row += (int64_t)nl * N;
-            }
-            fdone = true;
-          }
+          const bool fdone = false;
           if constexpr (CutPCfg<N>::UNIFIED) {
             // one stream: volume, interface, cut-face points (any axis) in chunks of 32
             const int nf = (fon && !fdone) ? e.nf : 0;
@@ -721,7 +637,8 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
               chunk.push_back(r);
             }
             int64_t fo = e.fb;
-            if (CutPCfg<N>::FMIX && fon && !fdone) {  // every face axis in one stream
+            (void)fo;
+            if (fon && !fdone) {  // every face axis in one stream (runtime-axis update)
               for (int q0 = 0; q0 < e.nf; q0 += 32) {
                 CChunk r;
                 r.vo = (int32_t)e.vb;
@@ -730,24 +647,11 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
                 r.cnt = std::min(32, e.nf - q0) << 16;
                 chunk.push_back(r);
               }
-              fdone = true;
-            }
-            for (int ax = 0; ax < 3 && fon && !fdone; ++ax) {
-              const int na = fax[i][ax];
-              for (int q0 = 0; q0 < na; q0 += 32) {
-                CChunk r;
-                r.vo = (int32_t)e.vb;
-                r.so = (int32_t)e.sb;
-                r.fo = (int32_t)(fo + q0);
-                r.cnt = std::min(32, na - q0) << 16;
-                chunk.push_back(r);
-              }
-              fo += na;
             }
           }
-          if (chunk.size() - k0 > 0xffff || nlc > 0xff || nfc > 0xff)
+          if (chunk.size() - k0 > 0xffff || nlc > 0xff)
             return fail(CUTFEM_EUNSUPPORTED, "k_cutp: too many point chunks in a cell");
-          c2o[pos - 1].nchunk = (int32_t)((uint32_t)(chunk.size() - k0) | ((uint32_t)nlc << 16) | ((uint32_t)nfc << 24));
+          c2o[pos - 1].nchunk = (int32_t)((uint32_t)(chunk.size() - k0) | ((uint32_t)nlc << 16));
         }
       }
       ws.push_back((int)(pos - o));
@@ -770,31 +674,6 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       CPacket cur = {(int64_t)strm.size() * 8, 0, 0};
       for (int k = ks[w]; k < ks[w + 1]; ++k) {
         const CChunk &r = chunk[k];
-        const bool fln = r.cnt >= 0 && ((r.cnt >> 30) & 1);  // cut-face lines
-        if (fln) {
-          const int nl = r.cnt & 0xff, dd = (r.cnt >> 24) & 3, e1 = dd == 0 ? 1 : 0, e2 = dd == 2 ? 1 : 2;
-          const int fbytes = 16 + (16 + 16 * N) * nl;
-          if (cur.nch > 0 && cur.bytes + fbytes > CutPCfg<N>::PK) {
-            pk.push_back(cur);
-            cur = {(int64_t)strm.size() * 8, 0, 0};
-          }
-          double hdr[2] = {0.0, 0.0};
-          std::memcpy(hdr, &r.cnt, sizeof(int32_t));
-          strm.insert(strm.end(), hdr, hdr + 2);
-          for (int l = 0; l < nl; ++l) {
-            const int64_t row = r.fo + (int64_t)l * N;
-            const int tl = ((int)fl_m[row]) >> 1;
-            strm.push_back(fl_s[row]);
-            strm.push_back(fl_m[row]);
-            for (int t = 0; t < N; ++t) {
-              strm.push_back(fac[4 * (row + t) + (tl ? e2 : e1)]);
-              strm.push_back(fac[4 * (row + t) + 3]);
-            }
-          }
-          cur.bytes += fbytes;
-          ++cur.nch;
-          continue;
-        }
         const bool line = r.cnt < 0, lsrf = line && ((r.cnt >> 29) & 1);
         const int cv = r.cnt & 0xff, cs = line ? 0 : (r.cnt >> 8) & 0xff, cf = line ? 0 : (r.cnt >> 16) & 0xff;
         const int bytes = line ? 16 + (16 + 16 * N + (lsrf ? 48 : 0)) * cv : 16 + 32 * cv + 64 * cs + 32 * cf;
@@ -879,13 +758,10 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     using C2 = Tile2Cfg<N>;
     CU(cudaFuncSetAttribute(k_tile2<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_tile2<N, 0>, C2::THREADS, C2::SMEM));
-  } else {
-    CU(cudaFuncSetAttribute(k_tile<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_tile<N, 0>, 32, C::SMEM));
+    CU(cudaFuncSetAttribute(k_gpw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, GpwCfg<N>::SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_gpw<N>, GpwCfg<N>::THREADS,
+                                                     GpwCfg<N>::SMEM));
   }
-  CU(cudaFuncSetAttribute(k_gpw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, GpwCfg<N>::SMEM));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_gpw<N>, GpwCfg<N>::THREADS,
-                                                   GpwCfg<N>::SMEM));
   for (int k = 0; k < 3; ++k) hd->occ_tile[k] = std::max(1, hd->occ_tile[k]);
   return 0;
 }
@@ -941,11 +817,9 @@ int dispatch_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vecto
     case 4: return setup_tiles<4>(hd, pb, ud, cd);
     case 5: return setup_uncw<5>(hd, pb, ud);
     case 6: return setup_uncw<6>(hd, pb, ud);
-    // n = 7..9: k_uncw where measured faster than k_uncut (bit n of uncw_hi; default n = 8:
-    // n = 7 neutral, n = 9 slower — 140 KB of tile data, one CTA per SM)
-    case 7: return (hd->uncw_hi >> 7) & 1 ? setup_uncw<7>(hd, pb, ud) : 0;
-    case 8: return (hd->uncw_hi >> 8) & 1 ? setup_uncw<8>(hd, pb, ud) : 0;
-    case 9: return (hd->uncw_hi >> 9) & 1 ? setup_uncw<9>(hd, pb, ud) : 0;
+    // n = 8: k_uncw (measured faster than k_uncut); n = 7 (neutral) and n = 9 (slower:
+    // 140 KB of tile data, one CTA per SM) stay on k_uncut
+    case 8: return setup_uncw<8>(hd, pb, ud);
   }
   return 0;
 }
@@ -961,7 +835,6 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
   const int64_t n0 = (which & 1) ? hd->t_cnt[0][part] : 0;
   const int64_t n1 = ((which & 1) && (hd->kp.mask & (TERM_GP | TERM_SIPG))) ? hd->t_cnt[1][part] : 0;
   const bool fork = nc > 0 && n0 > 0;
-  const bool cut_last = hd->cut_last;
   if (fork) {
     CU(cudaEventRecord(hd->ev_fork, st));
     CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
@@ -982,55 +855,42 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
     return 0;
   };
   int rc;
-  if (!cut_last && (rc = launch_cut())) return rc;
+  if ((rc = launch_cut())) return rc;
   const TileTab<NT> &tt = *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data());
   const char *tb = reinterpret_cast<const char *>(hd->d_tiles);  // byte offsets per set
-  if constexpr (NT <= 3) if (hd->cellk && (which & 1)) {
+  if constexpr (NT <= 3) {
     // p = 1, 2: one thread per uncut cell (plain cells, then the cells next to cut cells)
     const int64_t np = hd->r_cnt[part][0], ng = hd->r_cnt[part][1];
-    if (np + ng > 0) {
+    if ((which & 1) && np + ng > 0) {
       k_cell<NT><<<(unsigned)(((np + ng) * CELL_TPC + 127) / 128), 128, 0, st>>>(
           u, v, hd->d_udesc + hd->r_off[part][0], (int)np, hd->d_udesc + hd->r_off[part][1], (int)ng, tt,
           hd->kp.mask);
       CU(cudaGetLastError());
     }
-    if (cut_last && (rc = launch_cut())) return rc;
     if (fork) {
       CU(cudaEventRecord(hd->ev_join, hd->side));
       CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
     }
     return 0;
-  }
+  } else {
   if (n0 > 0) {
-    const unsigned grid = (unsigned)(hd->persist & 1 ? std::min<int64_t>(n0, (int64_t)hd->occ_tile[0] * hd->sm_count) : n0);
-    if constexpr (NT == 4) {
-      const auto *t0 = reinterpret_cast<const TileRec<Tile2Cfg<NT>::SMAX> *>(tb + hd->t_off[0][part]);
-      k_tile2<NT, 0><<<grid, Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, t0, (int)n0, tt, hd->kp.mask);
-    } else {
-      const auto *t0 = reinterpret_cast<const TileRec<C::SMAX> *>(tb + hd->t_off[0][part]);
-      k_tile<NT, 0><<<grid, 32, C::SMEM, st>>>(u, v, t0, (int)n0, tt, hd->kp.mask);
-    }
+    const unsigned grid = (unsigned)std::min<int64_t>(n0, (int64_t)hd->occ_tile[0] * hd->sm_count);
+    const auto *t0 = reinterpret_cast<const TileRec<Tile2Cfg<NT>::SMAX> *>(tb + hd->t_off[0][part]);
+    k_tile2<NT, 0><<<grid, Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, t0, (int)n0, tt, hd->kp.mask);
     CU(cudaGetLastError());
   }
-  bool joined = false;
-  if (n1 > 0 && hd->gpw_cut && fork && !cut_last) {
-    // k_gpw adds to cut-cell blocks too: wait for k_cutp's v = ...
-    CU(cudaEventRecord(hd->ev_join, hd->side));
-    CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
-    joined = true;
-  }
-  if (n1 > 0) {  // uncut cells next to cut cells: + ghost penalty (needs only k_tile*<0>)
-    const unsigned grid = (unsigned)(hd->persist & 2 ? std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count) : n1);
+  if (n1 > 0) {  // uncut cells next to cut cells: + ghost penalty (after k_tile2's v = ...)
+    const unsigned grid = (unsigned)std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count);
     k_gpw<NT><<<grid, GpwCfg<NT>::THREADS, GpwCfg<NT>::SMEM, st>>>(
         u, v, reinterpret_cast<const TileRec<GpwCfg<NT>::SMAX> *>(tb + hd->t_off[1][part]), (int)n1, tt, hd->kp.mask);
     CU(cudaGetLastError());
   }
-  if (cut_last && (rc = launch_cut())) return rc;
-  if (fork && !joined) {
+  if (fork) {
     CU(cudaEventRecord(hd->ev_join, hd->side));
     CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
   }
   return 0;
+  }
 }
 
 // which: bit0 structured (uncut) kernels, bit1 unstructured (cut) kernel; part:
@@ -1038,7 +898,8 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
 // kinds, the cut kernel runs on the forked side stream, concurrently.
 template <int N>
 int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which = 3, int part = 0) {
-  if (N <= 4 && hd->d_tiles) return launch_tiles<N>(hd, u, v, st, which, part);
+  if constexpr (N <= 4) return launch_tiles<N>(hd, u, v, st, which, part);
+  else {
   const int64_t np = (which & 1) ? hd->r_cnt[part][0] : 0, ng = (which & 1) ? hd->r_cnt[part][1] : 0;
   const int64_t nc = (which & 2) ? hd->r_cnt[part][2] : 0;
   const UDesc *dp = hd->d_udesc + hd->r_off[part][0], *dg = hd->d_udesc + hd->r_off[part][1];
@@ -1046,14 +907,13 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
   const int64_t nu = np + ng;
   const bool fork = nc > 0 && nu > 0;
   cudaStream_t cs = fork ? hd->side : st;
-  // n = 5, 6: the persistent uncut kernel (k_uncw) may go first with a capped grid,
-  // leaving room on every SM for the cut-cell CTAs (env CUTFEM_UNCW_FIRST, CUTFEM_UNCW_CTAS)
+  // n = 5, 6, 8: the persistent uncut kernel (k_uncw), after the cut-cell kernel
   auto launch_uncw = [&]() -> int {
     if (!(nu > 0 && N >= 5 && hd->d_tiles)) return 0;
     constexpr int NU = N >= 5 ? N : 5;
     const int64_t nt = hd->t_cnt[0][part];
     if (nt > 0) {
-      const int occ = hd->uncw_ctas > 0 ? std::min(hd->uncw_ctas, hd->occ_tile[0]) : hd->occ_tile[0];
+      const int occ = hd->occ_tile[0];
       const unsigned grid = (unsigned)std::min<int64_t>(nt, (int64_t)occ * hd->sm_count);
       k_uncw<NU><<<grid, UncwCfg<NU>::THREADS, UncwCfg<NU>::SMEM, st>>>(
           u, v, reinterpret_cast<const TileRec<TileCfg<NU>::SMAX> *>(hd->d_tiles) + hd->t_off[0][part], (int)nt,
@@ -1066,55 +926,25 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
     CU(cudaEventRecord(hd->ev_fork, st));
     CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
   }
-  if (hd->uncw_first) launch_uncw();
   if (nc > 0) {
-    if (N <= 4) {
-      using CW = CutWCfg<(N <= 4 ? N : 4)>;
-      const unsigned grid = (unsigned)((nc + CW::WARPS - 1) / CW::WARPS);
-      k_cutw<(N <= 4 ? N : 4)><<<grid, 32 * CW::WARPS, CW::SMEM, cs>>>(
-          u, v, dc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp, hd->d_sfptr, hd->kp,
-          hd->ft);
-    } else {
+    {
       k_cut<N><<<(unsigned)nc, CutCfg<N>::THREADS, CutCfg<N>::SMEM, cs>>>(
           u, v, dc, (int)nc, hd->d_vol, hd->d_volptr, hd->d_srf, hd->d_srfptr, hd->d_sfp, hd->d_sfptr, hd->kp,
           hd->ft, *reinterpret_cast<const TileTab<N> *>(hd->ttab.data()), hd->d_line_srf);
     }
     CU(cudaGetLastError());
   }
-  if (nu > 0 && N >= 5 && hd->d_tiles) {
-    if (!hd->uncw_first) launch_uncw();
-  } else if (nu > 0) {
-    if (N <= 5) {
-      constexpr int NC = (N <= 5 ? N : 5);
-      using C = Uncut3Cfg<NC>;
-      const int per_block = C::WARPS * C::CPW;
-      const bool plain_ok = (hd->kp.mask & TERM_SIPG) != 0;
-      auto grid_for = [&](int64_t n, int occ) {
-        const int64_t need = (n + per_block - 1) / per_block;
-        return (unsigned)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)occ * hd->sm_count));
-      };
-      // plain cells run the branch-free path (needs SIPG on); the rest the general one
-      if (np > 0) {
-        if (plain_ok)
-          k_uncut3<NC, true><<<grid_for(np, hd->occ_plain), 32 * C::WARPS, C::SMEM, st>>>(u, v, dp, (int)np,
-                                                                                            hd->kp, hd->ft);
-        else
-          k_uncut3<NC, false><<<grid_for(np, hd->occ_gen), 32 * C::WARPS, C::SMEM, st>>>(u, v, dp, (int)np,
-                                                                                            hd->kp, hd->ft);
-      }
-      if (ng > 0)
-        k_uncut3<NC, false><<<grid_for(ng, hd->occ_gen), 32 * C::WARPS, C::SMEM, st>>>(u, v, dg, (int)ng, hd->kp,
-                                                                                          hd->ft);
-    } else {
-      using C = UncutCfg<N>;
-      const int per_block = C::WARPS * C::CPW;
-      if (np > 0)
-        k_uncut<N><<<(unsigned)((np + per_block - 1) / per_block), 32 * C::WARPS, C::SMEM, st>>>(u, v, dp, (int)np,
-                                                                                               hd->kp, hd->ft);
-      if (ng > 0)
-        k_uncut<N><<<(unsigned)((ng + per_block - 1) / per_block), 32 * C::WARPS, C::SMEM, st>>>(u, v, dg, (int)ng,
-                                                                                               hd->kp, hd->ft);
-    }
+  if (nu > 0 && hd->d_tiles) {
+    launch_uncw();  // n = 5, 6, 8
+  } else if (nu > 0) {  // n = 7, 9
+    using C = UncutCfg<N>;
+    const int per_block = C::WARPS * C::CPW;
+    if (np > 0)
+      k_uncut<N><<<(unsigned)((np + per_block - 1) / per_block), 32 * C::WARPS, C::SMEM, st>>>(u, v, dp, (int)np,
+                                                                                             hd->kp, hd->ft);
+    if (ng > 0)
+      k_uncut<N><<<(unsigned)((ng + per_block - 1) / per_block), 32 * C::WARPS, C::SMEM, st>>>(u, v, dg, (int)ng,
+                                                                                             hd->kp, hd->ft);
     CU(cudaGetLastError());
   }
   if (fork) {
@@ -1122,36 +952,15 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
     CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
   }
   return 0;
-}
-
-template <int N>
-int query_occ(cutfem_handle *hd) {
-  if (N <= 4) {
-    constexpr int NC = (N <= 4 ? N : 4);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_cut, k_cutw<NC>, 128, CutWCfg<NC>::SMEM));
-    hd->occ_cut = std::max(1, hd->occ_cut);
   }
-  if (N <= 5) {
-    constexpr int NC = (N <= 5 ? N : 5);
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_plain, k_uncut3<NC, true>, 128, Uncut3Cfg<NC>::SMEM));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_gen, k_uncut3<NC, false>, 128, Uncut3Cfg<NC>::SMEM));
-    hd->occ_plain = std::max(1, hd->occ_plain);
-    hd->occ_gen = std::max(1, hd->occ_gen);
-  }
-  return 0;
 }
 
 template <int N>
 int set_attrs() {
-  CU(cudaFuncSetAttribute(k_cut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutCfg<N>::SMEM));
-  if (N <= 4)
-    CU(cudaFuncSetAttribute(k_cutw<(N <= 4 ? N : 4)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            CutWCfg<(N <= 4 ? N : 4)>::SMEM));
-  CU(cudaFuncSetAttribute(k_uncut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncutCfg<N>::SMEM));
-  if (N <= 5) {
-    constexpr int NC = (N <= 5 ? N : 5);
-    CU(cudaFuncSetAttribute(k_uncut3<NC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Uncut3Cfg<NC>::SMEM));
-    CU(cudaFuncSetAttribute(k_uncut3<NC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Uncut3Cfg<NC>::SMEM));
+  if constexpr (N >= 5) {
+    CU(cudaFuncSetAttribute(k_cut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutCfg<N>::SMEM));
+    if constexpr (N == 7 || N == 9)
+      CU(cudaFuncSetAttribute(k_uncut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncutCfg<N>::SMEM));
   }
   return 0;
 }
@@ -1168,16 +977,6 @@ int dispatch_part(cutfem_handle *hd, const double *u, double *v, cudaStream_t st
     case 9: return launch<9>(hd, u, v, st, which, part);
   }
   return fail(CUTFEM_EUNSUPPORTED, "degree");
-}
-
-int dispatch_occ(cutfem_handle *hd) {
-  switch (hd->n) {
-    case 2: return query_occ<2>(hd);
-    case 3: return query_occ<3>(hd);
-    case 4: return query_occ<4>(hd);
-    case 5: return query_occ<5>(hd);
-    default: return 0;
-  }
 }
 
 int halo_exchange(cutfem_handle *hd, const double *u_ext, cudaStream_t st);  // dist.inl
@@ -1398,13 +1197,11 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
       }
       // k_cut (n >= 5): volume points in lines -> flag bit 26, axis in bits 24-25; the
       // interface points on the lines -> bit 27, per-line index list from c.pad
-      if (n >= 5 && !std::getenv("CUTFEM_NO_VLINES")) {
+      if (n >= 5) {
         const int lax = vol_line_axis(pb->vol_pts + 4 * c.vb, c.nv, n);
         if (lax >= 0) {
           c.flags |= (1u << 26) | ((uint32_t)lax << 24);
-          const std::vector<int> li = std::getenv("CUTFEM_NO_SLINES")
-                                          ? std::vector<int>()
-                                          : srf_on_lines(pb->vol_pts + 4 * c.vb, c.nv, pb->srf_pts + 7 * c.sb, c.ns, n, lax);
+          const std::vector<int> li = srf_on_lines(pb->vol_pts + 4 * c.vb, c.nv, pb->srf_pts + 7 * c.sb, c.ns, n, lax);
           if (!li.empty()) {
             c.flags |= 1u << 27;
             c.pad = (int32_t)line_srf.size();
@@ -1494,19 +1291,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   if (!line_srf.empty() && (rc = upload(hd, &hd->d_line_srf, line_srf.data(), line_srf.size()))) return rc;
   if ((rc = upload(hd, &hd->d_srfptr, pb->srf_ptr, (size_t)(nc ? nc + 1 : 0)))) return rc;
   if ((rc = upload(hd, &hd->d_sfptr, pb->sf_ptr, (size_t)(nsf ? nsf + 1 : 0)))) return rc;
-  hd->cut_last = std::getenv("CUTFEM_CUT_LAST") != nullptr;
-  hd->uncw_first = std::getenv("CUTFEM_UNCW_FIRST") != nullptr;
-  hd->gpw_cut = std::getenv("CUTFEM_GPW_CUT") != nullptr;
-  hd->cellk = std::getenv("CUTFEM_NO_CELLK") == nullptr && !hd->gpw_cut;
-  if (hd->gpw_cut) hd->cut_last = false;  // k_gpw must follow k_cutp
-  if (const char *e = std::getenv("CUTFEM_UNCW_CTAS")) hd->uncw_ctas = std::atoi(e);
-  if (const char *e = std::getenv("CUTFEM_UNCW_HI")) hd->uncw_hi = (int)std::strtol(e, nullptr, 0);
-  hd->vlines = std::getenv("CUTFEM_NO_VLINES") == nullptr;
-  hd->slines = std::getenv("CUTFEM_NO_SLINES") == nullptr;
-  hd->flines = std::getenv("CUTFEM_FLINES") != nullptr;
-  if (const char *e = std::getenv("CUTFEM_TILE_PERSIST")) hd->persist = std::atoi(e);
-  else hd->persist = 3;
-  if (!std::getenv("CUTFEM_NO_TILE") && (rc = dispatch_tiles(hd, pb, ud, cd))) return rc;
+  if ((rc = dispatch_tiles(hd, pb, ud, cd))) return rc;
   if ((rc = upload_tables(p))) return rc;
   if (hd->ttab.empty()) {  // line operators for k_cut's structured faces (any degree)
     switch (p + 1) {
@@ -1528,7 +1313,6 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
     cudaDeviceGetAttribute(&smc, cudaDevAttrMultiProcessorCount, dev);
     hd->sm_count = smc;
   }
-  if ((rc = dispatch_occ(hd))) return rc;
   build_facetab(p, pb->h, pb->gp_gamma, hd->ft);
   hd->kp.h = pb->h;
   hd->kp.sigma = pb->sipg_gamma / pb->h;
@@ -1589,7 +1373,8 @@ int cutfem_apply(cutfem_handle *hd, const double *u_dev, double *v_dev, void *cu
   if (!hd) return fail(CUTFEM_EINVAL, "null handle");
   if (hd->n_active > 0 && (!u_dev || !v_dev)) return fail(CUTFEM_EINVAL, "null vector");
   if (u_dev == v_dev && hd->n_active > 0) return fail(CUTFEM_EINVAL, "u and v must not alias");
-  if (((uintptr_t)u_dev | (uintptr_t)v_dev) & 7) return fail(CUTFEM_EINVAL, "vectors must be 8-byte aligned");
+  // 16 bytes: blocks are moved by bulk copies / 16-byte vector accesses (even n)
+  if (((uintptr_t)u_dev | (uintptr_t)v_dev) & 15) return fail(CUTFEM_EINVAL, "vectors must be 16-byte aligned");
   CU(cudaSetDevice(hd->device));
   return dispatch_apply(hd, u_dev, v_dev, (cudaStream_t)cuda_stream);
 }
@@ -1598,18 +1383,24 @@ int cutfem_apply_kernel(cutfem_handle *hd, int which, const double *u_dev, doubl
   if (!hd) return fail(CUTFEM_EINVAL, "null handle");
   if (which != 0 && which != 1) return fail(CUTFEM_EINVAL, "which must be 0 (structured) or 1 (unstructured)");
   if (u_dev == v_dev && hd->n_active > 0) return fail(CUTFEM_EINVAL, "u and v must not alias");
+  if (hd->n_active > 0 && (!u_dev || !v_dev)) return fail(CUTFEM_EINVAL, "null vector");
+  if (((uintptr_t)u_dev | (uintptr_t)v_dev) & 15) return fail(CUTFEM_EINVAL, "vectors must be 16-byte aligned");
   CU(cudaSetDevice(hd->device));
   return dispatch_apply(hd, u_dev, v_dev, (cudaStream_t)cuda_stream, which == 0 ? 1 : 2);
 }
 
 int cutfem_apply_host(cutfem_handle *hd, const double *u_host, double *v_host, void *cuda_stream) {
   if (!hd) return fail(CUTFEM_EINVAL, "null handle");
+  if (hd->stats.n_dofs > 0 && (!u_host || !v_host)) return fail(CUTFEM_EINVAL, "null vector");
   CU(cudaSetDevice(hd->device));
   const size_t bytes = sizeof(double) * (size_t)hd->stats.n_dofs;
+  // u holds the ghost blocks behind the owned ones on a distributed handle
+  // (the halo exchange receives into them): size it with n_ext_dofs
+  const size_t ubytes = sizeof(double) * (size_t)std::max<int64_t>(hd->stats.n_ext_dofs, hd->stats.n_dofs);
   if (!hd->d_u) {
-    CU(cudaMalloc(&hd->d_u, std::max<size_t>(bytes, 8)));
-    CU(cudaMalloc(&hd->d_v, std::max<size_t>(bytes, 8)));
-    hd->dev_bytes += 2 * (int64_t)bytes;
+    CU(cudaMalloc(&hd->d_u, std::max<size_t>(ubytes, 16)));
+    CU(cudaMalloc(&hd->d_v, std::max<size_t>(bytes, 16)));
+    hd->dev_bytes += (int64_t)(ubytes + bytes);
   }
   cudaStream_t st = (cudaStream_t)cuda_stream;
   CU(cudaMemcpyAsync(hd->d_u, u_host, bytes, cudaMemcpyHostToDevice, st));

@@ -1506,6 +1506,18 @@ struct BF {
   __device__ static __forceinline__ bool writer(int lane) { return (lane & ((1 << (5 - S)) - 1)) == 0; }
 };
 
-#include "kernels_fast.cuh"
+// ------------------------------------------------------------ helpers
+template <int V>
+struct IC {
+  static constexpr int value = V;
+};
+template <int I, int E, class Fn>
+__device__ __forceinline__ void static_for(Fn &&fn) {
+  if constexpr (I < E) {
+    fn(IC<I>{});
+    static_for<I + 1, E>(fn);
+  }
+}
+
 #include "kernels_tile.cuh"
 #include "kernels_cut.cuh"

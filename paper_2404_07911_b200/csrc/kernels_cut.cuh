@@ -17,7 +17,7 @@
 // Every point is integrated into per-lane register accumulators for all n^3
 // DoFs by the factored contraction; one butterfly reduction over the
 // warp per cell, one coalesced write of the block.  The structured faces of the
-// cut cell (full-face SIPG, ghost penalty) are added afterwards by k_tile*<MODE 1>.
+// cut cell (full-face SIPG, ghost penalty) are computed here too, in w-space.
 //
 // Latency: the next cell's block + cut-face neighbour blocks are fetched (TMA
 // bulk copies, or cp.async for odd n) into the second buffer set while the
@@ -145,9 +145,6 @@ struct __align__(16) CPacket {
 #ifndef CUTP_BFLY_MAXACC
 #define CUTP_BFLY_MAXACC 32  // accumulators <= this: shuffle reduce-scatter instead of the transpose
 #endif
-#ifndef CUTP_FMIX
-#define CUTP_FMIX 1
-#endif
 #ifndef CUTP_HYB
 #define CUTP_HYB 1
 #endif
@@ -173,59 +170,12 @@ __device__ __forceinline__ void basis_v_sym(const RefTab &R, double x, double (&
   }
 }
 
-// One cut-face point of the face with normal axis D (own-side reference
-// coordinates; the normal coordinate is exactly 0 or 1).  Own-side test
-// functions at the point: l_m(face) = delta_{m,fo} along D, l'_m(face) = dw[m],
-// in-face values ls (lower in-face axis), lt (upper).  [u] = J and
-// d u_own + d u_nb = A are interpolated from the face traces; the
-// flux  W [(sigma J - s A/(2h)) phi - (s J/(2h)) d_D phi]  (s = +-1: own side)
-// is a rank-structured update of the n^3 accumulators.
-template <int N, int D, int ACC>
-__device__ __forceinline__ void face_point(double (&acc)[ACC], const RefTab &R, const double *JAB, double xi,
-                                           double eta, double zeta, double W, const KParams &kp) {
-  constexpr int NN = N * N;
-  const double xd = D == 0 ? xi : (D == 1 ? eta : zeta);
-  const int sd = xd == 1.0 ? 1 : 0;
-  double ls[N], lt[N];
-  basis_v_sym<N>(R, D == 0 ? eta : xi, ls);
-  basis_v_sym<N>(R, D == 2 ? eta : zeta, lt);
-  const double *JA = JAB + (2 * D + sd) * 2 * NN, *JB = JA + NN;
-  double J = 0.0, A = 0.0;
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    double r0 = 0.0, r1 = 0.0;
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      r0 = fma(ls[i], JA[i + N * j], r0);
-      r1 = fma(ls[i], JB[i + N * j], r1);
-    }
-    J = fma(lt[j], r0, J);
-    A = fma(lt[j], r1, A);
-  }
-  const double sg = sd ? kp.i2h : -kp.i2h;  // sign of the own side / (2h)
-  const double k1 = W * fma(kp.sigma, J, -sg * A), k2 = -W * sg * J;
-  // normal-direction factor T_m = k1 delta_{m,fo} + k2 l'_m(face)
-  double T[N];
-#pragma unroll
-  for (int m = 0; m < N; ++m) T[m] = k2 * (sd ? R.d1[m] : R.d0[m]);
-  if (sd) T[N - 1] += k1;
-  else T[0] += k1;
-#pragma unroll
-  for (int j = 0; j < N; ++j)
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const double P = ls[i] * lt[j];
-#pragma unroll
-      for (int m = 0; m < N; ++m) {
-        // (i, j) run over the in-face axes in ascending order, m along D
-        const int a = D == 0 ? m : i, b = D == 0 ? i : (D == 1 ? m : j), c = D == 2 ? m : j;
-        double &r = acc[(c * N + b) * N + a];
-        r = fma(P, T[m], r);
-      }
-    }
-}
-
-// The same cut-face point update for a runtime face axis d (chunks mixing axes):
+// One cut-face point (own-side reference coordinates; the normal coordinate is
+// exactly 0 or 1, which selects the face axis d at run time, so chunks mix axes).
+// Own-side test functions at the point: l_m(face) = delta_{m,fo} along d,
+// l'_m(face) = dw[m], in-face values ls (lower in-face axis), lt (upper).  [u] = J
+// and d u_own + d u_nb = A are interpolated from the face traces; the
+// flux  W [(sigma J - s A/(2h)) phi - (s J/(2h)) d_d phi]  (s = +-1: own side) is
 // the rank-1 update acc[c][b][a] += X_a Y_b Z_c with the normal factor T on axis d
 // and the in-face bases on the others (selected, not branched).
 template <int N, int ACC>
@@ -388,91 +338,6 @@ __device__ __forceinline__ void vol_line(double (&acc)[ACC], const RefTab &R, co
     }
 }
 
-// Cut-face points in LINES (the 2-D dimension-reduction rule on the face: n points
-// along one in-face axis at a fixed other in-face coordinate s).  Record:
-// [s, sd + 2 tl, (t, W) x n]: sd the side (0 lo face, 1 hi face of the normal axis D),
-// tl = 0 if the line runs along the lower in-face axis e1 (s on e2), 1 if along e2.
-// Per line: the trace interpolation reduced along s once (r_k = sum_m l_m(s) J[..]),
-// per point n-term sums for [u] and {d u} and M[m][k] += T_m l_k(t); then one
-// n^3 expansion acc(m on D, s-index, k on the line axis) += l(s) M.
-template <int N, int D, int ACC>
-__device__ __forceinline__ void face_line(double (&acc)[ACC], const RefTab &R, const double *JAB, const double *rec,
-                                          const KParams &kp) {
-  constexpr int NN = N * N, E1 = D == 0 ? 1 : 0, E2 = D == 2 ? 1 : 2;
-  const int meta = (int)rec[1], sd = meta & 1, tl = meta >> 1;
-  double ls[N];
-  basis_v_sym<N>(R, rec[0], ls);
-  const double *JA = JAB + (2 * D + sd) * 2 * NN, *JB = JA + NN;
-  double rJ[N], rA[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) {
-    double x = 0.0, y = 0.0;
-#pragma unroll
-    for (int m = 0; m < N; ++m) {
-      const int idx = tl ? (m + N * k) : (k + N * m);
-      x = fma(ls[m], JA[idx], x);
-      y = fma(ls[m], JB[idx], y);
-    }
-    rJ[k] = x;
-    rA[k] = y;
-  }
-  const double sg = sd ? kp.i2h : -kp.i2h;
-  double M[N][N];
-#pragma unroll
-  for (int m = 0; m < N; ++m)
-#pragma unroll
-    for (int k = 0; k < N; ++k) M[m][k] = 0.0;
-#pragma unroll
-  for (int t = 0; t < N; ++t) {
-    const double2 tw = *reinterpret_cast<const double2 *>(rec + 2 + 2 * t);
-    double lt[N];
-    basis_v_sym<N>(R, tw.x, lt);
-    double J = 0.0, A = 0.0;
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      J = fma(lt[k], rJ[k], J);
-      A = fma(lt[k], rA[k], A);
-    }
-    const double k1 = tw.y * fma(kp.sigma, J, -sg * A), k2 = -tw.y * sg * J;
-#pragma unroll
-    for (int m = 0; m < N; ++m) {
-      double T = k2 * (sd ? R.d1[m] : R.d0[m]);
-      if (m == (sd ? N - 1 : 0)) T += k1;
-#pragma unroll
-      for (int k = 0; k < N; ++k) M[m][k] = fma(T, lt[k], M[m][k]);
-    }
-  }
-  // acc(position with D-index m, s-axis index i, line-axis index k) += ls_i M[m][k]
-  auto pos = [](int mD, int m1, int m2) {  // (D, e1, e2) coordinates -> l = x + N y + N^2 z
-    int c[3];
-    c[D] = mD;
-    c[E1] = m1;
-    c[E2] = m2;
-    return c[0] + N * c[1] + NN * c[2];
-  };
-  if (tl) {
-#pragma unroll
-    for (int m = 0; m < N; ++m)
-#pragma unroll
-      for (int i = 0; i < N; ++i)
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double &r = acc[pos(m, i, k)];
-          r = fma(ls[i], M[m][k], r);
-        }
-  } else {
-#pragma unroll
-    for (int m = 0; m < N; ++m)
-#pragma unroll
-      for (int i = 0; i < N; ++i)
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double &r = acc[pos(m, k, i)];
-          r = fma(ls[i], M[m][k], r);
-        }
-  }
-}
-
 template <int N>
 struct CutPCfg {
   static constexpr bool BULK = CUTFEM_USE_BULK && (N % 2) == 0;
@@ -487,8 +352,7 @@ struct CutPCfg {
   // axis: runtime-axis face update); else chunks are kind- and axis-homogeneous
   static constexpr bool UNIFIED = N <= CUTP_UNIFIED_MAXN;
   // not unified: the cut-face points of a cell still form ONE stream over all face axes
-  // (runtime-axis update) instead of one per axis
-  static constexpr bool FMIX = !UNIFIED && CUTP_FMIX;
+  // (runtime-axis update)
   static constexpr bool BFLY = ACC <= CUTP_BFLY_MAXACC;
   // 64 accumulators: one butterfly level (xor 16) + a 16-lane shared-memory transpose
   static constexpr bool HYB = !BFLY && ACC == 64 && CUTP_HYB;
@@ -595,10 +459,9 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     if (has_next) nd = desc[c + 1];
     int nv, ns, nf;
     counts(cd, nv, ns, nf);
-    // chunks of the cell: the first KL are volume lines, the next KF cut-face lines
-    // (lines never occur at n = 2: the host plans none, and the loops are compiled out)
-    const int K = (int)((uint32_t)cd.nchunk & 0xffffu), KL = N >= 3 ? (int)(((uint32_t)cd.nchunk >> 16) & 0xffu) : 0,
-              KF = N >= 3 ? (int)((uint32_t)cd.nchunk >> 24) : 0;
+    // chunks of the cell: the first KL are volume lines
+    // (lines never occur at n = 2: the host plans none, and the loop is compiled out)
+    const int K = (int)((uint32_t)cd.nchunk & 0xffffu), KL = N >= 3 ? (int)(((uint32_t)cd.nchunk >> 16) & 0xffu) : 0;
     const uint32_t fm = fmask_of(cd);
     // ---- this cell's blocks
     if constexpr (C::BULK) {
@@ -780,25 +643,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
       __syncwarp();
       if (lane == 0 && left == 0) fence_proxy_async();
     }
-    // cut-face LINES (their own loop too): chunks of cv lines on faces of normal axis
-    // (cnt >> 24) & 3, records of 2 + 2N doubles
-    for (int k = KL; k < (N >= 3 ? KL + KF : KL); ++k) {
-      if (left == 0) next_packet();
-      const int cnt = reinterpret_cast<const int *>(S + pos)[0];
-      const int cv = cnt & 0xff, dn = (cnt >> 24) & 3;
-      const double *P = S + pos + 2;
-      --left;
-      pos += 2 + (2 + 2 * N) * cv;
-      if (lane < cv) {
-        const double *rec = P + (2 + 2 * N) * lane;
-        if (dn == 0) face_line<N, 0>(acc, R, JAB, rec, kp);
-        else if (dn == 1) face_line<N, 1>(acc, R, JAB, rec, kp);
-        else face_line<N, 2>(acc, R, JAB, rec, kp);
-      }
-      __syncwarp();
-      if (lane == 0 && left == 0) fence_proxy_async();
-    }
-    for (int k = KL + KF; k < K; ++k) {
+    for (int k = KL; k < K; ++k) {
       if (left == 0) next_packet();
       const int cnt = reinterpret_cast<const int *>(S + pos)[0];
       const int cv = cnt & 0xff, cs = (cnt >> 8) & 0xff, cf = (cnt >> 16) & 0xff;
@@ -869,14 +714,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
         }
       } else if (kind == 2) {
         // cut-face point: the face is the coordinate that is exactly 0 or 1
-        if constexpr (C::UNIFIED || C::FMIX) {
-          face_point_rt<N>(acc, R, JAB, xi, eta, zeta, W, kp);
-        } else {
-          const int d = (xi == 0.0 || xi == 1.0) ? 0 : ((eta == 0.0 || eta == 1.0) ? 1 : 2);
-          if (d == 0) face_point<N, 0>(acc, R, JAB, xi, eta, zeta, W, kp);
-          else if (d == 1) face_point<N, 1>(acc, R, JAB, xi, eta, zeta, W, kp);
-          else face_point<N, 2>(acc, R, JAB, xi, eta, zeta, W, kp);
-        }
+        face_point_rt<N>(acc, R, JAB, xi, eta, zeta, W, kp);
       }
       __syncwarp();  // every lane is done with the ring slot before it is refilled
       if (lane == 0 && left == 0) fence_proxy_async();

@@ -1,5 +1,5 @@
-// k_tile<N> (N = p+1 <= 4): structured (uncut) cells, ONE THREAD PER CELL with
-// the whole cell block held in registers (included by kernels.cuh).
+// Structured (uncut) cells in registers (included by kernels.cuh): k_tile2 (n = 4),
+// k_gpw (n = 4, ghost penalty), k_uncw (n = 5, 6, 8), k_cell (n = 2, 3).
 //
 // Why: the line-per-lane kernels sweep every 1-D line through shared memory,
 // i.e. one shared-memory access per FMA; the FP64 pipe needs ~4 FMAs per
@@ -176,162 +176,6 @@ __device__ __forceinline__ void vol_line(double (&w)[W], int t, const double (&u
 #pragma unroll
     for (int j = 0; j < N; ++j) r = fma(tt.L[csym<N>(i * N + j)], uo[j], r);
     w[lix<N, D>(t, i)] = fma(ev, r, w[lix<N, D>(t, i)]);
-  }
-}
-
-// Axis D: volume line operator and SIPG on both faces for every line (branch
-// free: a missing face reads a dummy line and is scaled by 0), then the
-// ghost-penalty faces of this axis (rare: only next to cut cells).
-template <int N, int D>
-__device__ __forceinline__ void axis_all(double (&w)[N * N * N], const double *Us, const double *Nl, const double *Nh,
-                                         double ev, double el, double eh, const TileTab<N> &tt) {
-  constexpr int NN = N * N;
-  if constexpr ((N % 2) == 0 && D != 0) {
-#pragma unroll
-    for (int t = 0; t < NN; t += 2) {
-      double u0[N], u1[N], a0[N], a1[N];
-      ld_pair<N, D>(Us, t, u0, u1);
-      vol_line<N, D>(w, t, u0, ev, tt);
-      vol_line<N, D>(w, t + 1, u1, ev, tt);
-      ld_pair<N, D>(Nl, t, a0, a1);
-      sipg_line<N, D, 0>(w, t, u0, a0, el, tt);
-      sipg_line<N, D, 0>(w, t + 1, u1, a1, el, tt);
-      ld_pair<N, D>(Nh, t, a0, a1);
-      sipg_line<N, D, 1>(w, t, u0, a0, eh, tt);
-      sipg_line<N, D, 1>(w, t + 1, u1, a1, eh, tt);
-    }
-  } else {
-#pragma unroll
-    for (int t = 0; t < NN; ++t) {
-      double u0[N], a0[N];
-      ld_line<N, D>(Us, t, u0);
-      vol_line<N, D>(w, t, u0, ev, tt);
-      ld_line<N, D>(Nl, t, a0);
-      sipg_line<N, D, 0>(w, t, u0, a0, el, tt);
-      ld_line<N, D>(Nh, t, a0);
-      sipg_line<N, D, 1>(w, t, u0, a0, eh, tt);
-    }
-  }
-}
-
-// MODE 0 / 1 as for k_tile2 below (volume + SIPG, v = ... / ghost penalty +
-// structured SIPG of cut cells, v += ...).
-template <int N, int MODE>
-__global__ void __launch_bounds__(32, T1MINB) k_tile(const double *__restrict__ u, double *__restrict__ v,
-                                                     const TileRec<TileCfg<N>::SMAX> *__restrict__ tiles,
-                                                     int ntiles, TileTab<N> tt, uint32_t mask) {
-  using C = TileCfg<N>;
-  constexpr int NN = N * N, N3 = NN * N, ST = C::ST;
-  extern __shared__ __align__(16) double smem[];
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-  double *S = smem + 2;
-  const int lane = threadIdx.x;
-  const bool cell_on = (mask & TERM_CELL) != 0, sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
-  if (C::BULK && lane == 0) {
-    mbar_init(bar, 1);
-    mbar_fence_init();
-  }
-  __syncwarp();
-  uint32_t it = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const TileRec<C::SMAX> *T = tiles + tile;
-    const int nslot = T->nslot, ncell = T->ncell;
-    const uint2 ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[lane][0]);
-    const int myblk = lane < ncell ? T->blk[lane] : 0;
-    const bool on = lane < ncell;
-    // ---- stage the tile's blocks (own cells first, then the halo)
-    if constexpr (C::BULK) {
-      fence_proxy_async();   // this lane's generic accesses precede the bulk writes into the slots
-      __syncwarp();
-      if (lane == 0) mbar_expect_tx(bar, (uint32_t)(nslot * N3 * 8));
-      __syncwarp();
-      for (int s = lane; s < nslot; s += 32) bulk_g2s(S + s * ST, u + (size_t)T->blk[s] * N3, N3 * 8, bar);
-      mbar_wait(bar, it & 1);
-    } else {
-      __syncwarp();
-      for (int s0 = 0; s0 < nslot; s0 += 32) {
-        const int bl = (s0 + lane < nslot) ? T->blk[s0 + lane] : 0;
-        const int cnt = min(32, nslot - s0);
-#pragma unroll 4
-        for (int j = 0; j < cnt; ++j) {
-          const int b = __shfl_sync(0xffffffffu, bl, j);
-          if (lane < N3) S[(s0 + j) * ST + lane] = __ldg(u + (size_t)b * N3 + lane);
-        }
-      }
-      __syncwarp();
-    }
-    double w[N3];
-#pragma unroll
-    for (int l = 0; l < N3; ++l) w[l] = 0.0;
-    if (on) {
-      const double *Us = S + lane * ST;
-      int nbs[6];
-#pragma unroll
-      for (int f = 0; f < 4; ++f) nbs[f] = (ln.x >> (8 * f)) & 0xff;
-      nbs[4] = ln.y & 0xff;
-      nbs[5] = (ln.y >> 8) & 0xff;
-      const uint32_t gpb = gp_on ? (ln.y >> 16) & 0x3fu : 0u, spb = sipg_on ? (ln.y >> 24) & 0x3fu : 0u;
-      const bool vol = ((ln.y >> 30) & 1u) && cell_on;
-      static_for<0, 3>([&](auto dc) {
-        constexpr int D = decltype(dc)::value;
-        const double *Nl = nbs[2 * D] != 0xff ? S + nbs[2 * D] * ST : Us;  // dummy line source when absent
-        const double *Nh = nbs[2 * D + 1] != 0xff ? S + nbs[2 * D + 1] * ST : Us;
-        const double el = ((spb >> (2 * D)) & 1u) ? 1.0 : 0.0, eh = ((spb >> (2 * D + 1)) & 1u) ? 1.0 : 0.0;
-        if constexpr (MODE == 0) {
-          axis_all<N, D>(w, Us, Nl, Nh, vol ? 1.0 : 0.0, el, eh, tt);
-        } else {
-          const double gl = ((gpb >> (2 * D)) & 1u) ? 1.0 : 0.0, gh = ((gpb >> (2 * D + 1)) & 1u) ? 1.0 : 0.0;
-#pragma unroll
-          for (int t = 0; t < NN; ++t) {
-            double uo[N], a0[N], a1[N];
-            ld_line<N, D>(Us, t, uo);
-            ld_line<N, D>(Nl, t, a0);
-            ld_line<N, D>(Nh, t, a1);
-            sipg_line<N, D, 0>(w, t, uo, a0, el, tt);
-            sipg_line<N, D, 1>(w, t, uo, a1, eh, tt);
-            gp_rows<N, 0, 0, N>(w, [&](int m) { return lix<N, D>(t, m); }, uo, a0, gl, tt);
-            gp_rows<N, 1, 0, N>(w, [&](int m) { return lix<N, D>(t, m); }, uo, a1, gh, tt);
-          }
-        }
-      });
-      // v = (M (x) M (x) M) w
-      static_for<0, 3>([&](auto dc) {
-        constexpr int D = decltype(dc)::value;
-#pragma unroll
-        for (int t = 0; t < NN; ++t) {
-          double x[N];
-#pragma unroll
-          for (int i = 0; i < N; ++i) {
-            double r = 0.0;
-#pragma unroll
-            for (int j = 0; j < N; ++j) r = fma(tt.M[csym<N>(i * N + j)], w[lix<N, D>(t, j)], r);
-            x[i] = r;
-          }
-#pragma unroll
-          for (int i = 0; i < N; ++i) w[lix<N, D>(t, i)] = x[i];
-        }
-      });
-    }
-    __syncwarp();  // every lane is done reading the tile's slots
-    if (on) {
-      double *Us = S + lane * ST;
-      if constexpr ((N % 2) == 0) {
-#pragma unroll
-        for (int l = 0; l < N3; l += 2) *reinterpret_cast<double2 *>(Us + l) = make_double2(w[l], w[l + 1]);
-      } else {
-#pragma unroll
-        for (int l = 0; l < N3; ++l) Us[l] = w[l];
-      }
-    }
-    __syncwarp();
-    // ---- coalesced write-back of the cell blocks (MODE 1: read-add-write)
-    for (int e = lane; e < ncell * N3; e += 32) {
-      const int c = e / N3, l = e - c * N3;
-      const int b = T->blk[c];
-      double x = S[c * ST + l];
-      if constexpr (MODE == 1) x += v[(size_t)b * N3 + l];
-      v[(size_t)b * N3 + l] = x;
-    }
   }
 }
 
