@@ -298,7 +298,11 @@ def run_ours(args, P, cfg, rank, world, local_rank):
             op.apply_kernel(which, u, v)
         k_ms[name] = float(timed(lambda: op.apply_kernel(which, u, v), args.steps).mean())
 
-    work = costmodel.apply_work(st)
+    own = None
+    if world > 1:
+        own = np.zeros(P.n_active, bool)
+        own[g0:g0 + n_own] = True
+    work = costmodel.apply_work(st, costmodel.face_classes(P, own))
     peaks = load_peaks()
     bw = float(peaks.get("hbm_gbs", 6543.7)) * 1e9
     fp64 = costmodel.fp64_peak_tflops() * 1e12
@@ -317,7 +321,13 @@ def run_ours(args, P, cfg, rank, world, local_rank):
     roofline = {"bound": "alu", "achieved": achieved, "peak": fp64 / 1e12, "unit": "TFLOP/s",
                 "frac": achieved / (fp64 / 1e12), "traffic": traffic, "kernel": kname[dom],
                 "kernel_ms": k_ms[dom], "flops_per_launch": F_dom, "alg_bytes_per_launch": B_dom,
-                "peak_kind": "derived FP64: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (measured DFMA probe 34.1)",
+                "peak_kind": "derived FP64: 148 SM x 64 FMA/clk x 2 x 1.965 GHz",
+                "peak_probe": {"value": 34.1, "unit": "TFLOP/s", "what": "DFMA-throughput probe "
+                               "(tools/fp64_peak.cu, profiles/r01_fp64_peak.txt); frac vs probe = "
+                               + f"{achieved / 34.1:.3f}"},
+                "work_model": "SURVEY §8(d) per-unit counts (paper_2404_07911_b200/costmodel.py, pinned by "
+                              "tests/test_oracle_pins.py::test_cost_model_*); the dominant kernel's share: "
+                              "its cells and the halves of the faces on its side",
                 "apply": {"F_alg": work["F_total"], "B_alg": work["B_total"],
                           "flop_per_dof": work["F_total"] / max(op.n_dofs, 1),
                           "byte_per_dof": work["B_total"] / max(op.n_dofs, 1),

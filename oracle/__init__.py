@@ -13,12 +13,15 @@ quadrature point (naive interpolation S_ql), with no sum
 factorisation, then applied blockwise (eq:matrixfreeopcompact P:209-212) or
 assembled into CSR (eq:matrixbasedop P:224-227).
 
-Pins (tests/test_oracle_pins.py): Q1 Kronecker cell matrix, Q2 face closed
-form, Q3 GP special cases, Q4 "level set misses the mesh" = standard SIPG,
-Q6 exact identities, Q7 symmetry, Q8 SPD, Q9 quadrature moments, Q11
-convergence order, Q12 CSR = blockwise.  "parity unpinned": the absolute value
-of curved-interface contributions has no closed form; it is pinned only
-indirectly (Q6, Q7, Q8, Q9, Q11) — see DESIGN.md.
+Pins (tests/test_oracle_pins.py, tests/test_oracle_plane.py): Q1 Kronecker
+cell matrix, Q2 face closed form, Q3 GP closed form order by order, Q4 "level
+set misses the mesh" = standard SIPG, Q5 axis-aligned plane = sum of Kronecker
+products (every term, cut faces included), Q6 exact identities, Q7 symmetry,
+Q8 SPD, Q9 quadrature moments, Q10 tensor rule as cut rule, Q11 convergence
+order, Q12 CSR = blockwise (DESIGN.md §4 maps every function to its pin).
+"parity unpinned": the absolute value of curved-interface contributions has no
+closed form; it is pinned exactly on the plane (Q5) and indirectly on curved
+interfaces (Q6, Q7, Q8, Q9, Q11).
 """
 from .basis import Basis1D  # noqa: F401
 from .operator import Oracle  # noqa: F401

@@ -12,6 +12,7 @@ import numpy.polynomial.legendre as npleg
 import pytest
 from numpy.polynomial import Polynomial
 
+import pin1d
 from oracle import Oracle
 from oracle.operator import TERM_CELL, TERM_GP, TERM_NITSCHE, TERM_SIPG, cg
 
@@ -93,7 +94,7 @@ def test_q1_uncut_cell_matrix_is_kronecker_sum(cutgen_mod, p):
 
 
 # --------------------------------------------------------------------- Q2
-@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("d", [0, 1, 2])
 def test_q2_uncut_face_matrix_closed_form(cutgen_mod, p, d):
     n = [1, 1, 1]
@@ -104,10 +105,14 @@ def test_q2_uncut_face_matrix_closed_form(cutgen_mod, p, d):
     (m, pl, dd, sf), = O.faces
     assert dd == d and sf == -1
     A = O.face_matrix(m, pl, d, sf, TERM_SIPG)
-    M1, _ = mass_stiff_np(p)
+    # independent 1-D route (tests/pin1d.py: barycentric D, mpmath GLL roots)
+    M1, _ = pin1d.mass_stiff(p)
     sigma = P.sipg_gamma / h
-    J = np.concatenate([traces_np(p, 0, 1), -traces_np(p, 0, 0)])
-    Av = 0.5 * np.concatenate([traces_np(p, 1, 1), traces_np(p, 1, 0)]) / h
+    J = np.concatenate([pin1d.trace(p, 0, 1), -pin1d.trace(p, 0, 0)])
+    Av = 0.5 * np.concatenate([pin1d.trace(p, 1, 1), pin1d.trace(p, 1, 0)]) / h
+    if p <= 4:  # a second route (numpy polynomials) for the traces where it is well conditioned
+        assert np.allclose(J, np.concatenate([traces_np(p, 0, 1), -traces_np(p, 0, 0)]), atol=1e-13)
+        assert np.allclose(Av * h, 0.5 * np.concatenate([traces_np(p, 1, 1), traces_np(p, 1, 0)]), atol=1e-11)
     S = sigma * np.outer(J, J) - np.outer(Av, J) - np.outer(J, Av)
     nn = p + 1
     for si in range(2):
@@ -121,7 +126,7 @@ def test_q2_uncut_face_matrix_closed_form(cutgen_mod, p, d):
 
 
 # --------------------------------------------------------------------- Q3
-@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_q3_gp_closed_form_and_special_cases(cutgen_mod, p):
     h = 0.25
     P = cutgen_mod.generate(FAR, [2, 1, 1], [0, 0, 0], [2 * h, h, h], p, force_cut_cells=True)
@@ -132,17 +137,30 @@ def test_q3_gp_closed_form_and_special_cases(cutgen_mod, p):
     # u = 1 on K-, 0 on K+: only j = 0 survives -> 0.1 h * |F|/h^2 ... = 0.1 h
     u = np.concatenate([np.ones(nd), np.zeros(nd)])
     assert abs(u @ A @ u - 0.1 * h) <= 1e-14 * (u @ np.abs(A) @ u)
-    # closed form [sum_j 0.1 h D_j D_j^T] (x) (M (x) M)
-    M1, _ = mass_stiff_np(p)
+    # closed form [sum_j 0.1 h D_j D_j^T] (x) (M (x) M), checked order by order
+    # (j-th term alone via a GP weight vector e_j: the high orders cannot mask a
+    # wrong low-order trace), traces from the independent D^j route (pin1d)
+    M1, _ = pin1d.mass_stiff(p)
     G = np.zeros((2 * nn, 2 * nn))
     for j in range(p + 1):
-        Dj = np.concatenate([traces_np(p, j, 1), -traces_np(p, j, 0)])
-        G += 0.1 * h * np.outer(Dj, Dj)
+        Dj = np.concatenate([pin1d.trace(p, j, 1), -pin1d.trace(p, j, 0)])
+        Gj = 0.1 * h * np.outer(Dj, Dj)
+        G += Gj
+        gj = np.zeros(p + 1)
+        gj[j] = 0.1
+        Pj = cutgen_mod.generate(FAR, [2, 1, 1], [0, 0, 0], [2 * h, h, h], p, force_cut_cells=True, gp_gamma=gj)
+        Oj = Oracle(Pj)
+        Aj = Oj.face_matrix(m, pl, d, sf, TERM_GP)
+        for si in range(2):
+            for sj in range(2):
+                ref = np.kron(M1, np.kron(M1, Gj[si * nn:(si + 1) * nn, sj * nn:(sj + 1) * nn]))
+                blk = Aj[si * nd:(si + 1) * nd, sj * nd:(sj + 1) * nd]
+                assert np.abs(blk - ref).max() <= 1e-11 * np.abs(Gj).max(), (j, np.abs(blk - ref).max())
     for si in range(2):
         for sj in range(2):
             ref = np.kron(M1, np.kron(M1, G[si * nn:(si + 1) * nn, sj * nn:(sj + 1) * nn]))
             blk = A[si * nd:(si + 1) * nd, sj * nd:(sj + 1) * nd]
-            assert np.abs(blk - ref).max() <= 1e-10 * np.abs(G).max()
+            assert np.abs(blk - ref).max() <= 1e-11 * np.abs(G).max()
     # A_GP q = 0 for a global polynomial of degree <= p per direction
     nodes = gll_np(p)
     rng = np.random.default_rng(0)
@@ -404,6 +422,13 @@ def test_eoc_helper_against_paper_golden():
 
 
 def _solve_manufactured(cutgen_mod, N, p):
+    """Solve A x = b (oracle CSR, oracle RHS) for the manufactured solution
+    u = cos(om R) - cos(om r) (-Laplace u = f, u = 0 on the sphere) and
+    return the oracle's relative L2 error.  The solver is test-side: CG with a
+    cell-block Jacobi preconditioner (inverse of each n^3 x n^3 diagonal block),
+    started from the nodal interpolant of u, stopped at ||r|| <= 1e-7 ||r0|| --
+    far below the discretisation error it measures (checked: 1e-10 changes the
+    8^3 p=3 error in the 7th digit)."""
     R, om = 0.7, math.pi
     c = np.array(cutgen_mod.SPHERE["center"])
     P = cutgen_mod.generate(cutgen_mod.SPHERE, N, -1.0, 1.0, p)
@@ -421,34 +446,149 @@ def _solve_manufactured(cutgen_mod, N, p):
         return math.cos(om * R) - np.cos(om * rr(x))
 
     b = O.rhs(f)
-    Minv = 1.0 / M.diagonal()
-    x, it = cg(lambda y: M @ y, b, tol=1e-11, M=Minv, maxiter=20000)
+    nd, nb = (p + 1) ** 3, P.n_active
+    Binv = np.empty((nb, nd, nd))
+    for K in range(nb):
+        Binv[K] = np.linalg.inv(M[K * nd:(K + 1) * nd, K * nd:(K + 1) * nd].toarray())
+
+    def prec(r):
+        return np.einsum("kij,kj->ki", Binv, r.reshape(nb, nd)).reshape(-1)
+
+    nodes = gll_np(p)
+    Z, Y, X = np.meshgrid(nodes, nodes, nodes, indexing="ij")
+    loc = np.stack([X.ravel(), Y.ravel(), Z.ravel()], 1)
+    x = uex(np.asarray(P.lower) + P.h * (P.active_ijk[:, None, :] + loc[None])).reshape(-1)
+    r = b - M @ x
+    z = prec(r)
+    pv = z.copy()
+    rz, r0 = r @ z, np.linalg.norm(r)
+    for _ in range(20000):
+        if np.linalg.norm(r) <= 1e-7 * r0:
+            break
+        Ap = M @ pv
+        alpha = rz / (pv @ Ap)
+        x += alpha * pv
+        r -= alpha * Ap
+        z = prec(r)
+        rzn = r @ z
+        pv = z + (rzn / rz) * pv
+        rz = rzn
+    assert np.linalg.norm(r) <= 1e-7 * r0
     return O.l2_error(x, uex)
 
 
-@pytest.mark.parametrize("p", [1, 2])
-def test_q11_convergence_order(cutgen_mod, p):
-    e1 = _solve_manufactured(cutgen_mod, 8, p)
-    e2 = _solve_manufactured(cutgen_mod, 16, p)
-    assert eoc(e1, e2) >= p + 0.6, (e1, e2, eoc(e1, e2))
+@pytest.mark.parametrize("p,meshes", [(1, (8, 16, 32)), (2, (8, 16, 32)), (3, (8, 12, 16))])
+def test_q11_convergence_order(cutgen_mod, p, meshes):
+    """L2 EOC >= p + 0.7 on three meshes (the paper's slope p+1,
+    P:716).  p = 3 uses 8/12/16 (a 32^3 p = 3 CSR has ~1.9e8 non-zeros: minutes on the
+    CPU; tools/q11_full.py runs 8/16/32 at p = 3 and its output is in profiles/)."""
+    errs = [_solve_manufactured(cutgen_mod, N, p) for N in meshes]
+    for k in range(len(meshes) - 1):
+        rate = math.log(errs[k] / errs[k + 1]) / math.log(meshes[k + 1] / meshes[k])
+        assert rate >= p + 0.7, (p, meshes, errs, rate)
 
 
 # ------------------------------------------------------------- cost formulas
 def test_paper_cost_formula_golden():
+    """The product's closed forms (paper_2404_07911_b200/costmodel.py) against the
+    values of the paper's formulas (tests/golden/paper_cost_formulas.txt)."""
+    from paper_2404_07911_b200 import costmodel as cm
     rows = [l.split() for l in open(__file__.replace("test_oracle_pins.py", "golden/paper_cost_formulas.txt"))
             if l.strip() and not l.startswith("#")]
     f = {
-        "structured_cell_fma": lambda k: 6 * k ** 4,
-        "structured_face_fma": lambda k: 7 * k ** 3,
-        "unstructured_cell_fma": lambda k: 2 * k ** 6 + 3 * k ** 5 + 4 * k ** 4,
-        "unstructured_face_fma": lambda k: 3 * k ** 4 + 5 * k ** 3,
-        "sparse_dg_bytes_per_dof": lambda k: 12 * 7 * k ** 3,
-        "sparse_dg_flops_per_dof": lambda k: 2 * 7 * k ** 3,
-        "sparse_cg_bytes_per_dof": lambda k: 12 * (k + 1) ** 3 // 1,
-        "sparse_cg_flops_per_dof": lambda k: 2 * (k + 1) ** 3,
+        "structured_cell_fma": cm.paper_structured_cell_fma,
+        "structured_face_fma": cm.paper_structured_face_fma,
+        "unstructured_cell_fma": cm.paper_unstructured_cell_fma,
+        "unstructured_face_fma": cm.paper_unstructured_face_fma,
+        # the sparse rows are keyed by k = p+1
+        "sparse_dg_bytes_per_dof": lambda k: cm.paper_sparse_dg_bytes_per_dof(k - 1),
+        "sparse_dg_flops_per_dof": lambda k: cm.paper_sparse_dg_flops_per_dof(k - 1),
+        "sparse_cg_bytes_per_dof": lambda k: cm.paper_sparse_cg_bytes_per_dof(k - 1),
+        "sparse_cg_flops_per_dof": lambda k: cm.paper_sparse_cg_flops_per_dof(k - 1),
     }
+    assert len(rows) == len(f)
     for name, k, val, *_ in rows:
-        # sparse CG rows use p = k-1: 12(p+2)^3 with p = 1 -> 12*27 = 324
-        kk = int(k)
-        got = f[name](kk) if not name.startswith("sparse_cg") else f[name](kk)
-        assert got == int(val), (name, got, val)
+        assert f[name](int(k)) == int(val), (name, f[name](int(k)), val)
+    # the cut-face count at n_q = k^2 is the paper's 3k^4 + 5k^3 (x 8: FLOPs, E+I, sides)
+    for k in range(2, 10):
+        assert cm.flops_cut_face(k, k * k) == 8 * cm.paper_unstructured_face_fma(k)
+
+
+class _Prob:
+    def __init__(self, ijk, cut, sf_cells=(), sf_axis=(), sf_npts=()):
+        self.active_ijk = np.asarray(ijk, dtype=np.int32)
+        self.is_cut = np.asarray(cut, dtype=np.uint8)
+        self.sf_cells = np.asarray(sf_cells, dtype=np.int32).reshape(-1, 2)
+        self.sf_axis = np.asarray(sf_axis, dtype=np.uint8)
+        self.sf_ptr = np.concatenate([[0], np.cumsum(sf_npts)]).astype(np.int64)
+
+
+def test_cost_model_hand_counted():
+    """apply_work on 2 x 1 x 1 meshes, counted by hand from SURVEY §8(d) at p = 1
+    (n = 2, even-odd line cost c_eo = n^2 + 2n = 8):
+      uncut cell   2*6*n^2*8 + 3n^3            = 384 + 24         = 408
+      full face    2*2*(2n^3 + 2*2*n*8) + 10n^2 = 4*(16 + 64) + 40 = 360
+      GP face      8n^4 + 2n^2*8               = 128 + 64         = 192
+      volume pt    4(2n^3+3n^2+4n) + 6n(n-1) + 12 = 144 + 12 + 12 = 168
+      interface pt volume pt + 12                                 = 180
+      cut face     8 (n^3 + n_q (3n^2 + 4n)), n_q = 5: 8 (8 + 100) = 864
+    bytes: 16 B per DoF (8 DoFs per cell), 8 B per cell, 12 B per special face side,
+    32 / 56 / 24 B per volume / interface / cut-face point."""
+    from paper_2404_07911_b200 import costmodel as cm
+    # uncut cell 0 | cut cell 1: one full face (SIPG) that is also a GP face
+    P = _Prob([[0, 0, 0], [1, 0, 0]], [0, 1])
+    c = cm.face_classes(P)
+    assert c == {"sipg_side_cut": 1, "sipg_side_uncut": 1, "gp_side_cut": 1, "gp_side_uncut": 1,
+                 "cutface_side": 0, "cutface_pts_side": 0}
+    st = {"degree": 1, "n_uncut": 1, "n_cut": 1, "n_vol_pts": 10, "n_srf_pts": 4, "n_face_pts": 0, "n_dofs": 16}
+    w = cm.apply_work(st, c)
+    assert w["F_uncut"] == 408 + 360 / 2 + 192 / 2
+    assert w["F_cut"] == 10 * 168 + 4 * 180 + 360 / 2 + 192 / 2
+    assert w["B_uncut"] == 16 * 8 + 8 + 12
+    assert w["B_cut"] == 16 * 8 + 8 + 10 * 32 + 4 * 56 + 12
+    # two cut cells sharing a listed cut face with 5 points (GP too), along y
+    P = _Prob([[0, 0, 0], [0, 1, 0]], [1, 1], [[0, 1]], [1], [5])
+    c = cm.face_classes(P)
+    assert c == {"sipg_side_cut": 0, "sipg_side_uncut": 0, "gp_side_cut": 2, "gp_side_uncut": 0,
+                 "cutface_side": 2, "cutface_pts_side": 10}
+    st = {"degree": 1, "n_uncut": 0, "n_cut": 2, "n_vol_pts": 0, "n_srf_pts": 0, "n_face_pts": 5, "n_dofs": 16}
+    w = cm.apply_work(st, c)
+    assert w["F_uncut"] == 0 and w["F_cut"] == 864 + 192
+    assert w["B_cut"] == 2 * (16 * 8 + 8) + 5 * 24 + 12 * 4
+    # a listed face with no points carries no SIPG (reading A13) but still the GP
+    P = _Prob([[0, 0, 0], [0, 0, 1]], [1, 0], [[0, 1]], [2], [0])
+    assert cm.face_classes(P)["sipg_side_cut"] == 0 and cm.face_classes(P)["gp_side_uncut"] == 1
+
+
+def test_cost_model_face_classes_match_oracle_faces(cutgen_mod):
+    """face_classes enumerates the same faces as the oracle (C1 and a gyroid box)."""
+    from paper_2404_07911_b200 import costmodel as cm
+    for P in (cutgen_mod.config("C1"), cutgen_mod.generate(cutgen_mod.GYROID, 6, 0.0, 1.0, 1)):
+        O = Oracle(P)
+        cut = P.is_cut.astype(bool)
+        ref = {"sipg_side_cut": 0, "sipg_side_uncut": 0, "gp_side_cut": 0, "gp_side_uncut": 0,
+               "cutface_side": 0, "cutface_pts_side": 0}
+        for (m, pl, d, sf) in O.faces:
+            npt = -1 if sf < 0 else int(P.sf_ptr[sf + 1] - P.sf_ptr[sf])
+            for s in (m, pl):
+                k = "cut" if cut[s] else "uncut"
+                if cut[m] or cut[pl]:
+                    ref["gp_side_" + k] += 1
+                if npt < 0:
+                    ref["sipg_side_" + k] += 1
+                elif npt > 0:
+                    ref["cutface_side"] += 1
+                    ref["cutface_pts_side"] += npt
+        assert cm.face_classes(P) == ref
+
+
+def test_oracle_cg_solves_spd_system():
+    """oracle.operator.cg (used by the GPU CG parity test) against a direct solve."""
+    rng = np.random.default_rng(4)
+    B = rng.standard_normal((40, 40))
+    A = B @ B.T + 40 * np.eye(40)
+    b = rng.standard_normal(40)
+    x, it = cg(lambda y: A @ y, b, tol=1e-14, maxiter=500)
+    assert np.abs(x - np.linalg.solve(A, b)).max() <= 1e-12 * np.abs(x).max()
+    x, it = cg(lambda y: A @ y, b, tol=0.0, maxiter=3)
+    assert it == 3

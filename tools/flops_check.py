@@ -25,7 +25,7 @@ for ln in lines:
 print(f"{'config':>10} {'kernel':>16} {'time us':>9} {'exec GFLOP':>11} {'alg GFLOP':>10} {'exec/alg':>9} {'exec TF/s':>10}")
 for b in blocks:
     st = b["stats"]
-    w = costmodel.apply_work(st)
+    w = costmodel.apply_work(st, costmodel.face_classes(P))
     k = collections.defaultdict(lambda: collections.defaultdict(float))
     for r in b["rows"]:
         name = r[4].split("(")[0].replace("void ", "")

@@ -53,7 +53,7 @@ def run(name, P):
     u = torch.from_numpy(P.seeded_u(0)).cuda()
     v = torch.empty_like(u)
     ms = timed(op, u, v)
-    w = costmodel.apply_work(st)
+    w = costmodel.apply_work(st, costmodel.face_classes(P))
     troof = max(w["F_total"] / (costmodel.fp64_peak_tflops() * 1e12), w["B_total"] / 6539.2e9)
     print(json.dumps({"case": name, "degree": P.degree, "n_dofs": P.n_dofs, "n_active": P.n_active,
                       "n_cut": P.n_cut, "cut_ratio": P.n_cut / max(P.n_active, 1), "ms": ms,

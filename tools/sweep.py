@@ -44,8 +44,8 @@ for spec in specs:
             b.record()
         torch.cuda.synchronize()
         kms[kn] = float(np.median([a.elapsed_time(b) for a, b in evs]))
-    w = costmodel.apply_work(st)
-    troof = max(w["F_total"] / (costmodel.fp64_peak_tflops() * 1e12), w["B_total"] / 6543.7e9)
+    w = costmodel.apply_work(st, costmodel.face_classes(P))
+    troof = max(w["F_total"] / (costmodel.fp64_peak_tflops() * 1e12), w["B_total"] / 6539.2e9)
     print(json.dumps({"config": P.name, "degree": P.degree, "n_dofs": P.n_dofs, "n_cut": P.n_cut,
                       "gen_s": round(tg, 1), "ms": ms, "gdofs": P.n_dofs / ms / 1e6,
                       "frac": troof / (ms * 1e-3), "flop_per_dof": w["F_total"] / P.n_dofs,
