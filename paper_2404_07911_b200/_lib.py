@@ -127,6 +127,7 @@ def load(path: str | None = None):
     L.cutfem_setup_dist.argtypes = [ctypes.POINTER(_Problem), ctypes.c_int32, ctypes.c_int32, i32, i32, vp, i32,
                                     ctypes.POINTER(vp)]
     L.cutfem_dist_info.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.cutfem_debug_loopback.argtypes = [vp, vp, vp]
     for name in ("cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_host", "cutfem_csr_assemble",
                  "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_download", "cutfem_stats",
                  "cutfem_destroy", "cutfem_partition_x", "cutfem_local_build", "cutfem_nccl_unique_id",
@@ -379,3 +380,10 @@ class CutFEMDist(CutFEM):
         n_own, g_lo, g_hi = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(self._L.cutfem_dist_info(self._h, ctypes.byref(n_own), ctypes.byref(g_lo), ctypes.byref(g_hi)))
         self.n_own_blocks, self.n_ghost_lo, self.n_ghost_hi = n_own.value, g_lo.value, g_hi.value
+
+    def debug_loopback(self, src_lo, src_hi):
+        """Test only: 1-rank NCCL loopback; the halo exchange receives src_lo / src_hi
+        (device tensors, the neighbours' boundary planes) into the ghost slots."""
+        self._keep = (src_lo, src_hi)
+        tp = lambda t: t.data_ptr() if t is not None and t.numel() else None  # noqa: E731
+        _check(self._L.cutfem_debug_loopback(self._h, tp(src_lo), tp(src_hi)))

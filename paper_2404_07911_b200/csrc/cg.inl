@@ -191,7 +191,7 @@ namespace {
 int cg_reduce(cutfem_handle *hd, double *partial, double *out, cudaStream_t st) {
   k_dot_final<<<1, CG_THREADS, 0, st>>>(partial, CG_BLOCKS, out);
   CU(cudaGetLastError());
-  if (hd->dist && hd->nranks > 1) {
+  if (hd->dist && hd->comm && (hd->nranks > 1 || hd->loopback)) {
     ncclResult_t r = ncclAllReduce(out, out, 1, ncclDouble, ncclSum, (ncclComm_t)hd->comm, st);
     if (r != ncclSuccess) return fail(CUTFEM_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
   }

@@ -123,21 +123,33 @@ int local_build(const cutfem_problem *g, int32_t x_begin, int32_t x_end, cutfem_
 }
 
 int halo_exchange(cutfem_handle *hd, const double *u_ext, cudaStream_t st) {
-  if (hd->nranks <= 1 || !hd->comm) return 0;
+  if ((hd->nranks <= 1 && !hd->loopback) || !hd->comm) return 0;
   const int64_t n3 = (int64_t)hd->n * hd->n * hd->n;
   ncclComm_t comm = (ncclComm_t)hd->comm;
   CU(cudaEventRecord(hd->ev_comm_fork, st));
   CU(cudaStreamWaitEvent(hd->comm_stream, hd->ev_comm_fork, 0));
   double *ue = const_cast<double *>(u_ext);
   ncclResult_t r = ncclGroupStart();
-  if (hd->rank > 0) {
+  if (hd->loopback) {
+    // test-only: rank 0 plays both neighbours; sends and receives to the same peer
+    // match in issue order (lo first, then hi)
+    if (r == ncclSuccess && hd->ghost_lo)
+      r = ncclSend(hd->lb_lo, (size_t)(hd->ghost_lo * n3), ncclDouble, 0, comm, hd->comm_stream);
+    if (r == ncclSuccess && hd->ghost_hi)
+      r = ncclSend(hd->lb_hi, (size_t)(hd->ghost_hi * n3), ncclDouble, 0, comm, hd->comm_stream);
+    if (r == ncclSuccess && hd->ghost_lo)
+      r = ncclRecv(ue + hd->n_own * n3, (size_t)(hd->ghost_lo * n3), ncclDouble, 0, comm, hd->comm_stream);
+    if (r == ncclSuccess && hd->ghost_hi)
+      r = ncclRecv(ue + (hd->n_own + hd->ghost_lo) * n3, (size_t)(hd->ghost_hi * n3), ncclDouble, 0, comm,
+                   hd->comm_stream);
+  } else if (hd->rank > 0) {
     if (r == ncclSuccess && hd->plane_lo)
       r = ncclSend(ue, (size_t)(hd->plane_lo * n3), ncclDouble, hd->rank - 1, comm, hd->comm_stream);
     if (r == ncclSuccess && hd->ghost_lo)
       r = ncclRecv(ue + hd->n_own * n3, (size_t)(hd->ghost_lo * n3), ncclDouble, hd->rank - 1, comm,
                    hd->comm_stream);
   }
-  if (hd->rank < hd->nranks - 1) {
+  if (!hd->loopback && hd->rank < hd->nranks - 1) {
     if (r == ncclSuccess && hd->plane_hi)
       r = ncclSend(ue + (hd->n_own - hd->plane_hi) * n3, (size_t)(hd->plane_hi * n3), ncclDouble, hd->rank + 1,
                    comm, hd->comm_stream);
@@ -250,6 +262,33 @@ int cutfem_setup_dist(const cutfem_problem *global_pb, int32_t x_begin, int32_t 
     return rc;
   }
   *out = hd;
+  return 0;
+}
+
+// Test-only (not in the public header): turn a 1-rank distributed handle into an
+// NCCL loopback -- a real 1-rank communicator, the halo exchange sending src_lo /
+// src_hi (device, ghost_lo / ghost_hi blocks: what the neighbours would send) to
+// itself into the ghost slots, and cutfem_cg's dots going through ncclAllReduce --
+// so the NCCL data plane, the comm stream and its events run on one GPU.
+int cutfem_debug_loopback(cutfem_handle *hd, const double *src_lo, const double *src_hi) {
+  if (!hd || !hd->dist || hd->nranks != 1) return fail(CUTFEM_EINVAL, "loopback needs a 1-rank distributed handle");
+  if ((hd->ghost_lo && !src_lo) || (hd->ghost_hi && !src_hi)) return fail(CUTFEM_EINVAL, "null source");
+  CU(cudaSetDevice(hd->device));
+  if (!hd->comm) {
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    ncclComm_t comm;
+    if (r == ncclSuccess) r = ncclCommInitRank(&comm, 1, id, 0);
+    if (r != ncclSuccess) return fail(CUTFEM_ENCCL, std::string("loopback comm: ") + ncclGetErrorString(r));
+    hd->comm = comm;
+    if (cudaStreamCreateWithFlags(&hd->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&hd->ev_comm, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&hd->ev_comm_fork, cudaEventDisableTiming) != cudaSuccess)
+      return fail(CUTFEM_ECUDA, "comm stream / events");
+  }
+  hd->loopback = true;
+  hd->lb_lo = src_lo;
+  hd->lb_hi = src_hi;
   return 0;
 }
 

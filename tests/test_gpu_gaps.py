@@ -1,0 +1,186 @@
+"""GPU parity beyond the generator's structured rules and at full size (VERDICT r1
+"what's missing" #2, #5): arbitrary quadrature arrays through every single-point
+path, BASELINE configs at full size (sampled blocks), multi-tile meshes at p = 7, 8,
+the CG at odd vector lengths, the pointer contract, and the NCCL data plane on one
+GPU (1-rank loopback communicator).  Tolerances as in test_gpu_parity.py.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import Oracle  # noqa: E402
+from test_gpu_parity import check, gpu_apply  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def cf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_07911_b200 as m
+    m.load()
+    return m
+
+
+def randomize_rules(P, seed, frac=0.5):
+    """Replace the rules of a random half of the cut cells (and of the listed faces)
+    by ARBITRARY ones: ragged point counts (0 .. > 3 chunks), points anywhere in the
+    cell / face (no lines: every single-point path of the kernels runs), random
+    unit normals and positive weights.  The operator is defined for any rule
+    (SURVEY §8(c) A17), so the oracle stays the reference."""
+    rng = np.random.default_rng(seed)
+    n, h = P.degree + 1, P.h
+    vol, srf = [], []
+    vptr, sptr = [0], [0]
+    for c in range(P.n_cut):
+        v = P.vol_pts[P.vol_ptr[c]:P.vol_ptr[c + 1]]
+        s = P.srf_pts[P.srf_ptr[c]:P.srf_ptr[c + 1]]
+        if rng.random() < frac:
+            nv = int(rng.integers(1, 3 * n ** 3 + 40))
+            v = np.concatenate([rng.random((nv, 3)), (h ** 3 / nv) * rng.uniform(0.1, 1.0, (nv, 1))], 1)
+            ns = int(rng.integers(0, 2 * n * n + 5))
+            nr = rng.standard_normal((ns, 3))
+            nr /= np.linalg.norm(nr, axis=1, keepdims=True)
+            s = np.concatenate([rng.random((ns, 3)), nr, (h * h / max(ns, 1)) * rng.uniform(0.1, 1.0, (ns, 1))], 1)
+        vol.append(v)
+        srf.append(s)
+        vptr.append(vptr[-1] + len(v))
+        sptr.append(sptr[-1] + len(s))
+    fpts, fptr = [], [0]
+    for f in range(P.sf_cells.shape[0]):
+        q = P.sf_pts[P.sf_ptr[f]:P.sf_ptr[f + 1]]
+        if rng.random() < frac:
+            nq = int(rng.integers(0, 2 * n * n + 5))  # 0: an empty face (no SIPG, A13)
+            q = np.concatenate([rng.random((nq, 2)), (h * h / max(nq, 1)) * rng.uniform(0.1, 1.0, (nq, 1))], 1)
+        fpts.append(q)
+        fptr.append(fptr[-1] + len(q))
+    P.vol_pts = np.concatenate(vol).reshape(-1, 4)
+    P.vol_ptr = np.asarray(vptr, dtype=np.int64)
+    P.srf_pts = np.concatenate(srf).reshape(-1, 7)
+    P.srf_ptr = np.asarray(sptr, dtype=np.int64)
+    P.sf_pts = np.concatenate(fpts).reshape(-1, 3) if fpts else P.sf_pts
+    P.sf_ptr = np.asarray(fptr, dtype=np.int64)
+    return P
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_arbitrary_rules(cf, cutgen_mod, p):
+    N = {1: 8, 2: 7, 3: 6, 4: 5, 5: 4, 6: 3, 7: 3, 8: 3}[p]
+    P = randomize_rules(cutgen_mod.generate(cutgen_mod.SPHERE, N, -1.0, 1.0, p), seed=100 + p)
+    u = P.seeded_u(p + 40)
+    v, _ = gpu_apply(cf, P, u)
+    check(P, v, u)
+    for mask in ((1, 2, 4, 8) if p <= 4 else (2,)):
+        v, _ = gpu_apply(cf, P, u, mask)
+        check(P, v, u, mask)
+
+
+def _sample(P, rng, k):
+    cut = np.where(P.is_cut.astype(bool))[0]
+    unc = np.where(~P.is_cut.astype(bool))[0]
+    ijk = P.active_ijk
+    nmax = np.asarray(P.n_cells) - 1
+    bnd = np.where(np.any((ijk == 0) | (ijk == nmax), axis=1))[0]
+    out = list(rng.choice(cut, k, replace=False)) + list(rng.choice(unc, k, replace=False))
+    if bnd.size:
+        out += list(rng.choice(bnd, min(k // 2, bnd.size), replace=False))
+    return sorted(set(int(b) for b in out))
+
+
+@pytest.mark.parametrize("cfg,deg,k", [("C5", None, 12), ("C4", None, 12), ("C3", 8, 8), ("C3", 4, 12)])
+def test_full_size_sampled_blocks_more(cf, cutgen_mod, cfg, deg, k):
+    """BASELINE configs[4] (gyroid p = 5, incl. box-boundary cells), configs[3]
+    (192^3, 84M DoFs) and the p = 8 / p = 4 sweep meshes, in the launch configuration
+    bench.py times: sampled output blocks against the oracle, per block (A18)."""
+    P = cutgen_mod.config(cfg, degree=deg)
+    u = P.seeded_u(1)
+    op = cf.CutFEM(P)
+    ud = torch.from_numpy(u).cuda()
+    v = op.apply(ud).cpu().numpy()
+    blocks = _sample(P, np.random.default_rng(7), k)
+    check(P, v, u, blocks=blocks)
+    del op, ud
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("p", [7, 8])
+def test_multi_tile_high_degree(cf, cutgen_mod, p):
+    """p = 7 (k_uncw<8>: 4-cell tiles) and p = 8 (k_uncut<9>) with several tiles /
+    CTAs of uncut cells, plain and next to cut cells: the whole operator."""
+    P = cutgen_mod.generate(cutgen_mod.SPHERE, 8, -1.0, 1.0, p)
+    u = P.seeded_u(50 + p)
+    v, op = gpu_apply(cf, P, u)
+    assert op.stats()["n_uncut"] >= 30
+    # every uncut cell (all tiles) and a sample of cut cells, per block
+    unc = np.where(~P.is_cut.astype(bool))[0]
+    cut = np.random.default_rng(p).choice(np.where(P.is_cut.astype(bool))[0], 8, replace=False)
+    check(P, v, u, blocks=sorted(set(unc.tolist()) | set(cut.tolist())))
+
+
+def test_cg_odd_length(cf, cutgen_mod):
+    """CG with an odd number of DoFs (odd p + 1 cubed times an odd cell count): the
+    vector kernels' tail entry."""
+    for N in range(6, 16):
+        P = cutgen_mod.generate(cutgen_mod.SPHERE, N, -1.0, 1.0, 2)
+        if P.n_dofs % 2 == 1:
+            break
+    assert P.n_dofs % 2 == 1
+    from oracle.operator import cg as oracle_cg
+    op = cf.CutFEM(P)
+    b = op.rhs_const(1.0)
+    x, hist = op.cg(b, iters=25)
+    xo, _ = oracle_cg(Oracle(P).apply, b.cpu().numpy(), tol=0.0, maxiter=25)
+    xg = x.cpu().numpy()
+    assert np.abs(xg - xo).max() <= 1e-8 * np.abs(xo).max()
+    r = b - op.apply(x)
+    assert abs(float(r.norm()) - hist[-1]) <= 1e-8 * hist[0]
+
+
+def test_misaligned_pointer_rejected(cf, cutgen_mod):
+    P = cutgen_mod.config("C1")
+    op = cf.CutFEM(P)
+    buf = torch.zeros(P.n_dofs + 2, dtype=torch.float64, device="cuda")
+    with pytest.raises(RuntimeError, match="16-byte"):
+        op.apply(buf[1:P.n_dofs + 1])
+
+
+@pytest.mark.parametrize("p,nparts", [(2, 2), (3, 3), (5, 2)])
+def test_nccl_loopback_halo(cf, cutgen_mod, p, nparts):
+    """The NCCL halo exchange on a real (1-rank) communicator: every slab's handle
+    receives its ghost planes through ncclSend/ncclRecv to itself on the comm stream,
+    overlapped with its interior cells; the result equals the global apply bit for
+    bit (same arithmetic per cell)."""
+    P = cutgen_mod.generate(cutgen_mod.SPHERE, 12, -1.0, 1.0, p)
+    nd = (p + 1) ** 3
+    ug = P.seeded_u(2).reshape(-1, nd)
+    vg = cf.CutFEM(P).apply(torch.from_numpy(ug.reshape(-1)).cuda()).cpu().numpy().reshape(-1, nd)
+    xs = cf.partition_x(P, nparts, 7.0)
+    out = np.zeros_like(vg)
+    for r in range(nparts):
+        L = cf.LocalProblem(P, xs[r], xs[r + 1])
+        d = cf.CutFEMDist(P, xs[r], xs[r + 1])
+        lo0, hi0 = L.global_begin - L.n_ghost_lo, L.global_begin + L.n_own
+        src_lo = torch.from_numpy(ug[lo0:L.global_begin].reshape(-1).copy()).cuda()
+        src_hi = torch.from_numpy(ug[hi0:hi0 + L.n_ghost_hi].reshape(-1).copy()).cuda()
+        d.debug_loopback(src_lo, src_hi)
+        ue = torch.full((L.n_active * nd,), np.nan, dtype=torch.float64, device="cuda")  # ghosts must arrive
+        ue[:L.n_own * nd] = torch.from_numpy(ug[L.global_begin:hi0].reshape(-1)).cuda()
+        v = d.apply(ue).cpu().numpy().reshape(-1, nd)
+        assert np.array_equal(ue[L.n_own * nd:L.n_own * nd + L.n_ghost_lo * nd].cpu().numpy(),
+                              src_lo.cpu().numpy())
+        out[L.global_begin:hi0] = v
+    assert np.array_equal(out, vg)
+
+
+def test_nccl_loopback_cg_allreduce(cf, cutgen_mod):
+    """cutfem_cg on a 1-slab loopback handle: each dot goes through ncclAllReduce
+    on the 1-rank communicator; the iterates equal the plain handle's bit for bit."""
+    P = cutgen_mod.config("C1")
+    op = cf.CutFEM(P)
+    b = op.rhs_const(1.0)
+    x0, h0 = op.cg(b, iters=20)
+    d = cf.CutFEMDist(P, 0, P.n_cells[0])
+    d.debug_loopback(None, None)
+    x1, h1 = d.cg(b, iters=20)
+    assert torch.equal(x0[:P.n_dofs], x1[:P.n_dofs]) and np.array_equal(h0, h1)
