@@ -67,6 +67,10 @@ struct cutfem_handle {
   int64_t ghost_lo = 0, ghost_hi = 0;      // ghost blocks after the owned ones
   int64_t plane_lo = 0, plane_hi = 0;      // owned blocks of the first / last owned plane
   void *comm = nullptr;                    // ncclComm_t
+  // test-only NCCL loopback (cutfem_debug_loopback): a 1-rank communicator whose
+  // halo exchange sends these caller buffers to itself into the ghost slots
+  bool loopback = false;
+  const double *lb_lo = nullptr, *lb_hi = nullptr;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_comm = nullptr, ev_comm_fork = nullptr;
   int sm_count = 148;
@@ -97,6 +101,7 @@ struct cutfem_handle {
   int32_t *d_line_srf = nullptr;  // k_cut line cells: interface point on each line (-1 none)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_started = nullptr;  // k_cutp launch completion (all CTAs begun)
   // host path buffers
   double *d_u = nullptr, *d_v = nullptr;
   // CSR
@@ -441,37 +446,34 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
           c.nb[f] = d.nb[f];
           if (d.nb[f] >= 0) nbm |= 1u << f;
         }
-        // K1_GP (n = 4): the ghost penalty of cells next to cut cells rides in k_tile2
-        constexpr bool k1gp = N == 4 && K1_GP;
-        c.gp = k1gp ? (d.flags & nbm & 0x3fu) : 0u;
+        // set 0 (k_tile2): cells without ghost-penalty faces; set 1 (k_uncw<4>): the
+        // cells next to cut cells, every structured term (volume, SIPG, GP).  The two
+        // sets and k_cutp's cut cells are disjoint: no kernel reads another's v.
+        c.gp = d.flags & nbm & 0x3fu;
         c.sipg = nbm;  // faces of an uncut cell are inside the domain: full SIPG
         c.vol = true;
-        set[0][pt - 1].push_back(c);
-        if (!k1gp && (d.flags & nbm & 0x3fu)) {
-          c.gp = d.flags & nbm & 0x3fu;
-          c.sipg = 0;
-          c.vol = false;
-          set[1][pt - 1].push_back(c);
+#if STRUCT4_GPW
+        if (c.gp) {
+          TCell g = c;
+          g.sipg = 0;
+          g.vol = false;
+          set[1][pt - 1].push_back(g);
         }
+        c.gp = 0;
+        set[0][pt - 1].push_back(c);
+#else
+        set[c.gp ? 1 : 0][pt - 1].push_back(c);
+#endif
       }
-    for (int64_t i = hd->r_off[pt][2]; i < hd->r_off[pt][2] + hd->r_cnt[pt][2]; ++i) {
-      const CDesc &d = cd[i];
-      TCell c;
-      c.blk = d.blk;
-      uint32_t nbm = 0;
-      for (int f = 0; f < 6; ++f) {
-        c.nb[f] = d.nb[f];
-        if (d.nb[f] >= 0) nbm |= 1u << f;
-      }
-      c.gp = d.flags & nbm & 0x3fu;
-      c.sipg = (d.flags >> 6) & nbm & 0x3fu;  // structured (full, uncut) faces of the cut cell
-      c.vol = false;
-      // (cut cells: k_cutp does their structured faces itself)
-    }
+
   }
-  // set 0: k_tile* tiles (TileCfg<N>; k_tile2 at n = 4: Tile2Cfg<4>::T); set 1: k_gpw
-  // tiles (smaller, GpwCfg<N>::T).  Offsets are in BYTES (the record sizes differ).
+  // set 0: k_tile2 tiles (Tile2Cfg<4>::T); set 1: k_uncw<4> tiles (TileCfg<4>).
+  // Offsets are in BYTES.
+#if STRUCT4_GPW
   using CG = typename GpwCfg<N>::T;
+#else
+  using CG = C;
+#endif
   using CK = typename std::conditional<N == 4, typename Tile2Cfg<4>::T, C>::type;
   std::vector<char> all;
   // (n <= 3: the uncut cells run k_cell from their descriptors; no tiles)
@@ -758,9 +760,15 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     using C2 = Tile2Cfg<N>;
     CU(cudaFuncSetAttribute(k_tile2<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_tile2<N, 0>, C2::THREADS, C2::SMEM));
+#if STRUCT4_GPW
     CU(cudaFuncSetAttribute(k_gpw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, GpwCfg<N>::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_gpw<N>, GpwCfg<N>::THREADS,
                                                      GpwCfg<N>::SMEM));
+#else
+    CU(cudaFuncSetAttribute(k_uncw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncwCfg<N>::SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_uncw<N>, UncwCfg<N>::THREADS,
+                                                     UncwCfg<N>::SMEM));
+#endif
   }
   for (int k = 0; k < 3; ++k) hd->occ_tile[k] = std::max(1, hd->occ_tile[k]);
   return 0;
@@ -824,73 +832,101 @@ int dispatch_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vecto
   return 0;
 }
 
-// N <= 4: k_cutp (cut cells: every term, v = ...) on the side stream,
-// concurrently with k_tile*<0> (uncut cells: volume + SIPG, v = ...) followed by
-// k_gpw (uncut cells next to cut cells: + ghost penalty, v += ...).
+// Launch on `st`; pdl: with the programmatic-serialization attribute (the kernel may
+// start once every CTA of the previous kernel in the stream has begun; see pdl_trigger).
+template <typename... KArgs, typename... Args>
+int launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st, bool pdl,
+             Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? at : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  CU(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+  return 0;
+}
+
+// N <= 4, one stream: k_cutp (cut cells, every term, v = ...; normal launch), then
+// the uncut cells -- k_cell (n <= 3), or k_tile2 (cells without ghost-penalty faces,
+// volume + SIPG) and k_uncw<4> (the cells next to cut cells, every term) -- each
+// v = ... on disjoint blocks, launched as programmatic dependents (kernels.cuh
+// pdl_trigger): they start only once all of k_cutp's CTAs have begun (k_cutp, the long
+// pole, holds its SM slots first; two free-running streams let the uncut kernels take
+// the SMs first in some applies: the r1 slow steps) and fill the slots its warps free.
 template <int N>
 int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int which, int part) {
   constexpr int NT = (N <= 4 ? N : 4);
-  using C = TileCfg<NT>;
   const int64_t nc = (which & 2) ? hd->r_cnt[part][2] : 0;
   const int64_t n0 = (which & 1) ? hd->t_cnt[0][part] : 0;
-  const int64_t n1 = ((which & 1) && (hd->kp.mask & (TERM_GP | TERM_SIPG))) ? hd->t_cnt[1][part] : 0;
-  const bool fork = nc > 0 && n0 > 0;
-  if (fork) {
-    CU(cudaEventRecord(hd->ev_fork, st));
-    CU(cudaStreamWaitEvent(hd->side, hd->ev_fork, 0));
-  }
-  auto launch_cut = [&]() -> int {
-    if (nc <= 0) return 0;
+  const int64_t n1 = (which & 1) ? hd->t_cnt[1][part] : 0;
+  const int64_t ncell = (which & 1) ? hd->r_cnt[part][0] + hd->r_cnt[part][1] : 0;
+  bool pdl = false;  // the first kernel of the apply is a normal launch
+  int rc;
+  if (nc > 0) {
     using CP = CutPCfg<NT>;
     // part 0 = the interior list then the slab-boundary list (each with its own warp schedule)
     for (int pt = 1; pt <= 2; ++pt) {
       if (part != 0 && part != pt) continue;
       if (hd->grid_cutp[pt] <= 0) continue;
-      k_cutp<NT><<<hd->grid_cutp[pt], 32 * CP::WARPS, CP::SMEM, fork ? hd->side : st>>>(
-          u, v, hd->d_cdesc2 + hd->r_off[pt][2], hd->d_chunks, hd->d_stream,
-          hd->d_wstart + hd->w_off[pt], hd->d_kstart + hd->w_off[pt], hd->kp,
-          *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data()));
+      if ((rc = launch_k(k_cutp<NT>, (unsigned)hd->grid_cutp[pt], 32 * CP::WARPS, CP::SMEM, st, pdl, u, v,
+                         hd->d_cdesc2 + hd->r_off[pt][2], hd->d_chunks, hd->d_stream, hd->d_wstart + hd->w_off[pt],
+                         hd->d_kstart + hd->w_off[pt], hd->kp, *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data()))))
+        return rc;
+      pdl = true;
     }
-    CU(cudaGetLastError());
-    return 0;
-  };
-  int rc;
-  if ((rc = launch_cut())) return rc;
+  }
   const TileTab<NT> &tt = *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data());
   const char *tb = reinterpret_cast<const char *>(hd->d_tiles);  // byte offsets per set
   if constexpr (NT <= 3) {
     // p = 1, 2: one thread per uncut cell (plain cells, then the cells next to cut cells)
     const int64_t np = hd->r_cnt[part][0], ng = hd->r_cnt[part][1];
-    if ((which & 1) && np + ng > 0) {
-      k_cell<NT><<<(unsigned)(((np + ng) * CELL_TPC + 127) / 128), 128, 0, st>>>(
-          u, v, hd->d_udesc + hd->r_off[part][0], (int)np, hd->d_udesc + hd->r_off[part][1], (int)ng, tt,
-          hd->kp.mask);
-      CU(cudaGetLastError());
-    }
-    if (fork) {
-      CU(cudaEventRecord(hd->ev_join, hd->side));
-      CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
-    }
-    return 0;
+    if (ncell > 0 && (rc = launch_k(k_cell<NT>, (unsigned)(((np + ng) * CELL_TPC + 127) / 128), 128, 0, st, pdl, u, v,
+                                    hd->d_udesc + hd->r_off[part][0], (int)np, hd->d_udesc + hd->r_off[part][1],
+                                    (int)ng, tt, hd->kp.mask)))
+      return rc;
   } else {
-  if (n0 > 0) {
-    const unsigned grid = (unsigned)std::min<int64_t>(n0, (int64_t)hd->occ_tile[0] * hd->sm_count);
-    const auto *t0 = reinterpret_cast<const TileRec<Tile2Cfg<NT>::SMAX> *>(tb + hd->t_off[0][part]);
-    k_tile2<NT, 0><<<grid, Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st>>>(u, v, t0, (int)n0, tt, hd->kp.mask);
-    CU(cudaGetLastError());
-  }
-  if (n1 > 0) {  // uncut cells next to cut cells: + ghost penalty (after k_tile2's v = ...)
-    const unsigned grid = (unsigned)std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count);
-    k_gpw<NT><<<grid, GpwCfg<NT>::THREADS, GpwCfg<NT>::SMEM, st>>>(
-        u, v, reinterpret_cast<const TileRec<GpwCfg<NT>::SMAX> *>(tb + hd->t_off[1][part]), (int)n1, tt, hd->kp.mask);
-    CU(cudaGetLastError());
-  }
-  if (fork) {
-    CU(cudaEventRecord(hd->ev_join, hd->side));
-    CU(cudaStreamWaitEvent(st, hd->ev_join, 0));
+#ifdef CUTFEM_UNCW_FIRST
+    if (n1 > 0) {  // cells next to cut cells: volume + SIPG + ghost penalty
+      const unsigned grid = (unsigned)std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count);
+      const auto *t1 = reinterpret_cast<const TileRec<TileCfg<NT>::SMAX> *>(tb + hd->t_off[1][part]);
+      if ((rc = launch_k(k_uncw<NT>, grid, UncwCfg<NT>::THREADS, UncwCfg<NT>::SMEM, st, pdl, u, v, t1, (int)n1, tt,
+                         hd->kp.mask)))
+        return rc;
+      pdl = true;
+    }
+    const int64_t n1x = 0;
+#else
+    const int64_t n1x = n1;
+#endif
+    if (n0 > 0) {  // cells without ghost-penalty faces: volume + SIPG
+      const unsigned grid = (unsigned)std::min<int64_t>(n0, (int64_t)hd->occ_tile[0] * hd->sm_count);
+      const auto *t0 = reinterpret_cast<const TileRec<Tile2Cfg<NT>::SMAX> *>(tb + hd->t_off[0][part]);
+      if ((rc = launch_k(k_tile2<NT, 0>, grid, Tile2Cfg<NT>::THREADS, Tile2Cfg<NT>::SMEM, st, pdl, u, v, t0, (int)n0,
+                         tt, hd->kp.mask)))
+        return rc;
+      pdl = true;
+    }
+    if (n1x > 0) {  // cells next to cut cells: volume + SIPG + ghost penalty
+      const unsigned grid = (unsigned)std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count);
+#if STRUCT4_GPW
+      const auto *t1 = reinterpret_cast<const TileRec<GpwCfg<NT>::SMAX> *>(tb + hd->t_off[1][part]);
+      if ((rc = launch_k(k_gpw<NT>, grid, GpwCfg<NT>::THREADS, GpwCfg<NT>::SMEM, st, pdl, u, v, t1, (int)n1, tt,
+                         hd->kp.mask)))
+        return rc;
+#else
+      const auto *t1 = reinterpret_cast<const TileRec<TileCfg<NT>::SMAX> *>(tb + hd->t_off[1][part]);
+      if ((rc = launch_k(k_uncw<NT>, grid, UncwCfg<NT>::THREADS, UncwCfg<NT>::SMEM, st, pdl, u, v, t1, (int)n1, tt,
+                         hd->kp.mask)))
+        return rc;
+#endif
+    }
   }
   return 0;
-  }
 }
 
 // which: bit0 structured (uncut) kernels, bit1 unstructured (cut) kernel; part:
@@ -1040,6 +1076,7 @@ void free_handle(cutfem_handle *hd) {
   if (hd->ev_comm_fork) cudaEventDestroy(hd->ev_comm_fork);
   if (hd->ev_fork) cudaEventDestroy(hd->ev_fork);
   if (hd->ev_join) cudaEventDestroy(hd->ev_join);
+  if (hd->ev_started) cudaEventDestroy(hd->ev_started);
   delete hd;
 }
 
@@ -1327,6 +1364,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   CU(cudaStreamCreateWithFlags(&hd->side, cudaStreamNonBlocking));
   CU(cudaEventCreateWithFlags(&hd->ev_fork, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&hd->ev_join, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&hd->ev_started, cudaEventDisableTiming));
   cutfem_stats_t &s = hd->stats;
   std::memset(&s, 0, sizeof(s));
   s.n_active = hd->n_own;

@@ -225,6 +225,18 @@ struct BlkU {
   }
 };
 
+// ---- programmatic dependent launch (griddepcontrol, sm_90+).  An apply at p <= 3 is
+// ONE stream: k_cutp (normal launch) -> uncut-cell kernel(s) launched with the
+// programmatic-serialization attribute.  Every CTA triggers its dependents at its
+// start, so a dependent grid is released only once ALL k_cutp CTAs have begun (k_cutp,
+// the long pole, holds its SM slots first) and then fills the slots k_cutp's warps
+// free.  The dependents never read what their primary writes (disjoint v blocks), so
+// they do not wait up front; one CTA of each dependent waits at its END, which makes
+// the dependent grid complete only after its primary has completed (transitively the
+// whole apply), so stream order after the apply holds.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // ---- mbarrier + cp.async.bulk (TMA bulk copy, SASS UBLKCP) helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {

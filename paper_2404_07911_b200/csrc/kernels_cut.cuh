@@ -382,6 +382,10 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // warp gw owns cells [wstart[gw], wstart[gw+1]) and their packets [pstart[gw], pstart[gw+1])
   // (longest-processing-time assignment computed at setup, heaviest first)
+  pdl_trigger();  // every CTA of k_cutp has begun -> the uncut-cell kernels may start
+  // a k_cutp launched behind another one (interior + boundary lists) completes only
+  // after it (no-op for the apply's first, normally launched kernel)
+  if (blockIdx.x == 0 && threadIdx.x == 0) pdl_wait();
   const int gw = blockIdx.x * C::WARPS + warp;
   const int c0w = wstart[gw], c1w = wstart[gw + 1];
   if (c0w >= c1w) return;

@@ -1,5 +1,5 @@
 // Structured (uncut) cells in registers (included by kernels.cuh): k_tile2 (n = 4),
-// k_gpw (n = 4, ghost penalty), k_uncw (n = 5, 6, 8), k_cell (n = 2, 3).
+// k_uncw (n = 4: the cells next to cut cells; n = 5, 6, 8: all), k_cell (n = 2, 3).
 //
 // Why: the line-per-lane kernels sweep every 1-D line through shared memory,
 // i.e. one shared-memory access per FMA; the FP64 pipe needs ~4 FMAs per
@@ -41,12 +41,12 @@
 #define TILE8_SMAX 36  // slots of an 8-cell tile (a full 2x2x2 brick needs 32; merged partial bricks
                        // more; 32 measured: k_uncw<6> 3 CTAs/SM instead of 2, same time)
 #endif
-#ifndef GPW_TC4
-#define GPW_TC4 8  // cells per k_gpw tile at n = 4 (4 measured neutral at C2)
+#ifndef STRUCT4_GPW
+#define STRUCT4_GPW 0  // n = 4 uncut cells: 0 = k_tile2 (plain cells) + k_uncw<4> (cells next to cut
+                       // cells); 1 = k_tile2 (all, volume + SIPG) then k_gpw (+ ghost penalty)
 #endif
-#ifndef K1_GP
-#define K1_GP 0  // k_tile2<4,0> adds the uncut cells' ghost penalty itself (no k_gpw for them);
-                 // measured: structured 40 -> 70 us at C2 (spills), so k_gpw stays
+#ifndef GPW_TC4
+#define GPW_TC4 8
 #endif
 #ifndef K1_TC
 #define K1_TC 32  // cells per k_tile2 tile (16 measured: structured 40 -> 42 us, apply 109 -> 150 us at C2)
@@ -321,10 +321,8 @@ __device__ __forceinline__ TileLane tile_lane(const TileRec<SMAX> *T, int cell, 
   return r;
 }
 
-// MODE 0: volume (per-lane bit) + SIPG (per-face bits) of uncut cells, v = result.
-// MODE 1: ghost penalty (per-face bits) of uncut cells next to cut cells, v += result.
-// MODE 2: ghost penalty + SIPG of the structured faces of cut cells, v = result
-//         (v is then a scratch vector, added by k_addcut once k_cutp has written).
+// MODE 0 (the only one): volume (per-lane bit) + SIPG (per-face bits) of uncut cells
+// without ghost-penalty faces, v = result.
 // Lane flags: lane_nb[l][1] byte 2 = GP faces, byte 3 = SIPG faces | volume << 6.
 template <int N, int MODE>
 __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__ u, double *__restrict__ v,
@@ -335,7 +333,7 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
   constexpr int P = C::P, NN = C::NN, N3 = C::N3, NP = C::NP, ST = C::ST;
   static_assert(C::SMAX <= 2 * C::THREADS, "two slot copies per thread");
   extern __shared__ __align__(16) double smem[];
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);  // [0] tile blocks, [1] v blocks (MODE 1)
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);  // [0] tile blocks
   double *S = smem + 2;
   const int tid = threadIdx.x, lane = tid & 31;
   const int cell = 16 * (tid >> 5) + (lane & 15), h = lane >> 4;
@@ -343,6 +341,7 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
   // the thread's frame: plane cc of the half is physical plane zb + zs cc; z position m at zb + zs m
   const int zb = h ? NN * (N - 1) : 0, zs = h ? -NN : NN;
   TL_BEGIN(1);
+  pdl_trigger();
   if (tid == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
@@ -387,8 +386,9 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
     const double *Nb[6];
 #pragma unroll
     for (int f = 0; f < 6; ++f) Nb[f] = nbs[f] != 0xff ? S + nbs[f] * ST : Us;  // dummy source when absent
-    if (on || MODE != 0) {
-      if constexpr (MODE == 0) {
+    static_assert(MODE == 0, "k_tile2: volume + SIPG only");
+    if (on) {
+      {
         const double ev = vol ? 1.0 : 0.0;
         // x and y: plane-local
         static_for<0, 2>([&](auto dc) {
@@ -410,52 +410,6 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
           z_line<N>(w, t, u0, a0, ev, el, act, tt);
           z_line<N>(w, t + 1, u1, a1, ev, el, act, tt);
         }
-      }
-    }
-    // ghost penalty (+ structured SIPG in MODE 1), face by face, skipped when no lane of
-    // the warp has it.  MODE 0 with K1_GP: the uncut cells' ghost penalty is added here
-    // from the tile already in shared memory (no separate k_gpw pass); every lane of the
-    // warp takes part (the votes), lanes without the face contribute zero.
-    if constexpr (MODE != 0 || K1_GP) {
-      {
-        static_for<0, 6>([&](auto fc) {
-          constexpr int F = decltype(fc)::value, D = F / 2, SS = F % 2;
-          const bool g = (gpb >> F) & 1u, sp = MODE != 0 && ((spb >> F) & 1u);
-          const bool anyg = __any_sync(0xffffffffu, g), anys = __any_sync(0xffffffffu, sp);
-          if (!(anyg || anys)) return;
-          const double eg = g ? 1.0 : 0.0, es = sp ? 1.0 : 0.0;
-          const double *Nf = Nb[F];
-          if constexpr (D < 2) {
-#pragma unroll
-            for (int cc = 0; cc < P; ++cc) {
-              const int pz = zb + zs * cc;
-#pragma unroll
-              for (int q = 0; q < N; ++q) {
-                double uo[N], un[N];
-                ld_line<N, D>(Us + pz, q, uo);
-                ld_line<N, D>(Nf + pz, q, un);
-                if (anys) sipg_line<N, D, SS>(w, q + N * cc, uo, un, es, tt);
-                if (anyg)
-                  gp_rows<N, SS, 0, N>(w, [&](int m) { return lix<N, D>(q + N * cc, m); }, uo, un, eg, tt);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int t = 0; t < NN; t += 2) {
-              double u0[N], u1[N], a0[N], a1[N];
-              ld_zpair<N>(Us, t, zb, zs, u0, u1);
-              ld_zpair<N>(Nf, t, zb, zs, a0, a1);
-              if (anys) {
-                zsipg_line<N, SS>(w, t, u0, a0, es, tt);
-                zsipg_line<N, SS>(w, t + 1, u1, a1, es, tt);
-              }
-              if (anyg) {
-                gp_rows<N, SS, 0, P>(w, [&](int m) { return t + NN * m; }, u0, a0, eg, tt);
-                gp_rows<N, SS, 0, P>(w, [&](int m) { return t + 1 + NN * m; }, u1, a1, eg, tt);
-              }
-            }
-          }
-        });
       }
     }
     __syncthreads();  // every thread is done reading the tile's blocks
@@ -518,11 +472,6 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
           ob[c] = __shfl_sync(0xffffffffu, cu.myblk, g + c);
           if (g + c < ncw) {
             x[c] = *reinterpret_cast<const double2 *>(S + (c0 + g + c) * ST + 2 * lane);
-            if constexpr (MODE == 1) {
-              const double2 o = *reinterpret_cast<const double2 *>(v + (size_t)ob[c] * N3 + 2 * lane);
-              x[c].x += o.x;
-              x[c].y += o.y;
-            }
           }
         }
 #pragma unroll
@@ -533,8 +482,10 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
   }
 
   TL_END(1);
+  if (blockIdx.x == 0) pdl_wait();  // complete only after the primary (k_cutp) has
 }
 
+#if STRUCT4_GPW
 // ===================================================================== k_gpw
 // k_gpw<N> (N <= 4): ghost penalty of every cell next to a cut cell plus the
 // full-face SIPG of the cut cells (their faces shared with uncut cells),
@@ -572,6 +523,8 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
   constexpr int TPC = C::TPC, CPW = C::CPW;
   const int tid = threadIdx.x, cell = tid / TPC, r = tid % TPC;
   const bool sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
+  pdl_trigger();
+  pdl_wait();  // v += ...: k_tile2 (the primary) must have written v
   if (C::BULK && tid == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
@@ -733,10 +686,12 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
 }
 
 
+#endif
+
 // ===================================================================== k_uncw
 // k_uncw<N> (N = 5..9): uncut cells at high degree, every structured term (volume,
 // SIPG on all faces, ghost penalty on faces to cut cells), v = result.  The same
-// w-space arithmetic as k_tile2, organised like k_gpw (runtime line loops, w in
+// w-space arithmetic as k_tile2, organised for small code (runtime line loops, w in
 // shared memory, small code): TPC threads per cell take every TPC-th line; the
 // volume line operator and both faces of an axis touch the same lines, so only a
 // __syncwarp separates the axes.
@@ -763,6 +718,8 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
   double *Wb = S + TC_::SMAX * ST;
   const int tid = threadIdx.x, cell = tid / TPC, r = tid % TPC;
   const bool cell_on = (mask & TERM_CELL) != 0, sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
+  pdl_trigger();
+  TL_BEGIN(2);
   if (TC_::BULK && tid == 0) {
     mbar_init(bar, 1);
     mbar_fence_init();
@@ -904,6 +861,8 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
       v[(size_t)T->blk[c] * N3 + l] = Wb[c * WST + l];
     }
   }
+  TL_END(2);
+  if (blockIdx.x == 0) pdl_wait();  // complete only after the primary grid has
 }
 
 // ===================================================================== k_cell
@@ -950,6 +909,8 @@ __global__ void __launch_bounds__(128) k_cell(const double *__restrict__ u, doub
   // CELL_TPC = 2: a cell on a thread pair, faces 0-2 / 3-5 (halving each thread's chain of
   // dependent neighbour loads), w summed by one __shfl_xor per value
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, i = gt / TPC, part = gt % TPC;
+  // CTA 0 completes only after the primary (k_cutp) has: the apply's end in stream order
+  if (blockIdx.x == 0 && threadIdx.x == 0) pdl_wait();
   if (TPC == 1 && i >= n0 + n1) return;
   const bool valid = i < n0 + n1;  // (TPC = 2: every thread stays for the shuffles)
   const int ic = valid ? i : 0;

@@ -20,7 +20,7 @@ L.cutfem_debug_timeline.argtypes = [ctypes.c_int, ctypes.c_void_p]
 u = torch.from_numpy(P.seeded_u(0)).cuda()
 v = torch.empty_like(u)
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-names = {0: "k_cutp", 1: "k_tile2", 2: "k_gpw"}
+names = {0: "k_cutp", 1: "k_tile2", 2: "k_uncw"}
 for rep in range(4):
     flush.zero_()
     torch.cuda.synchronize()
