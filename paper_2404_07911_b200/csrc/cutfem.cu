@@ -462,7 +462,11 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         c.gp = 0;
         set[0][pt - 1].push_back(c);
 #else
+#ifdef UNCW4_ALL
+        set[1][pt - 1].push_back(c);
+#else
         set[c.gp ? 1 : 0][pt - 1].push_back(c);
+#endif
 #endif
       }
 
@@ -472,7 +476,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
 #if STRUCT4_GPW
   using CG = typename GpwCfg<N>::T;
 #else
-  using CG = C;
+  using CG = typename std::conditional<N == 4, TileCfgX<N, UNCW4_TC>, C>::type;
 #endif
   using CK = typename std::conditional<N == 4, typename Tile2Cfg<4>::T, C>::type;
   std::vector<char> all;
@@ -765,9 +769,9 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_gpw<N>, GpwCfg<N>::THREADS,
                                                      GpwCfg<N>::SMEM));
 #else
-    CU(cudaFuncSetAttribute(k_uncw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncwCfg<N>::SMEM));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_uncw<N>, UncwCfg<N>::THREADS,
-                                                     UncwCfg<N>::SMEM));
+    using CU4 = UncwCfg<N, UNCW4_TC>;
+    CU(cudaFuncSetAttribute(k_uncw<N, UNCW4_TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, CU4::SMEM));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_uncw<N, UNCW4_TC>, CU4::THREADS, CU4::SMEM));
 #endif
   }
   for (int k = 0; k < 3; ++k) hd->occ_tile[k] = std::max(1, hd->occ_tile[k]);
@@ -893,9 +897,9 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
 #ifdef CUTFEM_UNCW_FIRST
     if (n1 > 0) {  // cells next to cut cells: volume + SIPG + ghost penalty
       const unsigned grid = (unsigned)std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count);
-      const auto *t1 = reinterpret_cast<const TileRec<TileCfg<NT>::SMAX> *>(tb + hd->t_off[1][part]);
-      if ((rc = launch_k(k_uncw<NT>, grid, UncwCfg<NT>::THREADS, UncwCfg<NT>::SMEM, st, pdl, u, v, t1, (int)n1, tt,
-                         hd->kp.mask)))
+      const auto *t1 = reinterpret_cast<const TileRec<TileCfgX<NT, UNCW4_TC>::SMAX> *>(tb + hd->t_off[1][part]);
+      if ((rc = launch_k(k_uncw<NT, UNCW4_TC>, grid, UncwCfg<NT, UNCW4_TC>::THREADS, UncwCfg<NT, UNCW4_TC>::SMEM, st,
+                         pdl, u, v, t1, (int)n1, tt, hd->kp.mask)))
         return rc;
       pdl = true;
     }
@@ -919,9 +923,9 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
                          hd->kp.mask)))
         return rc;
 #else
-      const auto *t1 = reinterpret_cast<const TileRec<TileCfg<NT>::SMAX> *>(tb + hd->t_off[1][part]);
-      if ((rc = launch_k(k_uncw<NT>, grid, UncwCfg<NT>::THREADS, UncwCfg<NT>::SMEM, st, pdl, u, v, t1, (int)n1, tt,
-                         hd->kp.mask)))
+      const auto *t1 = reinterpret_cast<const TileRec<TileCfgX<NT, UNCW4_TC>::SMAX> *>(tb + hd->t_off[1][part]);
+      if ((rc = launch_k(k_uncw<NT, UNCW4_TC>, grid, UncwCfg<NT, UNCW4_TC>::THREADS, UncwCfg<NT, UNCW4_TC>::SMEM, st,
+                         pdl, u, v, t1, (int)n1, tt, hd->kp.mask)))
         return rc;
 #endif
     }

@@ -48,6 +48,9 @@
 #ifndef GPW_TC4
 #define GPW_TC4 8
 #endif
+#ifndef UNCW4_TC
+#define UNCW4_TC 8  // cells per k_uncw<4> tile (the cells next to cut cells at n = 4)
+#endif
 #ifndef K1_TC
 #define K1_TC 32  // cells per k_tile2 tile (16 measured: structured 40 -> 42 us, apply 109 -> 150 us at C2)
 #endif
@@ -695,21 +698,22 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
 // shared memory, small code): TPC threads per cell take every TPC-th line; the
 // volume line operator and both faces of an axis touch the same lines, so only a
 // __syncwarp separates the axes.
-template <int N>
+template <int N, int TCN = TileCfg<N>::TC>
 struct UncwCfg {
+  using T = TileCfgX<N, TCN>;
   static constexpr int N3 = N * N * N, NN = N * N;
-  static constexpr int TC = TileCfg<N>::TC, TPC = 128 / TC;
+  static constexpr int TC = TCN, TPC = 128 / TC;
   static constexpr int WST = N3 + ((N3 & 1) ? 0 : 1);  // odd: consecutive cells on different banks
   static constexpr int THREADS = 128;
-  static constexpr int SMEM = TileCfg<N>::SMEM + TC * WST * 8;
+  static constexpr int SMEM = T::SMEM + TC * WST * 8;
 };
 
-template <int N>
+template <int N, int TCN = TileCfg<N>::TC>
 __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, double *__restrict__ v,
-                                              const TileRec<TileCfg<N>::SMAX> *__restrict__ tiles, int ntiles,
+                                              const TileRec<TileCfgX<N, TCN>::SMAX> *__restrict__ tiles, int ntiles,
                                               TileTab<N> tt, uint32_t mask) {
-  using TC_ = TileCfg<N>;
-  using C = UncwCfg<N>;
+  using TC_ = TileCfgX<N, TCN>;
+  using C = UncwCfg<N, TCN>;
   constexpr int NN = C::NN, N3 = C::N3, ST = TC_::ST, WST = C::WST, TPC = C::TPC;
   static_assert(32 % TPC == 0, "a cell's threads in one warp");
   extern __shared__ __align__(16) double smem[];
