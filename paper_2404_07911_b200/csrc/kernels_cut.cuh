@@ -364,7 +364,11 @@ struct CutPCfg {
   static constexpr int OFF_WS = OFF_RING + NB * RSLOT;  // w of the structured faces (n^3)
   static constexpr int OFF_RED = OFF_WS + ((N3 + 1) & ~1);  // reduction transpose [RW][33]
   static constexpr int RW = ACC < CUTP_RW ? ACC : CUTP_RW;      // accumulators per reduction pass
-  static constexpr int WSLOT = OFF_RED + (BFLY ? 0 : (HYB ? 32 * 17 : RW * 33));
+  // the warp's next <= DG cell descriptors, staged by one coalesced load per group
+  // (8: 640 B, what is left of the SM's shared memory at 8 warps per SM)
+  static constexpr int DG = 8;
+  static constexpr int OFF_DSC = OFF_RED + (BFLY ? 0 : (HYB ? 32 * 17 : RW * 33));
+  static constexpr int WSLOT = OFF_DSC + DG * (int)(sizeof(CDesc2) / 8);
   static constexpr int SMEM = WARPS * WSLOT * 8;
 };
 
@@ -442,7 +446,22 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     mbar_fence_init();
   }
   __syncwarp();
-  CDesc2 cd = desc[c0w];
+  // descriptors: groups of DG staged in shared memory (5 lanes per 80-byte descriptor,
+  // one 16-byte word each; a global descriptor load per cell was exposed latency: ~4 %
+  // of the stall samples)
+  CDesc2 *DS = reinterpret_cast<CDesc2 *>(base + C::OFF_DSC);
+  auto stage_desc = [&](int g0) {
+    constexpr int W16 = (int)(sizeof(CDesc2) / 16);
+    __syncwarp();
+    for (int k = lane; k < C::DG * W16; k += 32) {
+      const int c = g0 + k / W16;
+      if (c < c1w)
+        reinterpret_cast<uint4 *>(DS)[k] = reinterpret_cast<const uint4 *>(desc + c)[k % W16];
+    }
+    __syncwarp();
+  };
+  stage_desc(c0w);
+  CDesc2 cd = DS[0];
   issue_blocks(cd, 0);
   // prologue: NB-1 packets in flight, the record of the next one prefetched into a register
   CPacket rn = {0, 0, 0};
@@ -460,7 +479,10 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     const int set = it & 1;
     const bool has_next = c + 1 < c1w;
     CDesc2 nd;
-    if (has_next) nd = desc[c + 1];
+    if (has_next) {
+      if (((c + 1 - c0w) % C::DG) == 0) stage_desc(c + 1);  // cd (this cell) is in registers
+      nd = DS[(c + 1 - c0w) % C::DG];
+    }
     int nv, ns, nf;
     counts(cd, nv, ns, nf);
     // chunks of the cell: the first KL are volume lines
