@@ -198,6 +198,33 @@ int cutfem_rhs_const(cutfem_handle *hd, double f, double *b_dev, void *cuda_stre
 int cutfem_cg(cutfem_handle *hd, const double *b_dev, double *x_dev, int iters, double tol, double *res_hist,
               int *iters_done, void *cuda_stream);
 
+/* ---- H^1-conforming (continuous Galerkin) operator.
+ * PAPER eq:bilinear_cg: a_CG(v,u) = (grad v, grad u)_Omega + Nitsche on
+ * Gamma, plus the face ghost penalty of the problem (BASELINE configs[0]), on the
+ * CONTINUOUS Q_p space of the active cells (GLL nodes, shared on faces, edges and
+ * vertices).  v = A_CG u with A_CG = P^T A P: P gathers the global vector into the
+ * cell blocks, A is the block operator of cutfem_apply without the SIPG terms (the
+ * same integrals; the j = 0 ghost-penalty jump of a continuous field is zero).
+ * Global numbering: lattice node (p i + a, p j + b, p k + c) of active cell (i,j,k),
+ * local l = a + n b + n^2 c, nodes of active cells in lexicographic order (x slowest).
+ * cutfem_h1_setup: as cutfem_setup (host arrays deep-copied; pb->term_mask's SIPG
+ *   bit is ignored); *out receives an opaque handle, NULL on error.
+ * cutfem_h1_ndofs: number of global nodes n_h1.
+ * cutfem_h1_map: host array [n_active * n^3] <- global node of each block entry.
+ * cutfem_h1_apply: u_dev, v_dev DEVICE pointers to n_h1 doubles (8-byte aligned, no
+ *   alias); v is overwritten; stream ordered, no host sync; every node summed by one
+ *   thread in a fixed order (deterministic, no atomics).
+ * cutfem_h1_rhs_const: b_i = f int_Omega phi_i, b_dev: n_h1 doubles.
+ * Errors as cutfem_setup / cutfem_apply. */
+typedef struct cutfem_h1 cutfem_h1;
+int cutfem_h1_setup(const cutfem_problem *pb, int device, cutfem_h1 **out);
+int cutfem_h1_ndofs(const cutfem_h1 *h, int64_t *n_h1);
+int cutfem_h1_map(const cutfem_h1 *h, int32_t *map_host);
+int cutfem_h1_apply(cutfem_h1 *h, const double *u_dev, double *v_dev, void *cuda_stream);
+int cutfem_h1_rhs_const(cutfem_h1 *h, double f, double *b_dev, void *cuda_stream);
+int cutfem_h1_stats(const cutfem_h1 *h, cutfem_stats_t *out);
+int cutfem_h1_destroy(cutfem_h1 *h);
+
 int cutfem_stats(const cutfem_handle *hd, cutfem_stats_t *out);
 const char *cutfem_last_error(void);
 int cutfem_destroy(cutfem_handle *hd);

@@ -82,7 +82,8 @@ EXPORTS = ["cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_
            "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_nnz", "cutfem_csr_download",
            "cutfem_stats", "cutfem_last_error", "cutfem_destroy", "cutfem_partition_x",
            "cutfem_local_build", "cutfem_local_free", "cutfem_nccl_unique_id", "cutfem_setup_dist",
-           "cutfem_dist_info", "cutfem_rhs_const", "cutfem_cg"]
+           "cutfem_dist_info", "cutfem_rhs_const", "cutfem_cg", "cutfem_h1_setup", "cutfem_h1_ndofs",
+           "cutfem_h1_map", "cutfem_h1_apply", "cutfem_h1_rhs_const", "cutfem_h1_stats", "cutfem_h1_destroy"]
 
 
 class _Local(ctypes.Structure):
@@ -128,10 +129,18 @@ def load(path: str | None = None):
                                     ctypes.POINTER(vp)]
     L.cutfem_dist_info.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.cutfem_debug_loopback.argtypes = [vp, vp, vp]
+    L.cutfem_h1_setup.argtypes = [ctypes.POINTER(_Problem), i32, ctypes.POINTER(vp)]
+    L.cutfem_h1_ndofs.argtypes = [vp, ctypes.POINTER(i64)]
+    L.cutfem_h1_map.argtypes = [vp, vp]
+    L.cutfem_h1_apply.argtypes = [vp, vp, vp, vp]
+    L.cutfem_h1_rhs_const.argtypes = [vp, ctypes.c_double, vp, vp]
+    L.cutfem_h1_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+    L.cutfem_h1_destroy.argtypes = [vp]
     for name in ("cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_host", "cutfem_csr_assemble",
                  "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_download", "cutfem_stats",
                  "cutfem_destroy", "cutfem_partition_x", "cutfem_local_build", "cutfem_nccl_unique_id",
-                 "cutfem_setup_dist", "cutfem_dist_info"):
+                 "cutfem_setup_dist", "cutfem_dist_info", "cutfem_h1_setup", "cutfem_h1_ndofs", "cutfem_h1_map",
+                 "cutfem_h1_apply", "cutfem_h1_rhs_const", "cutfem_h1_stats", "cutfem_h1_destroy"):
         getattr(L, name).restype = i32
     if path is None:
         _lib = L
@@ -360,6 +369,58 @@ class CutFEM:
     def close(self):
         if getattr(self, "_h", None):
             self._L.cutfem_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class CutFEMH1:
+    """The H^1-conforming (continuous Galerkin) operator v = A_CG u on one GPU
+    (include/cutfem.h cutfem_h1_*); vectors hold the n_dofs global lattice nodes."""
+
+    def __init__(self, prob, device: int = 0, term_mask: int = TERM_ALL):
+        L = load()
+        pb, keep = _marshal(prob, term_mask)
+        h = ctypes.c_void_p()
+        _check(L.cutfem_h1_setup(ctypes.byref(pb), int(device), ctypes.byref(h)))
+        self._h, self._L, self.device = h, L, device
+        n = ctypes.c_int64()
+        _check(L.cutfem_h1_ndofs(h, ctypes.byref(n)))
+        self.n_dofs = int(n.value)
+        self.n_blk = int(prob.active_ijk.shape[0]) * (int(prob.degree) + 1) ** 3
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(self._L.cutfem_h1_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def map(self) -> np.ndarray:
+        m = np.zeros(self.n_blk, dtype=np.int32)
+        _check(self._L.cutfem_h1_map(self._h, m.ctypes.data if m.size else None))
+        return m
+
+    def apply(self, u, v=None, stream=None):
+        import torch
+        if v is None:
+            v = torch.empty(self.n_dofs, dtype=torch.float64, device=u.device)
+        assert u.dtype == torch.float64 and u.is_cuda and u.numel() == self.n_dofs and v.numel() == self.n_dofs
+        _check(self._L.cutfem_h1_apply(self._h, u.data_ptr(), v.data_ptr(), _stream_ptr(stream)))
+        return v
+
+    def rhs_const(self, f: float = 1.0, b=None, stream=None):
+        import torch
+        if b is None:
+            b = torch.empty(self.n_dofs, dtype=torch.float64, device=f"cuda:{self.device}")
+        _check(self._L.cutfem_h1_rhs_const(self._h, float(f), b.data_ptr(), _stream_ptr(stream)))
+        return b
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.cutfem_h1_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -1502,3 +1502,4 @@ int cutfem_destroy(cutfem_handle *hd) {
 #include "csr.inl"
 #include "dist.inl"
 #include "cg.inl"
+#include "h1.inl"
