@@ -198,6 +198,20 @@ int cutfem_rhs_const(cutfem_handle *hd, double f, double *b_dev, void *cuda_stre
 int cutfem_cg(cutfem_handle *hd, const double *b_dev, double *x_dev, int iters, double tol, double *res_hist,
               int *iters_done, void *cuda_stream);
 
+/* ---- Preconditioned solve (PAPER P:573-578 uses a preconditioned CG).
+ * cutfem_pcg: cutfem_cg with a preconditioner M^-1: CUTFEM_PRECOND_NONE (= cutfem_cg)
+ *   or CUTFEM_PRECOND_JACOBI (M = diag(A)).  res_hist receives ||r_k||_2 (the true
+ *   residual, not r.z).  The diagonal is probed once per handle on first use
+ *   (2 (p+1)^3 applies: unit vectors on each local index of the cells of one colour
+ *   of the checkerboard (i+j+k) mod 2 -- face neighbours differ in colour, so each
+ *   probe returns exact diagonal entries).
+ * cutfem_diag: d_dev (n_dofs doubles, device) <- diag(A) (the same probing). */
+#define CUTFEM_PRECOND_NONE 0
+#define CUTFEM_PRECOND_JACOBI 1
+int cutfem_pcg(cutfem_handle *hd, const double *b_dev, double *x_dev, int iters, double tol, int precond,
+               double *res_hist, int *iters_done, void *cuda_stream);
+int cutfem_diag(cutfem_handle *hd, double *d_dev, void *cuda_stream);
+
 /* ---- H^1-conforming (continuous Galerkin) operator.
  * PAPER eq:bilinear_cg: a_CG(v,u) = (grad v, grad u)_Omega + Nitsche on
  * Gamma, plus the face ghost penalty of the problem (BASELINE configs[0]), on the
@@ -223,6 +237,14 @@ int cutfem_h1_map(const cutfem_h1 *h, int32_t *map_host);
 int cutfem_h1_apply(cutfem_h1 *h, const double *u_dev, double *v_dev, void *cuda_stream);
 int cutfem_h1_rhs_const(cutfem_h1 *h, double f, double *b_dev, void *cuda_stream);
 int cutfem_h1_stats(const cutfem_h1 *h, cutfem_stats_t *out);
+/* PCG / diagonal of the H1 operator (as cutfem_pcg / cutfem_diag; vectors of n_h1
+ * doubles, 16-byte aligned).  The diagonal is probed with the lattice colouring
+ * (I, J, K) mod (2p+1) per axis ((2p+1)^3 applies): two nodes of one colour never
+ * share a cell or a ghost-penalty face pair, so each probe returns exact diagonal
+ * entries. */
+int cutfem_h1_pcg(cutfem_h1 *h, const double *b_dev, double *x_dev, int iters, double tol, int precond,
+                  double *res_hist, int *iters_done, void *cuda_stream);
+int cutfem_h1_diag(cutfem_h1 *h, double *d_dev, void *cuda_stream);
 int cutfem_h1_destroy(cutfem_h1 *h);
 
 int cutfem_stats(const cutfem_handle *hd, cutfem_stats_t *out);

@@ -83,7 +83,11 @@ EXPORTS = ["cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_
            "cutfem_stats", "cutfem_last_error", "cutfem_destroy", "cutfem_partition_x",
            "cutfem_local_build", "cutfem_local_free", "cutfem_nccl_unique_id", "cutfem_setup_dist",
            "cutfem_dist_info", "cutfem_rhs_const", "cutfem_cg", "cutfem_h1_setup", "cutfem_h1_ndofs",
-           "cutfem_h1_map", "cutfem_h1_apply", "cutfem_h1_rhs_const", "cutfem_h1_stats", "cutfem_h1_destroy"]
+           "cutfem_h1_map", "cutfem_h1_apply", "cutfem_h1_rhs_const", "cutfem_h1_stats", "cutfem_h1_destroy",
+           "cutfem_pcg", "cutfem_diag", "cutfem_h1_pcg", "cutfem_h1_diag"]
+
+
+PRECOND = {"none": 0, "jacobi": 1}
 
 
 class _Local(ctypes.Structure):
@@ -136,11 +140,17 @@ def load(path: str | None = None):
     L.cutfem_h1_rhs_const.argtypes = [vp, ctypes.c_double, vp, vp]
     L.cutfem_h1_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     L.cutfem_h1_destroy.argtypes = [vp]
+    pcg_args = [vp, vp, vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ctypes.c_int), vp]
+    L.cutfem_pcg.argtypes = pcg_args
+    L.cutfem_h1_pcg.argtypes = pcg_args
+    L.cutfem_diag.argtypes = [vp, vp, vp]
+    L.cutfem_h1_diag.argtypes = [vp, vp, vp]
     for name in ("cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_host", "cutfem_csr_assemble",
                  "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_download", "cutfem_stats",
                  "cutfem_destroy", "cutfem_partition_x", "cutfem_local_build", "cutfem_nccl_unique_id",
                  "cutfem_setup_dist", "cutfem_dist_info", "cutfem_h1_setup", "cutfem_h1_ndofs", "cutfem_h1_map",
-                 "cutfem_h1_apply", "cutfem_h1_rhs_const", "cutfem_h1_stats", "cutfem_h1_destroy"):
+                 "cutfem_h1_apply", "cutfem_h1_rhs_const", "cutfem_h1_stats", "cutfem_h1_destroy",
+                 "cutfem_pcg", "cutfem_diag", "cutfem_h1_pcg", "cutfem_h1_diag"):
         getattr(L, name).restype = i32
     if path is None:
         _lib = L
@@ -326,18 +336,25 @@ class CutFEM:
         _check(self._L.cutfem_rhs_const(self._h, float(f), b.data_ptr(), _stream_ptr(stream)))
         return b
 
-    def cg(self, b, x=None, iters: int = 50, tol: float = 0.0, stream=None):
-        """Unpreconditioned CG on A x = b in the library's kernels; x (in/out) needs
-        n_ext_dofs entries.  Returns (x, residual norms ||r_k||, k = 0..done)."""
+    def cg(self, b, x=None, iters: int = 50, tol: float = 0.0, stream=None, precond: str = "none"):
+        """(Preconditioned) CG on A x = b in the library's kernels; x (in/out) needs
+        n_ext_dofs entries; precond "none" | "jacobi".  Returns (x, ||r_k||, k = 0..done)."""
         import torch
         if x is None:
             x = torch.zeros(self.n_ext_dofs, dtype=torch.float64, device=b.device)
         assert x.numel() == self.n_ext_dofs and b.numel() == self.n_dofs
         hist = np.zeros(int(iters) + 1, dtype=np.float64)
         done = ctypes.c_int()
-        _check(self._L.cutfem_cg(self._h, b.data_ptr(), x.data_ptr(), int(iters), float(tol), hist.ctypes.data,
-                                 ctypes.byref(done), _stream_ptr(stream)))
+        _check(self._L.cutfem_pcg(self._h, b.data_ptr(), x.data_ptr(), int(iters), float(tol), PRECOND[precond],
+                                  hist.ctypes.data, ctypes.byref(done), _stream_ptr(stream)))
         return x, hist[:done.value + 1]
+
+    def diag(self, stream=None):
+        """diag(A) (device), probed (include/cutfem.h cutfem_diag)."""
+        import torch
+        d = torch.empty(self.n_dofs, dtype=torch.float64, device=f"cuda:{self.device}")
+        _check(self._L.cutfem_diag(self._h, d.data_ptr(), _stream_ptr(stream)))
+        return d
 
     def csr_assemble(self) -> int:
         nnz = ctypes.c_int64()
@@ -417,6 +434,22 @@ class CutFEMH1:
             b = torch.empty(self.n_dofs, dtype=torch.float64, device=f"cuda:{self.device}")
         _check(self._L.cutfem_h1_rhs_const(self._h, float(f), b.data_ptr(), _stream_ptr(stream)))
         return b
+
+    def cg(self, b, x=None, iters: int = 50, tol: float = 0.0, stream=None, precond: str = "none"):
+        import torch
+        if x is None:
+            x = torch.zeros(self.n_dofs, dtype=torch.float64, device=b.device)
+        hist = np.zeros(int(iters) + 1, dtype=np.float64)
+        done = ctypes.c_int()
+        _check(self._L.cutfem_h1_pcg(self._h, b.data_ptr(), x.data_ptr(), int(iters), float(tol), PRECOND[precond],
+                                     hist.ctypes.data, ctypes.byref(done), _stream_ptr(stream)))
+        return x, hist[:done.value + 1]
+
+    def diag(self, stream=None):
+        import torch
+        d = torch.empty(self.n_dofs, dtype=torch.float64, device=f"cuda:{self.device}")
+        _check(self._L.cutfem_h1_diag(self._h, d.data_ptr(), _stream_ptr(stream)))
+        return d
 
     def close(self):
         if getattr(self, "_h", None):

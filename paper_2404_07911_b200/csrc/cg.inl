@@ -50,15 +50,18 @@ __global__ void __launch_bounds__(CG_THREADS) k_dot_final(const double *__restri
   if (threadIdx.x == 0) *out = s;
 }
 
-// x += alpha p, r -= alpha q (alpha = rr[k] / pq[k]); partial sums of |r|^2
+// x += alpha p, r -= alpha q (alpha = rz[k] / pq[k]); with a Jacobi preconditioner
+// (dinv != null) z = dinv r; partial sums of r.z (part_rz) and |r|^2 (part_rr; only
+// when preconditioned -- else r.z = |r|^2)
 __global__ void __launch_bounds__(CG_THREADS) k_cg_xr(double *__restrict__ x, double *__restrict__ r,
+                                                      double *__restrict__ z, const double *__restrict__ dinv,
                                                       const double *__restrict__ p, const double *__restrict__ q,
-                                                      int64_t n, const double *__restrict__ rr,
+                                                      int64_t n, const double *__restrict__ rz,
                                                       const double *__restrict__ pq, int k,
-                                                      double *__restrict__ partial) {
+                                                      double *__restrict__ part_rz, double *__restrict__ part_rr) {
   __shared__ double sh[CG_THREADS];
-  const double alpha = rr[k] / pq[k];
-  double s = 0.0;
+  const double alpha = rz[k] / pq[k];
+  double s = 0.0, s2 = 0.0;
   double2 *x2 = reinterpret_cast<double2 *>(x), *r2 = reinterpret_cast<double2 *>(r);
   const double2 *p2 = reinterpret_cast<const double2 *>(p), *q2 = reinterpret_cast<const double2 *>(q);
   for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n / 2; i += (int64_t)gridDim.x * CG_THREADS) {
@@ -66,45 +69,91 @@ __global__ void __launch_bounds__(CG_THREADS) k_cg_xr(double *__restrict__ x, do
     x2[i] = make_double2(fma(alpha, pi.x, xi.x), fma(alpha, pi.y, xi.y));
     const double2 ri = make_double2(fma(-alpha, qi.x, ri0.x), fma(-alpha, qi.y, ri0.y));
     r2[i] = ri;
-    s = fma(ri.x, ri.x, fma(ri.y, ri.y, s));
+    if (dinv) {
+      const double2 di = reinterpret_cast<const double2 *>(dinv)[i];
+      const double2 zi = make_double2(di.x * ri.x, di.y * ri.y);
+      reinterpret_cast<double2 *>(z)[i] = zi;
+      s = fma(ri.x, zi.x, fma(ri.y, zi.y, s));
+      s2 = fma(ri.x, ri.x, fma(ri.y, ri.y, s2));
+    } else {
+      s = fma(ri.x, ri.x, fma(ri.y, ri.y, s));
+    }
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd n: the tail entry
     x[n - 1] = fma(alpha, p[n - 1], x[n - 1]);
     const double rt = fma(-alpha, q[n - 1], r[n - 1]);
     r[n - 1] = rt;
-    s = fma(rt, rt, s);
+    if (dinv) {
+      const double zt = dinv[n - 1] * rt;
+      z[n - 1] = zt;
+      s = fma(rt, zt, s);
+      s2 = fma(rt, rt, s2);
+    } else {
+      s = fma(rt, rt, s);
+    }
   }
   s = block_sum(s, sh);
-  if (threadIdx.x == 0) partial[blockIdx.x] = s;
-}
-
-// p = r + beta p, beta = rr[k+1] / rr[k]
-__global__ void __launch_bounds__(CG_THREADS) k_cg_p(double *__restrict__ p, const double *__restrict__ r, int64_t n,
-                                                     const double *__restrict__ rr, int k) {
-  const double beta = rr[k + 1] / rr[k];
-  double2 *p2 = reinterpret_cast<double2 *>(p);
-  const double2 *r2 = reinterpret_cast<const double2 *>(r);
-  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n / 2; i += (int64_t)gridDim.x * CG_THREADS) {
-    const double2 pi = p2[i], ri = r2[i];
-    p2[i] = make_double2(fma(beta, pi.x, ri.x), fma(beta, pi.y, ri.y));
+  if (threadIdx.x == 0) part_rz[blockIdx.x] = s;
+  if (dinv) {
+    __syncthreads();
+    s2 = block_sum(s2, sh);
+    if (threadIdx.x == 0) part_rr[blockIdx.x] = s2;
   }
-  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = fma(beta, p[n - 1], r[n - 1]);
 }
 
-// r = b - q, p = r, partial sums of |r|^2
-__global__ void __launch_bounds__(CG_THREADS) k_cg_init(double *__restrict__ r, double *__restrict__ p,
+// p = z + beta p, beta = rz[k+1] / rz[k]
+__global__ void __launch_bounds__(CG_THREADS) k_cg_p(double *__restrict__ p, const double *__restrict__ z, int64_t n,
+                                                     const double *__restrict__ rz, int k) {
+  const double beta = rz[k + 1] / rz[k];
+  double2 *p2 = reinterpret_cast<double2 *>(p);
+  const double2 *z2 = reinterpret_cast<const double2 *>(z);
+  for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n / 2; i += (int64_t)gridDim.x * CG_THREADS) {
+    const double2 pi = p2[i], zi = z2[i];
+    p2[i] = make_double2(fma(beta, pi.x, zi.x), fma(beta, pi.y, zi.y));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = fma(beta, p[n - 1], z[n - 1]);
+}
+
+// r = b - q, z = dinv r (or r), p = z, partial sums of r.z and |r|^2
+__global__ void __launch_bounds__(CG_THREADS) k_cg_init(double *__restrict__ r, double *__restrict__ z,
+                                                        double *__restrict__ p, const double *__restrict__ dinv,
                                                         const double *__restrict__ b, const double *__restrict__ q,
-                                                        int64_t n, double *__restrict__ partial) {
+                                                        int64_t n, double *__restrict__ part_rz,
+                                                        double *__restrict__ part_rr) {
   __shared__ double sh[CG_THREADS];
-  double s = 0.0;
+  double s = 0.0, s2 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)CG_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * CG_THREADS) {
     const double ri = b[i] - q[i];
+    const double zi = dinv ? dinv[i] * ri : ri;
     r[i] = ri;
-    p[i] = ri;
-    s = fma(ri, ri, s);
+    if (dinv) z[i] = zi;
+    p[i] = zi;
+    s = fma(ri, zi, s);
+    s2 = fma(ri, ri, s2);
   }
   s = block_sum(s, sh);
-  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+  if (threadIdx.x == 0) part_rz[blockIdx.x] = s;
+  __syncthreads();
+  s2 = block_sum(s2, sh);
+  if (threadIdx.x == 0) part_rr[blockIdx.x] = s2;
+}
+
+// dinv = 1 / d (the Jacobi preconditioner from the probed diagonal)
+__global__ void k_recip(double *__restrict__ d, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = 1.0 / d[i];
+}
+
+// diagonal probing: u[e] = 1 on the entries of probe (colour, local index), else 0
+__global__ void k_probe_unit(double *__restrict__ u, const int32_t *__restrict__ probe_of, int32_t probe, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    u[i] = probe_of[i] == probe ? 1.0 : 0.0;
+}
+// d[e] = v[e] on the entries of the probe
+__global__ void k_probe_take(double *__restrict__ d, const double *__restrict__ v, const int32_t *__restrict__ probe_of,
+                             int32_t probe, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (probe_of[i] == probe) d[i] = v[i];
 }
 
 // ---- right-hand side b = f int_Ω phi_i
@@ -171,31 +220,151 @@ __global__ void __launch_bounds__(128) k_rhs_cut(double *__restrict__ b, const C
 }  // namespace
 
 struct cutfem_cg_work {
-  double *r = nullptr, *p = nullptr, *q = nullptr, *partial = nullptr, *rr = nullptr, *pq = nullptr;
-  int cap = 0;  // iterations the scalar arrays hold
+  double *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr, *partial = nullptr, *partial2 = nullptr;
+  double *rr = nullptr, *rz = nullptr, *pq = nullptr, *bb = nullptr;
+  double *dinv = nullptr;         // Jacobi: 1 / diag(A) (probed, lazily)
+  int32_t *probe_of = nullptr;    // probe index of every entry (diagonal probing)
+  int64_t n = 0, n_p = 0;         // vector length; p length (ghost room for a distributed apply)
+  int cap = 0;                    // iterations the scalar arrays hold
 };
 
 void cg_free(cutfem_cg_work *w) {
   if (!w) return;
-  cudaFree(w->r);
-  cudaFree(w->p);
-  cudaFree(w->q);
-  cudaFree(w->partial);
-  cudaFree(w->rr);
-  cudaFree(w->pq);
+  for (double *x : {w->r, w->p, w->q, w->z, w->partial, w->partial2, w->rr, w->rz, w->pq, w->bb, w->dinv}) cudaFree(x);
+  cudaFree(w->probe_of);
   delete w;
 }
 
 namespace {
 
+int cg_alloc(cutfem_cg_work &w, int64_t n, int64_t n_p, int iters, int64_t &dev_bytes) {
+  if (!w.r) {
+    w.n = n;
+    w.n_p = n_p;
+    CU(cudaMalloc(&w.r, sizeof(double) * std::max<int64_t>(n, 2)));
+    CU(cudaMalloc(&w.z, sizeof(double) * std::max<int64_t>(n, 2)));
+    CU(cudaMalloc(&w.p, sizeof(double) * std::max<int64_t>(n_p, 2)));  // ghost room for the apply
+    CU(cudaMalloc(&w.q, sizeof(double) * std::max<int64_t>(n, 2)));
+    CU(cudaMalloc(&w.partial, sizeof(double) * CG_BLOCKS));
+    CU(cudaMalloc(&w.partial2, sizeof(double) * CG_BLOCKS));
+    CU(cudaMalloc(&w.bb, sizeof(double) * 2));
+    dev_bytes += (int64_t)sizeof(double) * (3 * n + n_p + 2 * CG_BLOCKS);
+  }
+  if (w.cap < iters + 1) {
+    cudaFree(w.rr);
+    cudaFree(w.rz);
+    cudaFree(w.pq);
+    w.cap = iters + 1;
+    CU(cudaMalloc(&w.rr, sizeof(double) * (w.cap + 1)));
+    CU(cudaMalloc(&w.rz, sizeof(double) * (w.cap + 1)));
+    CU(cudaMalloc(&w.pq, sizeof(double) * (w.cap + 1)));
+  }
+  return 0;
+}
+
+// Jacobi diagonal by probing (P:228's "column by column through unit vectors"): for
+// every probe index k, u = 1 on the entries of probe k, v = A u, diag = v there.  The
+// probe classes are chosen so that no two entries of one class couple (the caller's
+// colouring), so v on a probed entry is exactly its diagonal entry.  dinv = 1 / diag.
+template <class Apply>
+int cg_probe_diag(cutfem_cg_work &w, int nprobe, Apply apply, cudaStream_t st, int sms, int64_t &dev_bytes) {
+  const unsigned g = (unsigned)std::min<int64_t>((w.n_p + 255) / 256, 16 * sms);
+  if (!w.dinv) {
+    CU(cudaMalloc(&w.dinv, sizeof(double) * std::max<int64_t>(w.n, 2)));
+    dev_bytes += (int64_t)sizeof(double) * w.n;
+  }
+  for (int k = 0; k < nprobe; ++k) {
+    k_probe_unit<<<g, 256, 0, st>>>(w.p, w.probe_of, k, w.n_p);
+    CU(cudaGetLastError());
+    int rc = apply(w.p, w.q);
+    if (rc) return rc;
+    k_probe_take<<<g, 256, 0, st>>>(w.dinv, w.q, w.probe_of, k, w.n);
+    CU(cudaGetLastError());
+  }
+  k_recip<<<g, 256, 0, st>>>(w.dinv, w.n);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+// (Preconditioned) conjugate gradients, every vector operation in the kernels above,
+// the scalars on the device (no host sync per iteration unless tol > 0).
+template <class Apply, class Reduce>
+int cg_run(cutfem_cg_work &w, Apply apply, Reduce reduce, const double *b, double *x, int iters, double tol,
+           bool jacobi, double *res_hist, int *iters_done, cudaStream_t st) {
+  const int64_t n = w.n;
+  const double *dinv = jacobi ? w.dinv : nullptr;
+  double *z = jacobi ? w.z : w.r;
+  int rc;
+  // r0 = b - A x0, z0 = M^-1 r0, p0 = z0
+  if ((rc = apply(x, w.q))) return rc;
+  k_cg_init<<<CG_BLOCKS, CG_THREADS, 0, st>>>(w.r, z, w.p, dinv, b, w.q, n, w.partial, w.partial2);
+  CU(cudaGetLastError());
+  if ((rc = reduce(w.partial, w.rz))) return rc;
+  if ((rc = reduce(w.partial2, w.rr))) return rc;
+  double bb = 0.0;
+  if (tol > 0) {
+    k_dot<<<CG_BLOCKS, CG_THREADS, 0, st>>>(b, b, n, w.partial);
+    if ((rc = reduce(w.partial, w.bb))) return rc;
+    CU(cudaMemcpyAsync(&bb, w.bb, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
+  int k = 0;
+  for (; k < iters; ++k) {
+    if ((rc = apply(w.p, w.q))) return rc;  // q = A p
+    k_dot<<<CG_BLOCKS, CG_THREADS, 0, st>>>(w.p, w.q, n, w.partial);
+    if ((rc = reduce(w.partial, w.pq + k))) return rc;
+    k_cg_xr<<<CG_BLOCKS, CG_THREADS, 0, st>>>(x, w.r, z, dinv, w.p, w.q, n, w.rz, w.pq, k, w.partial, w.partial2);
+    CU(cudaGetLastError());
+    if ((rc = reduce(w.partial, w.rz + k + 1))) return rc;
+    if (jacobi && (rc = reduce(w.partial2, w.rr + k + 1))) return rc;
+    k_cg_p<<<CG_BLOCKS, CG_THREADS, 0, st>>>(w.p, z, n, w.rz, k);
+    CU(cudaGetLastError());
+    if (tol > 0) {
+      double rk = 0.0;
+      CU(cudaMemcpyAsync(&rk, (jacobi ? w.rr : w.rz) + k + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      if (std::sqrt(rk) <= tol * std::sqrt(bb)) {
+        ++k;
+        break;
+      }
+    }
+  }
+  if (res_hist) {
+    std::vector<double> h2(k + 1);
+    if (jacobi) {
+      CU(cudaMemcpyAsync(h2.data(), w.rr, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st));
+    } else {  // |r_0|^2 from the init, |r_k|^2 = r.z for k >= 1
+      CU(cudaMemcpyAsync(h2.data(), w.rz, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st));
+    }
+    CU(cudaStreamSynchronize(st));
+    for (int i = 0; i <= k; ++i) res_hist[i] = std::sqrt(h2[i]);
+  } else {
+    CU(cudaStreamSynchronize(st));
+  }
+  if (iters_done) *iters_done = k;
+  return 0;
+}
+
 int cg_reduce(cutfem_handle *hd, double *partial, double *out, cudaStream_t st) {
   k_dot_final<<<1, CG_THREADS, 0, st>>>(partial, CG_BLOCKS, out);
   CU(cudaGetLastError());
-  if (hd->dist && hd->comm && (hd->nranks > 1 || hd->loopback)) {
+  if (hd && hd->dist && hd->comm && (hd->nranks > 1 || hd->loopback)) {
     ncclResult_t r = ncclAllReduce(out, out, 1, ncclDouble, ncclSum, (ncclComm_t)hd->comm, st);
     if (r != ncclSuccess) return fail(CUTFEM_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
   }
   return 0;
+}
+
+// DG probe classes: block colour (i + j + k) mod 2 (face neighbours differ) x local index
+int dg_probes(cutfem_handle *hd, cutfem_cg_work &w) {
+  if (w.probe_of) return 0;
+  const int n3 = hd->n * hd->n * hd->n;
+  std::vector<int32_t> pr((size_t)w.n_p, -1);
+  for (int64_t K = 0; K < (int64_t)hd->blk_ijk.size() / 3; ++K) {
+    const int c = (int)((hd->blk_ijk[3 * K] + hd->blk_ijk[3 * K + 1] + hd->blk_ijk[3 * K + 2]) & 1);
+    for (int l = 0; l < n3; ++l) pr[(size_t)K * n3 + l] = c * n3 + l;
+  }
+  return upload(hd, &w.probe_of, pr.data(), pr.size());
 }
 
 }  // namespace
@@ -232,74 +401,53 @@ int cutfem_rhs_const(cutfem_handle *hd, double f, double *b_dev, void *cuda_stre
   return 0;
 }
 
-int cutfem_cg(cutfem_handle *hd, const double *b_dev, double *x_dev, int iters, double tol, double *res_hist,
-              int *iters_done, void *cuda_stream) {
+int cutfem_pcg(cutfem_handle *hd, const double *b_dev, double *x_dev, int iters, double tol, int precond,
+               double *res_hist, int *iters_done, void *cuda_stream) {
   if (!hd) return fail(CUTFEM_EINVAL, "null handle");
   if (iters < 0) return fail(CUTFEM_EINVAL, "iters < 0");
+  if (precond != CUTFEM_PRECOND_NONE && precond != CUTFEM_PRECOND_JACOBI) return fail(CUTFEM_EINVAL, "precond");
   if (hd->stats.n_dofs > 0 && (!b_dev || !x_dev)) return fail(CUTFEM_EINVAL, "null vector");
   if (((uintptr_t)b_dev | (uintptr_t)x_dev) & 15) return fail(CUTFEM_EINVAL, "vectors must be 16-byte aligned");
   if (b_dev == x_dev && hd->stats.n_dofs > 0) return fail(CUTFEM_EINVAL, "b and x must not alias");
   CU(cudaSetDevice(hd->device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  const int64_t n = hd->stats.n_dofs, next = hd->stats.n_ext_dofs;
   if (!hd->cg) hd->cg = new cutfem_cg_work();
   cutfem_cg_work &w = *hd->cg;
-  if (!w.r) {
-    CU(cudaMalloc(&w.r, sizeof(double) * std::max<int64_t>(n, 1)));
-    CU(cudaMalloc(&w.p, sizeof(double) * std::max<int64_t>(next, 1)));  // ghost room for the apply
-    CU(cudaMalloc(&w.q, sizeof(double) * std::max<int64_t>(n, 1)));
-    CU(cudaMalloc(&w.partial, sizeof(double) * CG_BLOCKS));
-    hd->dev_bytes += (int64_t)sizeof(double) * (2 * n + next + CG_BLOCKS);
-  }
-  if (w.cap < iters + 1) {
-    cudaFree(w.rr);
-    cudaFree(w.pq);
-    w.cap = iters + 1;
-    CU(cudaMalloc(&w.rr, sizeof(double) * (w.cap + 1)));
-    CU(cudaMalloc(&w.pq, sizeof(double) * (w.cap + 1)));
-  }
   int rc;
-  // r0 = b - A x0, p0 = r0, rr[0] = |r0|^2
-  if ((rc = dispatch_apply(hd, x_dev, w.q, st))) return rc;
-  k_cg_init<<<CG_BLOCKS, CG_THREADS, 0, st>>>(w.r, w.p, b_dev, w.q, n, w.partial);
+  if ((rc = cg_alloc(w, hd->stats.n_dofs, hd->stats.n_ext_dofs, iters, hd->dev_bytes))) return rc;
+  auto apply = [&](const double *u, double *v) { return dispatch_apply(hd, u, v, st); };
+  auto reduce = [&](double *part, double *out) { return cg_reduce(hd, part, out, st); };
+  const bool jac = precond == CUTFEM_PRECOND_JACOBI;
+  if (jac && !w.dinv) {
+    if ((rc = dg_probes(hd, w))) return rc;
+    if ((rc = cg_probe_diag(w, 2 * hd->n * hd->n * hd->n, apply, st, hd->sm_count, hd->dev_bytes))) return rc;
+  }
+  return cg_run(w, apply, reduce, b_dev, x_dev, iters, tol, jac, res_hist, iters_done, st);
+}
+
+int cutfem_cg(cutfem_handle *hd, const double *b_dev, double *x_dev, int iters, double tol, double *res_hist,
+              int *iters_done, void *cuda_stream) {
+  return cutfem_pcg(hd, b_dev, x_dev, iters, tol, CUTFEM_PRECOND_NONE, res_hist, iters_done, cuda_stream);
+}
+
+int cutfem_diag(cutfem_handle *hd, double *d_dev, void *cuda_stream) {
+  if (!hd) return fail(CUTFEM_EINVAL, "null handle");
+  if (hd->stats.n_dofs > 0 && !d_dev) return fail(CUTFEM_EINVAL, "null vector");
+  CU(cudaSetDevice(hd->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (!hd->cg) hd->cg = new cutfem_cg_work();
+  cutfem_cg_work &w = *hd->cg;
+  int rc;
+  if ((rc = cg_alloc(w, hd->stats.n_dofs, hd->stats.n_ext_dofs, 1, hd->dev_bytes))) return rc;
+  auto apply = [&](const double *u, double *v) { return dispatch_apply(hd, u, v, st); };
+  if (!w.dinv) {
+    if ((rc = dg_probes(hd, w))) return rc;
+    if ((rc = cg_probe_diag(w, 2 * hd->n * hd->n * hd->n, apply, st, hd->sm_count, hd->dev_bytes))) return rc;
+  }
+  const unsigned g = (unsigned)std::min<int64_t>((w.n + 255) / 256, 16 * hd->sm_count);
+  CU(cudaMemcpyAsync(d_dev, w.dinv, sizeof(double) * w.n, cudaMemcpyDeviceToDevice, st));
+  k_recip<<<g, 256, 0, st>>>(d_dev, w.n);
   CU(cudaGetLastError());
-  if ((rc = cg_reduce(hd, w.partial, w.rr, st))) return rc;
-  double bb = 0.0;
-  if (tol > 0) {
-    k_dot<<<CG_BLOCKS, CG_THREADS, 0, st>>>(b_dev, b_dev, n, w.partial);
-    if ((rc = cg_reduce(hd, w.partial, w.pq + w.cap, st))) return rc;
-    CU(cudaMemcpyAsync(&bb, w.pq + w.cap, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-  }
-  int k = 0;
-  for (; k < iters; ++k) {
-    if ((rc = dispatch_apply(hd, w.p, w.q, st))) return rc;  // q = A p (halo exchange inside)
-    k_dot<<<CG_BLOCKS, CG_THREADS, 0, st>>>(w.p, w.q, n, w.partial);
-    if ((rc = cg_reduce(hd, w.partial, w.pq + k, st))) return rc;
-    k_cg_xr<<<CG_BLOCKS, CG_THREADS, 0, st>>>(x_dev, w.r, w.p, w.q, n, w.rr, w.pq, k, w.partial);
-    CU(cudaGetLastError());
-    if ((rc = cg_reduce(hd, w.partial, w.rr + k + 1, st))) return rc;
-    k_cg_p<<<CG_BLOCKS, CG_THREADS, 0, st>>>(w.p, w.r, n, w.rr, k);
-    CU(cudaGetLastError());
-    if (tol > 0) {
-      double rk = 0.0;
-      CU(cudaMemcpyAsync(&rk, w.rr + k + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
-      if (std::sqrt(rk) <= tol * std::sqrt(bb)) {
-        ++k;
-        break;
-      }
-    }
-  }
-  if (res_hist) {
-    std::vector<double> h2(k + 1);
-    CU(cudaMemcpyAsync(h2.data(), w.rr, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    for (int i = 0; i <= k; ++i) res_hist[i] = std::sqrt(h2[i]);
-  } else {
-    CU(cudaStreamSynchronize(st));
-  }
-  if (iters_done) *iters_done = k;
   return 0;
 }
 

@@ -117,6 +117,7 @@ struct cutfem_handle {
   cutfem_stats_t stats;
   int64_t dev_bytes = 0;
   cutfem_cg_work *cg = nullptr;  // CG work vectors (lazy)
+  std::vector<int32_t> blk_ijk;  // cell of every block (owned, then ghosts): probe colouring
 };
 
 namespace {
@@ -1104,6 +1105,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   hd->h = pb->h;
   hd->n_active = na;
   hd->mask = pb->term_mask ? pb->term_mask : CUTFEM_TERM_ALL;
+  if (na > 0) hd->blk_ijk.assign(pb->active_ijk, pb->active_ijk + 3 * na);
   CU(cudaSetDevice(device));
   // grid -> block map
   std::vector<int32_t> grid((size_t)(nx * ny * nz), -1);

@@ -25,7 +25,11 @@ struct cutfem_h1 {
   int32_t *d_ent = nullptr;     // [n_blk] block entries of each node, ascending
   double *d_ub = nullptr, *d_vb = nullptr;
   std::vector<int32_t> map;     // host copy (cutfem_h1_map)
+  std::vector<int64_t> lat;     // lattice coordinates of every node (3 per node): probe colouring
+  cutfem_cg_work *cg = nullptr;
 };
+
+int cutfem_h1_apply_impl(cutfem_h1 *h, const double *u_dev, double *v_dev, cudaStream_t st);
 
 namespace {
 
@@ -46,6 +50,7 @@ __global__ void k_h1_scatter(double *__restrict__ v, const double *__restrict__ 
 
 void h1_free(cutfem_h1 *h) {
   if (!h) return;
+  cg_free(h->cg);
   if (h->dg) free_handle(h->dg);
   cudaFree(h->d_map);
   cudaFree(h->d_rp);
@@ -53,6 +58,22 @@ void h1_free(cutfem_h1 *h) {
   cudaFree(h->d_ub);
   cudaFree(h->d_vb);
   delete h;
+}
+
+// lattice colouring (I, J, K) mod (2p+1): nodes of one class share no cell and no
+// ghost-penalty face pair (a GP face couples nodes <= 2p lattice steps apart)
+int h1_probe_diag(cutfem_h1 *h, cudaStream_t st) {
+  cutfem_cg_work &w = *h->cg;
+  const int m = 2 * h->dg->degree + 1;
+  if (!w.probe_of) {
+    std::vector<int32_t> pr((size_t)h->n_h1);
+    for (int64_t g = 0; g < h->n_h1; ++g)
+      pr[g] = (int32_t)(((h->lat[3 * g] % m) * m + h->lat[3 * g + 1] % m) * m + h->lat[3 * g + 2] % m);
+    int rc = upload(h->dg, &w.probe_of, pr.data(), pr.size());
+    if (rc) return rc;
+  }
+  auto apply = [&](const double *u, double *v) { return cutfem_h1_apply_impl(h, u, v, st); };
+  return cg_probe_diag(w, m * m * m, apply, st, h->dg->sm_count, h->dg->dev_bytes);
 }
 
 }  // namespace
@@ -110,6 +131,12 @@ int cutfem_h1_setup(const cutfem_problem *pb, int device, cutfem_h1 **out) {
     h1_free(h);
     return fail(CUTFEM_EUNSUPPORTED, "H1 operator: nodes need int32");
   }
+  h->lat.resize(3 * h->n_h1);
+  for (int64_t g = 0; g < h->n_h1; ++g) {
+    h->lat[3 * g] = uk[g] / (LY * LZ);
+    h->lat[3 * g + 1] = (uk[g] / LZ) % LY;
+    h->lat[3 * g + 2] = uk[g] % LZ;
+  }
   h->map.resize(h->n_blk);
   std::vector<int64_t> rp(h->n_h1 + 1, 0);
   for (int64_t e = 0; e < h->n_blk; ++e) {
@@ -158,7 +185,12 @@ int cutfem_h1_apply(cutfem_h1 *h, const double *u_dev, double *v_dev, void *cuda
   if (((uintptr_t)u_dev | (uintptr_t)v_dev) & 7) return fail(CUTFEM_EINVAL, "vectors must be 8-byte aligned");
   if (h->n_h1 == 0) return 0;
   CU(cudaSetDevice(h->device));
-  cudaStream_t st = (cudaStream_t)cuda_stream;
+  return cutfem_h1_apply_impl(h, u_dev, v_dev, (cudaStream_t)cuda_stream);
+}
+
+}  // extern "C"
+
+int cutfem_h1_apply_impl(cutfem_h1 *h, const double *u_dev, double *v_dev, cudaStream_t st) {
   const int sms = h->dg->sm_count;
   const unsigned gb = (unsigned)std::min<int64_t>((h->n_blk + 255) / 256, 16 * sms);
   k_h1_gather<<<gb, 256, 0, st>>>(h->d_ub, u_dev, h->d_map, h->n_blk);
@@ -171,6 +203,8 @@ int cutfem_h1_apply(cutfem_h1 *h, const double *u_dev, double *v_dev, void *cuda
   return 0;
 }
 
+extern "C" {
+
 int cutfem_h1_rhs_const(cutfem_h1 *h, double f, double *b_dev, void *cuda_stream) {
   if (!h) return fail(CUTFEM_EINVAL, "null handle");
   if (h->n_h1 > 0 && !b_dev) return fail(CUTFEM_EINVAL, "null vector");
@@ -181,6 +215,44 @@ int cutfem_h1_rhs_const(cutfem_h1 *h, double f, double *b_dev, void *cuda_stream
   if (rc) return rc;
   const unsigned gs = (unsigned)std::min<int64_t>((h->n_h1 + 255) / 256, 16 * h->dg->sm_count);
   k_h1_scatter<<<gs, 256, 0, st>>>(b_dev, h->d_vb, h->d_rp, h->d_ent, h->n_h1);
+  CU(cudaGetLastError());
+  return 0;
+}
+
+int cutfem_h1_pcg(cutfem_h1 *h, const double *b_dev, double *x_dev, int iters, double tol, int precond,
+                  double *res_hist, int *iters_done, void *cuda_stream) {
+  if (!h) return fail(CUTFEM_EINVAL, "null handle");
+  if (iters < 0) return fail(CUTFEM_EINVAL, "iters < 0");
+  if (precond != CUTFEM_PRECOND_NONE && precond != CUTFEM_PRECOND_JACOBI) return fail(CUTFEM_EINVAL, "precond");
+  if (h->n_h1 > 0 && (!b_dev || !x_dev)) return fail(CUTFEM_EINVAL, "null vector");
+  if (((uintptr_t)b_dev | (uintptr_t)x_dev) & 15) return fail(CUTFEM_EINVAL, "vectors must be 16-byte aligned");
+  if (b_dev == x_dev && h->n_h1 > 0) return fail(CUTFEM_EINVAL, "b and x must not alias");
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (!h->cg) h->cg = new cutfem_cg_work();
+  cutfem_cg_work &w = *h->cg;
+  int rc;
+  if ((rc = cg_alloc(w, h->n_h1, h->n_h1, iters, h->dg->dev_bytes))) return rc;
+  auto apply = [&](const double *u, double *v) { return cutfem_h1_apply(h, u, v, st); };
+  auto reduce = [&](double *part, double *out) { return cg_reduce(nullptr, part, out, st); };
+  const bool jac = precond == CUTFEM_PRECOND_JACOBI;
+  if (jac && !w.dinv && (rc = h1_probe_diag(h, st))) return rc;
+  return cg_run(w, apply, reduce, b_dev, x_dev, iters, tol, jac, res_hist, iters_done, st);
+}
+
+int cutfem_h1_diag(cutfem_h1 *h, double *d_dev, void *cuda_stream) {
+  if (!h) return fail(CUTFEM_EINVAL, "null handle");
+  if (h->n_h1 > 0 && !d_dev) return fail(CUTFEM_EINVAL, "null vector");
+  CU(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (!h->cg) h->cg = new cutfem_cg_work();
+  cutfem_cg_work &w = *h->cg;
+  int rc;
+  if ((rc = cg_alloc(w, h->n_h1, h->n_h1, 1, h->dg->dev_bytes))) return rc;
+  if (!w.dinv && (rc = h1_probe_diag(h, st))) return rc;
+  const unsigned g = (unsigned)std::min<int64_t>((w.n + 255) / 256, 16 * h->dg->sm_count);
+  CU(cudaMemcpyAsync(d_dev, w.dinv, sizeof(double) * w.n, cudaMemcpyDeviceToDevice, st));
+  k_recip<<<g, 256, 0, st>>>(d_dev, w.n);
   CU(cudaGetLastError());
   return 0;
 }
