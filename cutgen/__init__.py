@@ -85,6 +85,8 @@ class Problem:
     nitsche_tau: float              # tau = nitsche_tau / h
     gp_gamma: np.ndarray            # f64 [degree+1], GP weight gp_gamma[j]*h^(2j-1)
     name: str = ""
+    gp_kind: int = 0                # 0 face ghost penalty, 1 volume ghost penalty (stable neighbour)
+    tau_v: float = 1.0              # volume GP penalty tau_v
     level_set: dict = field(default_factory=dict)
     n_subdivided: int = 0
     n_nonmonotone: int = 0
@@ -125,7 +127,7 @@ def _copy(ptr, n, dtype, shape):
 def generate(level_set: dict, n_cells, lower, upper, degree: int, *, q: int | None = None,
              max_depth: int = 3, force_cut_cells: bool = False, force_cut_faces: bool = False,
              sipg_gamma: float | None = None, nitsche_tau: float | None = None,
-             gp_gamma=None, nthreads: int = 0, name: str = "") -> Problem:
+             gp_gamma=None, nthreads: int = 0, name: str = "", gp_kind: int = 0, tau_v: float = 1.0) -> Problem:
     """Generate a problem.  ``level_set``: {"type": "sphere", "center": [..], "radius": r} |
     {"type": "gyroid", "c": c} | {"type": "plane", "normal": [..], "offset": o}.
     Penalties default to BASELINE.json: gamma = tau_D = 10 p^2, GP weights 0.1."""
@@ -182,7 +184,7 @@ def generate(level_set: dict, n_cells, lower, upper, degree: int, *, q: int | No
             sipg_gamma=float(sipg_gamma if sipg_gamma is not None else 10.0 * degree ** 2),
             nitsche_tau=float(nitsche_tau if nitsche_tau is not None else 10.0 * degree ** 2),
             gp_gamma=np.asarray(gp_gamma if gp_gamma is not None else [0.1] * (degree + 1), dtype=np.float64),
-            name=name, level_set=dict(level_set),
+            name=name, level_set=dict(level_set), gp_kind=int(gp_kind), tau_v=float(tau_v),
             n_subdivided=int(r.n_subdivided), n_nonmonotone=int(r.n_nonmonotone))
     finally:
         lib.cutgen_free(ctypes.byref(r))

@@ -80,7 +80,25 @@ typedef struct {
   double nitsche_tau;        /* tau   = nitsche_tau / h (BASELINE: 10 p^2)          */
   const double *gp_gamma;    /* [degree+1]: weight gp_gamma[j] * h^(2j-1) (BASELINE 0.1) */
   uint32_t term_mask;        /* CUTFEM_TERM_* bits; 0 means ALL                      */
+  int32_t gp_kind;           /* stabilisation: CUTFEM_GP_FACE (default, BASELINE configs[0])
+                                or CUTFEM_GP_VOLUME (PAPER eq:volume_based_gp P:96-108)  */
+  double tau_v;              /* volume GP: tau_v (P:595 uses 1); unused for face GP */
 } cutfem_problem;
+
+/* Ghost-penalty kinds.
+ * CUTFEM_GP_FACE: on every face between two active cells with >= 1 cut cell,
+ *   sum_{j=0..p} gp_gamma[j] h^(2j-1) int_F [d_n^j v][d_n^j u] (full-face Gauss).
+ * CUTFEM_GP_VOLUME: the paper's volume-based ghost penalty with the stable-neighbour
+ *   strategy: every cut cell forms ONE patch P = E1 u E2 with its most
+ *   stable face neighbour -- largest volume fraction |E cap Omega| / |E| (uncut = 1,
+ *   cut = sum of its volume weights / h^3), ties to the lowest face index 2d + s (s = 0
+ *   lower, 1 upper) (reading A23) -- duplicates merged, and
+ *   g_v = tau_v / h^2 int_P (v1 - v2)(u1 - u2) with v1, v2 the two cells' polynomials
+ *   extended to the whole patch (the extrapolation operator E), by the
+ *   (p+1)-point tensor Gauss rule on each cell (exact).  Not supported on distributed
+ *   handles (CUTFEM_EUNSUPPORTED: a ghost cell's choice needs a second ghost plane). */
+#define CUTFEM_GP_FACE 0
+#define CUTFEM_GP_VOLUME 1
 
 typedef struct {
   int64_t n_active, n_uncut, n_cut;

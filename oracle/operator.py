@@ -8,6 +8,8 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Follows SURVEY.md §8(c)
          + sum_F int_{F∩Ω} [-{∂_n v}[u] - [v]{∂_n u} + γ/h [v][u]]  (SIPG, eq:bilinear_dg P:85-90)
          + sum_{F touching a cut cell} sum_{j=0..p} g_j h^(2j-1) int_F [∂_n^j v][∂_n^j u]
                                                          (face ghost penalty, BASELINE configs[0])
+     or  + sum_{P} tau_v/h^2 int_P [v]_P [u]_P          (volume ghost penalty, eq:volume_based_gp
+                                                         P:96-108, stable-neighbour patches, prob.gp_kind = 1)
 
 with [·] = (·)^- - (·)^+, {·} = ((·)^- + (·)^+)/2, minus = lower cell,
 n = +e_d.  Uncut cells/faces and all GP faces use the tensor
@@ -59,6 +61,9 @@ class Oracle:
         WT, WS = np.meshgrid(gw, gw, indexing="ij")
         self.face_rule = np.stack([S.ravel(), T.ravel(), (WS * WT).ravel()], 1)
         self.faces = self._enumerate_faces()
+        self.gp_kind = int(getattr(prob, "gp_kind", 0))
+        self.tau_v = float(getattr(prob, "tau_v", 1.0))
+        self.patches = self._stable_neighbour_patches() if self.gp_kind == 1 else set()
 
     # ------------------------------------------------------------ basis
     def _phi(self, xi):
@@ -138,6 +143,31 @@ class Oracle:
                 out.append((K, L, d, self.sface.get((K, d), -1)))
         return out
 
+    def _stable_neighbour_patches(self):
+        """P:108 stable-neighbour strategy: every cut cell forms one patch with the face
+        neighbour of largest volume fraction |E cap Omega| / |E| (uncut cells: 1; cut cells:
+        sum of the volume weights / h^3), ties to the lowest face index 2d + s (s = 0 the
+        lower neighbour) -- DESIGN reading A23.  Returns {(minus, plus, d)}."""
+        P, h = self.P, self.h
+        frac = np.ones(len(self.ijk))
+        for K in np.where(self.is_cut)[0]:
+            c = self.cut_index[K]
+            frac[K] = P.vol_pts[P.vol_ptr[c]:P.vol_ptr[c + 1], 3].sum() / h ** 3
+        out = set()
+        for K in np.where(self.is_cut)[0]:
+            best = None
+            for f in range(6):
+                d, s = f // 2, f % 2
+                nb = [int(v) for v in self.ijk[K]]
+                nb[d] += 1 if s else -1
+                L = self.lookup.get(tuple(nb))
+                if L is not None and (best is None or frac[L] > frac[best[0]]):
+                    best = (L, d, s)
+            if best is not None:
+                L, d, s = best
+                out.add((int(K), L, d) if s else (L, int(K), d))
+        return out
+
     def face_matrix(self, minus: int, plus: int, d: int, sf: int, mask: int | None = None):
         """A_F (2n^3 x 2n^3) on [u^-; u^+]: SIPG + ghost penalty."""
         mask = self.mask if mask is None else mask
@@ -157,7 +187,20 @@ class Oracle:
                 Av = 0.5 * np.hstack([Dm, Dp])     # {∂_n v} rows
                 sigma = P.sipg_gamma / h
                 A += sigma * J.T @ (W[:, None] * J) - Av.T @ (W[:, None] * J) - J.T @ (W[:, None] * Av)
-        if mask & TERM_GP and (self.is_cut[minus] or self.is_cut[plus]):
+        if mask & TERM_GP and self.gp_kind == 1 and (minus, plus, d) in self.patches:
+            # volume GP on the patch E1 (minus) u E2 (plus): tau_v / h^2 int_P [v]_P [u]_P with
+            # [u]_E1 = u1 - E u2, [u]_E2 = E u1 - u2, E the polynomial extension into the
+            # neighbour; tensor Gauss with p+1 points per direction on each cell
+            cell = self.cell_rule.copy()
+            shift = np.zeros(3)
+            shift[d] = 1.0
+            for pts, off1, off2 in ((cell[:, :3], 0.0, -1.0), (cell[:, :3], 1.0, 0.0)):
+                Jm = self._phi(pts + off1 * shift)   # minus-cell basis at the points (its coordinates)
+                Jp = self._phi(pts + off2 * shift)   # plus-cell basis at the same points
+                J = np.hstack([Jm, -Jp])
+                W = cell[:, 3] * h ** 3
+                A += self.tau_v / h ** 2 * J.T @ (W[:, None] * J)
+        if mask & TERM_GP and self.gp_kind == 0 and (self.is_cut[minus] or self.is_cut[plus]):
             st, W = full[:, :2], full[:, 2]
             for j in range(self.p + 1):
                 Dm = self._normal_deriv_on_face(j, 1, d, st) * h ** (-j)

@@ -63,6 +63,7 @@ class _Problem(ctypes.Structure):
         ("sf_ptr", ctypes.c_void_p), ("sf_pts", ctypes.c_void_p),
         ("sipg_gamma", ctypes.c_double), ("nitsche_tau", ctypes.c_double),
         ("gp_gamma", ctypes.c_void_p), ("term_mask", ctypes.c_uint32),
+        ("gp_kind", ctypes.c_int32), ("tau_v", ctypes.c_double),
     ]
 
 
@@ -206,6 +207,8 @@ def _marshal(prob, term_mask=TERM_ALL):
     pb.sipg_gamma, pb.nitsche_tau = float(prob.sipg_gamma), float(prob.nitsche_tau)
     pb.gp_gamma = _ptr(keep["gp"])
     pb.term_mask = int(term_mask)
+    pb.gp_kind = int(getattr(prob, "gp_kind", 0))
+    pb.tau_v = float(getattr(prob, "tau_v", 1.0))
     return pb, keep
 
 

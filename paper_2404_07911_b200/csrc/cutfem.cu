@@ -185,29 +185,67 @@ int upload_tables(int p) {
   return 0;
 }
 
-void build_facetab(int p, double h, const double *gpg, FaceTab &ft) {
-  cutfem_tables::Ref r = cutfem_tables::build(p);
+// The 1-D ghost-penalty coupling of a face, own cell on the PLUS side (its lo face):
+// the face's stabilisation matrix is  (this 2n x 2n own/neighbour coupling) (x) in-face
+// mass M (x) M  for both kinds, so both run through the same line-operator code.
+//   face GP (BASELINE configs[0]): own-own  h sum_j g_j l_m^(j)(0) l_a^(j)(0),
+//     own-nb  -h sum_j g_j l_m^(j)(0) l_a^(j)(1)   (jump [.] = (.)^- - (.)^+, physical
+//     derivatives: g_j h^(2j-1) h^-2j h^2 = g_j h)
+//   volume GP: the patch E1 u E2 in the own cell's coordinates is
+//     [-1, 1] (the neighbour E1 at [-1, 0]); tau_v / h^2 int_P (u1 - u2)(v1 - v2) with
+//     the polynomials extended over the patch = tau_v h [G (x) M (x) M],
+//     own-own  tau_v h int_{-1}^{1} l_m l_a,  own-nb  -tau_v h int_{-1}^{1} l_m(y) l_a(y+1)
+//     ((p+1)-point Gauss on [-1,0] and [0,1]: exact for the degree-2p products).
+// The own-MINUS blocks are the centro-symmetric mirrors (GLL symmetry).
+void gp_blocks(int p, double h, const double *gpg, int kind, double tau_v, std::vector<long double> &oo,
+               std::vector<long double> &on) {
+  typedef long double ld;
   const int n = p + 1;
-  std::memset(&ft, 0, sizeof(ft));
-  for (int s = 0; s < 2; ++s) {
-    const int own = s == 0 ? 1 : 0, oth = 1 - own;  // s=0: own minus -> traces at xi=1
-    for (int m = 0; m < n; ++m)
-      for (int a = 0; a < n; ++a) {
-        long double goo = 0, gon = 0;
+  cutfem_tables::Ref r = cutfem_tables::build(p);
+  oo.assign(n * n, 0);
+  on.assign(n * n, 0);
+  auto tr = [&](int j, int s, int a) { return r.tr[(j * 2 + s) * n + a]; };
+  for (int m = 0; m < n; ++m)
+    for (int a = 0; a < n; ++a) {
+      if (kind == CUTFEM_GP_FACE) {
         for (int j = 0; j <= p; ++j) {
-          long double em = r.tr[(j * 2 + own) * n + m];
-          goo += (long double)gpg[j] * em * r.tr[(j * 2 + own) * n + a];
-          gon += (long double)gpg[j] * em * r.tr[(j * 2 + oth) * n + a];
+          oo[m * n + a] += (ld)h * gpg[j] * tr(j, 0, m) * tr(j, 0, a);
+          on[m * n + a] -= (ld)h * gpg[j] * tr(j, 0, m) * tr(j, 1, a);
         }
-        ft.Goo[s][m * n + a] = (double)(h * goo);
-        ft.Gon[s][m * n + a] = (double)(h * gon);
+      } else {
+        ld so = 0, sn = 0;
+        for (int q = 0; q < n; ++q)
+          for (int half = 0; half < 2; ++half) {
+            const ld y = r.g[q] - (half ? 0 : 1);  // [-1,0] then [0,1]
+            const ld lm = cutfem_tables::lag(r.x, m, y);
+            so += r.w[q] * lm * cutfem_tables::lag(r.x, a, y);
+            sn += r.w[q] * lm * cutfem_tables::lag(r.x, a, y + 1);
+          }
+        oo[m * n + a] = (ld)tau_v * h * so;
+        on[m * n + a] = -(ld)tau_v * h * sn;
       }
-  }
+    }
+}
+
+void build_facetab(int p, double h, const double *gpg, int kind, double tau_v, FaceTab &ft) {
+  const int n = p + 1;
+  std::vector<long double> oo, on;
+  gp_blocks(p, h, gpg, kind, tau_v, oo, on);
+  std::memset(&ft, 0, sizeof(ft));
+  // ft[s]: s = 0 own minus (mirror), s = 1 own plus; the kernels compute Goo uo - Gon un
+  for (int m = 0; m < n; ++m)
+    for (int a = 0; a < n; ++a) {
+      const int k = m * n + a, km = (n - 1 - m) * n + (n - 1 - a);
+      ft.Goo[1][k] = (double)oo[k];
+      ft.Gon[1][k] = (double)(-on[k]);
+      ft.Goo[0][k] = (double)oo[km];
+      ft.Gon[0][k] = (double)(-on[km]);
+    }
 }
 
 // ---- k_tile: per-handle line operators (long double, then rounded)
 template <int N>
-void build_tiletab(double h, double sipg_gamma, const double *gpg, TileTab<N> &tt) {
+void build_tiletab(double h, double sipg_gamma, const double *gpg, int gp_kind, double tau_v, TileTab<N> &tt) {
   typedef long double ld;
   const int p = N - 1, n = N;
   cutfem_tables::Ref r = cutfem_tables::build(p);
@@ -264,15 +302,9 @@ void build_tiletab(double h, double sipg_gamma, const double *gpg, TileTab<N> &t
     tt.cA[m] = (double)(al * hs);
     tt.d0[m] = (double)tr(1, 0, m);
   }
-  // ghost penalty (lo face, own coordinate 0, neighbour 1):
-  //   Goo[m][a] = h sum_j g_j l_m^(j)(0) l_a^(j)(0), Gon[m][a] = h sum_j g_j l_m^(j)(0) l_a^(j)(1)
-  std::vector<ld> Goo(n * n, 0), Gon(n * n, 0);
-  for (int m = 0; m < n; ++m)
-    for (int a = 0; a < n; ++a)
-      for (int j = 0; j <= p; ++j) {
-        Goo[m * n + a] += (ld)h * gpg[j] * tr(j, 0, m) * tr(j, 0, a);
-        Gon[m * n + a] += (ld)h * gpg[j] * tr(j, 0, m) * tr(j, 1, a);
-      }
+  // ghost penalty (lo face, own cell the plus side; gp_blocks): M^{-1}-premultiplied
+  std::vector<ld> Goo, Gon;
+  gp_blocks(p, h, gpg, gp_kind, tau_v, Goo, Gon);
   for (int m = 0; m < n; ++m)
     for (int a = 0; a < n; ++a) {
       ld go = 0, gn = 0;
@@ -281,14 +313,15 @@ void build_tiletab(double h, double sipg_gamma, const double *gpg, TileTab<N> &t
         gn += Mi[m * n + k] * Gon[k * n + a];
       }
       tt.Goo[m * n + a] = (double)go;
-      tt.Gon[m * n + a] = (double)(-gn);
+      tt.Gon[m * n + a] = (double)gn;
     }
 }
 
 template <int N>
 int build_ttab(cutfem_handle *hd, const cutfem_problem *pb) {
   hd->ttab.resize(sizeof(TileTab<N>));
-  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
+  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, pb->gp_kind, pb->tau_v,
+                   *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
   return 0;
 }
 
@@ -760,7 +793,8 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     }
   }
   hd->ttab.resize(sizeof(TileTab<N>));
-  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
+  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, pb->gp_kind, pb->tau_v,
+                   *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
   if constexpr (N == 4) {
     using C2 = Tile2Cfg<N>;
     CU(cudaFuncSetAttribute(k_tile2<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
@@ -814,7 +848,8 @@ int setup_uncw(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<UD
   int rc = upload(hd, reinterpret_cast<char **>(&hd->d_tiles), b0.data(), b0.size());
   if (rc) return rc;
   hd->ttab.resize(sizeof(TileTab<N>));
-  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
+  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, pb->gp_kind, pb->tau_v,
+                   *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
   CU(cudaFuncSetAttribute(k_uncw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncwCfg<N>::SMEM));
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_uncw<N>, UncwCfg<N>::THREADS,
                                                    UncwCfg<N>::SMEM));
@@ -1179,6 +1214,48 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
     sfid[pl * 6 + 2 * d] = (int32_t)f;
     if (pb->sf_ptr[f + 1] > pb->sf_ptr[f]) ++n_fcut; else ++n_fempty;
   }
+  // ghost-penalty faces per (block, face): face GP on every face with a cut side;
+  // volume GP on the stable-neighbour patches (include/cutfem.h CUTFEM_GP_VOLUME)
+  if (pb->gp_kind != CUTFEM_GP_FACE && pb->gp_kind != CUTFEM_GP_VOLUME) return fail(CUTFEM_EINVAL, "gp_kind");
+  if (pb->gp_kind == CUTFEM_GP_VOLUME && !(pb->tau_v >= 0)) return fail(CUTFEM_EINVAL, "tau_v < 0");
+  if (pb->gp_kind == CUTFEM_GP_VOLUME && n_compute >= 0 && n_compute != na)
+    return fail(CUTFEM_EUNSUPPORTED, "volume ghost penalty on a distributed handle");
+  auto nb_of = [&](int64_t b, int f) -> int32_t {
+    int32_t q[3] = {pb->active_ijk[3 * b], pb->active_ijk[3 * b + 1], pb->active_ijk[3 * b + 2]};
+    const int d = f >> 1;
+    q[d] += (f & 1) ? 1 : -1;
+    if (q[d] < 0 || q[d] >= pb->n_cells[d]) return -1;
+    return grid[(size_t)((q[0] * ny + q[1]) * nz + q[2])];
+  };
+  std::vector<uint8_t> gpf((size_t)na * 6, 0);
+  if (pb->gp_kind == CUTFEM_GP_FACE) {
+    for (int64_t b = 0; b < na; ++b)
+      for (int f = 0; f < 6; ++f) {
+        const int32_t q = nb_of(b, f);
+        if (q >= 0 && (pb->is_cut[b] || pb->is_cut[q])) gpf[b * 6 + f] = 1;
+      }
+  } else {
+    std::vector<double> frac(na, 1.0);  // |E cap Omega| / |E|: 1 for uncut cells
+    const double h3 = pb->h * pb->h * pb->h;
+    for (int64_t b = 0; b < na; ++b)
+      if (pb->is_cut[b]) {
+        const int64_t c = cut_ord[b];
+        double s = 0;
+        for (int64_t q = pb->vol_ptr[c]; q < pb->vol_ptr[c + 1]; ++q) s += pb->vol_pts[4 * q + 3];
+        frac[b] = s / h3;
+      }
+    for (int64_t b = 0; b < na; ++b) {
+      if (!pb->is_cut[b]) continue;
+      int best = -1;
+      for (int f = 0; f < 6; ++f) {
+        const int32_t q = nb_of(b, f);
+        if (q >= 0 && (best < 0 || frac[q] > frac[nb_of(b, best)])) best = f;
+      }
+      if (best < 0) continue;  // an isolated cut cell: nothing to stabilise against
+      gpf[b * 6 + best] = 1;
+      gpf[(size_t)nb_of(b, best) * 6 + (best ^ 1)] = 1;
+    }
+  }
   // descriptors
   std::vector<UDesc> ud;
   std::vector<CDesc> cd;
@@ -1211,7 +1288,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
       u.blk = (int32_t)b;
       for (int f = 0; f < 6; ++f) {
         u.nb[f] = nb[f];
-        if (nb[f] >= 0 && pb->is_cut[nb[f]]) u.flags |= 1u << f;
+        if (nb[f] >= 0 && gpf[b * 6 + f]) u.flags |= 1u << f;  // ghost-penalty face
       }
       ud.push_back(u);
     } else {
@@ -1228,7 +1305,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
         c.nb[f] = nb[f];
         c.sf[f] = -1;
         if (nb[f] < 0) continue;
-        c.flags |= 1u << f;  // ghost penalty: this cell is cut
+        if (gpf[b * 6 + f]) c.flags |= 1u << f;  // ghost-penalty face
         const int32_t s = sfid[b * 6 + f];
         if (s < 0) {
           c.flags |= 1u << (6 + f);
@@ -1262,7 +1339,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
     for (int d = 0; d < 3; ++d) {
       const int32_t q = nb[2 * d + 1];
       if (q < 0) continue;
-      if (cut || pb->is_cut[q]) ++n_gp;
+      if (gpf[b * 6 + 2 * d + 1]) ++n_gp;
       if (sfid[b * 6 + 2 * d + 1] < 0) ++n_struct;
     }
   }
@@ -1356,7 +1433,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
     cudaDeviceGetAttribute(&smc, cudaDevAttrMultiProcessorCount, dev);
     hd->sm_count = smc;
   }
-  build_facetab(p, pb->h, pb->gp_gamma, hd->ft);
+  build_facetab(p, pb->h, pb->gp_gamma, pb->gp_kind, pb->tau_v, hd->ft);
   hd->kp.h = pb->h;
   hd->kp.sigma = pb->sipg_gamma / pb->h;
   hd->kp.tau = pb->nitsche_tau / pb->h;
