@@ -152,7 +152,10 @@ class Oracle:
         frac = np.ones(len(self.ijk))
         for K in np.where(self.is_cut)[0]:
             c = self.cut_index[K]
-            frac[K] = P.vol_pts[P.vol_ptr[c]:P.vol_ptr[c + 1], 3].sum() / h ** 3
+            acc = 0.0  # sequential fp64 sum in point order: the argmax below is a floating-point
+            for w in P.vol_pts[P.vol_ptr[c]:P.vol_ptr[c + 1], 3].tolist():  # decision, taken in
+                acc += w  # the same arithmetic as the library's setup (DESIGN reading A23)
+            frac[K] = acc / (h * h * h)
         out = set()
         for K in np.where(self.is_cut)[0]:
             best = None
