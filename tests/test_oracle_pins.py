@@ -592,3 +592,16 @@ def test_oracle_cg_solves_spd_system():
     assert np.abs(x - np.linalg.solve(A, b)).max() <= 1e-12 * np.abs(x).max()
     x, it = cg(lambda y: A @ y, b, tol=0.0, maxiter=3)
     assert it == 3
+
+
+def test_oracle_spmv_c_matches_scipy(cutgen_mod):
+    """oracle/csrc/spmv.c (the host-core sparse baseline) = scipy's CSR product on the
+    oracle-assembled C1 matrix, for 1 and several threads."""
+    from oracle import spmv
+    P = cutgen_mod.config("C1")
+    M = Oracle(P).assemble_csr()
+    u = P.seeded_u(2)
+    ref = M @ u
+    for nt in (1, 3):
+        y, _ = spmv.spmv(M, u, nthreads=nt)
+        assert np.abs(y - ref).max() <= 1e-13 * np.abs(ref).max()
