@@ -1,0 +1,66 @@
+"""Race / synchronisation evidence without compute-sanitizer (closed on this GPU
+pool): every kernel family's apply repeated many times back to back -- with the L2
+flushed in between, with the two-step launches interleaved with other work on the
+stream -- must give BIT-IDENTICAL results (a shared-memory race, a missed mbarrier
+phase or a missing PDL dependency shows up as run-to-run differences), and equal the
+oracle (a stale read shows up as a wrong value)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from test_gpu_parity import check  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def cf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_07911_b200 as m
+    m.load()
+    return m
+
+
+CASES = [(1, 8), (2, 8), (3, 10), (4, 6), (5, 6), (6, 5), (7, 5), (8, 4)]
+
+
+@pytest.mark.parametrize("p,N", CASES)
+def test_repeated_applies_bit_identical(cf, cutgen_mod, p, N):
+    P = cutgen_mod.generate(cutgen_mod.SPHERE, N, -1.0, 1.0, p)
+    op = cf.CutFEM(P)
+    u = torch.from_numpy(P.seeded_u(1)).cuda()
+    v0 = op.apply(u).clone()
+    junk = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    vs = [torch.empty_like(v0) for _ in range(4)]
+    for k in range(60):
+        if k % 3 == 0:
+            junk.zero_()  # flush L2 between applies
+        op.apply(u, vs[k % 4])
+        if k % 4 == 3:
+            torch.cuda.synchronize()
+            for w in vs:
+                assert torch.equal(w, v0), (p, k)
+    check(P, v0.cpu().numpy(), P.seeded_u(1))
+
+
+def test_cg_loop_bit_identical(cf, cutgen_mod):
+    """50 CG iterations (apply + dots + axpys, no host sync inside) twice: identical."""
+    P = cutgen_mod.config("C1", degree=3)
+    op = cf.CutFEM(P)
+    b = op.rhs_const(1.0)
+    x0, h0 = op.cg(b, iters=50)
+    x1, h1 = op.cg(b, iters=50)
+    assert torch.equal(x0, x1) and np.array_equal(h0, h1)
+
+
+def test_c2_repeated(cf, cutgen_mod):
+    P = cutgen_mod.config("C2")
+    op = cf.CutFEM(P)
+    u = torch.from_numpy(P.seeded_u(0)).cuda()
+    v0 = op.apply(u).clone()
+    v = torch.empty_like(v0)
+    for _ in range(30):
+        op.apply(u, v)
+    torch.cuda.synchronize()
+    assert torch.equal(v, v0)
