@@ -22,7 +22,7 @@ def cf():
     return m
 
 
-CASES = [(1, 8), (2, 8), (3, 10), (4, 6), (5, 6), (6, 5), (7, 5), (8, 4)]
+CASES = [(1, 8), (2, 8), (3, 10), (4, 6), (5, 6), (6, 5), (7, 6), (8, 6)]
 
 
 @pytest.mark.parametrize("p,N", CASES)
