@@ -245,7 +245,8 @@ void build_facetab(int p, double h, const double *gpg, int kind, double tau_v, F
 
 // ---- k_tile: per-handle line operators (long double, then rounded)
 template <int N>
-void build_tiletab(double h, double sipg_gamma, const double *gpg, int gp_kind, double tau_v, TileTab<N> &tt) {
+void build_tiletab(double h, double sipg_gamma, const double *gpg, int gp_kind, double tau_v, uint32_t mask,
+                   TileTab<N> &tt) {
   typedef long double ld;
   const int p = N - 1, n = N;
   cutfem_tables::Ref r = cutfem_tables::build(p);
@@ -315,12 +316,29 @@ void build_tiletab(double h, double sipg_gamma, const double *gpg, int gp_kind, 
       tt.Goo[m * n + a] = (double)go;
       tt.Gon[m * n + a] = (double)gn;
     }
+  // folded operator for cells with six faces (k_tile2): Lf = L (cell term) + the own
+  // parts of both SIPG faces, lo face F[m][k] = cJ[m] delta_k0 + cA[m] d0[k], hi face its
+  // mirror; neighbour coefficients nJ = -cJ, nA = -cA (0 without the SIPG term)
+  const bool con = (mask & CUTFEM_TERM_CELL) != 0, son = (mask & CUTFEM_TERM_SIPG) != 0;
+  for (int m = 0; m < n; ++m) {
+    for (int k = 0; k < n; ++k) {
+      ld x = con ? (ld)tt.L[m * n + k] : 0;
+      if (son) {
+        const int mm = n - 1 - m, km = n - 1 - k;
+        x += (k == 0 ? (ld)tt.cJ[m] : 0) + (ld)tt.cA[m] * tt.d0[k];
+        x += (km == 0 ? (ld)tt.cJ[mm] : 0) + (ld)tt.cA[mm] * tt.d0[km];
+      }
+      tt.Lf[m * n + k] = (double)x;
+    }
+    tt.nJ[m] = son ? -tt.cJ[m] : 0.0;
+    tt.nA[m] = son ? -tt.cA[m] : 0.0;
+  }
 }
 
 template <int N>
 int build_ttab(cutfem_handle *hd, const cutfem_problem *pb) {
   hd->ttab.resize(sizeof(TileTab<N>));
-  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, pb->gp_kind, pb->tau_v,
+  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, pb->gp_kind, pb->tau_v, hd->mask,
                    *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
   return 0;
 }
@@ -499,7 +517,9 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
 #ifdef UNCW4_ALL
         set[1][pt - 1].push_back(c);
 #else
-        set[c.gp ? 1 : 0][pt - 1].push_back(c);
+        // k_tile2 (folded operators) takes the cells with all six faces and no ghost
+        // penalty; the rest (next to cut cells, on the box boundary) go to k_uncw<4>
+        set[(c.gp || nbm != 0x3fu) ? 1 : 0][pt - 1].push_back(c);
 #endif
 #endif
       }
@@ -793,7 +813,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     }
   }
   hd->ttab.resize(sizeof(TileTab<N>));
-  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, pb->gp_kind, pb->tau_v,
+  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, pb->gp_kind, pb->tau_v, hd->mask,
                    *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
   if constexpr (N == 4) {
     using C2 = Tile2Cfg<N>;
@@ -848,7 +868,7 @@ int setup_uncw(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<UD
   int rc = upload(hd, reinterpret_cast<char **>(&hd->d_tiles), b0.data(), b0.size());
   if (rc) return rc;
   hd->ttab.resize(sizeof(TileTab<N>));
-  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, pb->gp_kind, pb->tau_v,
+  build_tiletab<N>(pb->h, pb->sipg_gamma, pb->gp_gamma, pb->gp_kind, pb->tau_v, hd->mask,
                    *reinterpret_cast<TileTab<N> *>(hd->ttab.data()));
   CU(cudaFuncSetAttribute(k_uncw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncwCfg<N>::SMEM));
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_uncw<N>, UncwCfg<N>::THREADS,

@@ -92,6 +92,12 @@ struct TileTab {
   double cA[N];
   double Goo[N * N];  // ghost penalty (lo face), own line:        M^{-1} G_oo
   double Gon[N * N];  // ghost penalty (lo face), neighbour line: -M^{-1} G_on
+  // k_tile2 (cells with all six faces, no ghost penalty): the volume line operator and
+  // the OWN-side SIPG parts of both faces folded into one operator (centro-symmetric),
+  // the neighbour parts as a rank-2 update (lo face: w += nJ u_nb(N-1) + nA sum_k
+  // d0[N-1-k] u_nb(k); the hi face mirrored); the handle's term mask is built in
+  double Lf[N * N];
+  double nJ[N], nA[N];
 };
 
 // canonical index of a centro-symmetric n x n matrix entry

@@ -51,6 +51,9 @@
 #ifndef UNCW4_TC
 #define UNCW4_TC 8  // cells per k_uncw<4> tile (the cells next to cut cells at n = 4)
 #endif
+#ifndef K2_FOLD
+#define K2_FOLD 1  // k_tile2: folded volume + own-side SIPG operator (cells with six faces)
+#endif
 #ifndef K1_TC
 #define K1_TC 32  // cells per k_tile2 tile (16 measured: structured 40 -> 42 us, apply 109 -> 150 us at C2)
 #endif
@@ -238,6 +241,57 @@ __device__ __forceinline__ void axis_plane(double (&w)[W], const double *Up, con
   }
 }
 
+// ---- folded forms (K2_FOLD): cells with all six faces; tt.Lf holds the volume
+// operator plus the own-side SIPG parts of both faces, so a line costs one n x n
+// product plus the neighbours' rank-2 parts (J_nb = a neighbour trace value, A_nb =
+// its normal derivative: n FMAs per face) -- 12 instead of 20 operations per line and
+// face.
+template <int N, int D, int W>
+__device__ __forceinline__ void lineop_f(double (&w)[W], int t, const double (&uo)[N], const double (&ul)[N],
+                                         const double (&uh)[N], const TileTab<N> &tt) {
+  double Al = 0.0, Ah = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    Al = fma(tt.d0[N - 1 - k], ul[k], Al);  // lo neighbour (minus side): its l'(1) = -d0 mirrored
+    Ah = fma(tt.d0[k], uh[k], Ah);          // hi neighbour (plus side): its l'(0)
+  }
+  const double Jl = ul[N - 1], Jh = uh[0];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double r = w[lix<N, D>(t, i)];
+#pragma unroll
+    for (int j = 0; j < N; ++j) r = fma(tt.Lf[csym<N>(i * N + j)], uo[j], r);
+    r = fma(tt.nJ[i], Jl, fma(tt.nA[i], Al, r));
+    r = fma(tt.nJ[N - 1 - i], Jh, fma(tt.nA[N - 1 - i], Ah, r));
+    w[lix<N, D>(t, i)] = r;
+  }
+}
+
+template <int N, int D, int W>
+__device__ __forceinline__ void axis_plane_f(double (&w)[W], const double *Up, const double *Lp, const double *Hp,
+                                             int cc, const TileTab<N> &tt) {
+  if constexpr (D == 1 && (N % 2) == 0) {
+#pragma unroll
+    for (int q = 0; q < N; q += 2) {
+      double u0[N], u1[N], l0[N], l1[N], h0[N], h1[N];
+      ld_pair<N, D>(Up, q, u0, u1);
+      ld_pair<N, D>(Lp, q, l0, l1);
+      ld_pair<N, D>(Hp, q, h0, h1);
+      lineop_f<N, D>(w, q + N * cc, u0, l0, h0, tt);
+      lineop_f<N, D>(w, q + 1 + N * cc, u1, l1, h1, tt);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double u0[N], l0[N], h0[N];
+      ld_line<N, D>(Up, q, u0);
+      ld_line<N, D>(Lp, q, l0);
+      ld_line<N, D>(Hp, q, h0);
+      lineop_f<N, D>(w, q + N * cc, u0, l0, h0, tt);
+    }
+  }
+}
+
 // z-line t = a + N b read in the thread's frame: position m at zb + zs*m
 template <int N>
 __device__ __forceinline__ void ld_zpair(const double *B, int t, int zb, int zs, double (&a)[N], double (&b)[N]) {
@@ -278,6 +332,29 @@ __device__ __forceinline__ void z_line(double (&w)[W], int t, const double (&uo)
     double &r = w[t + NN * c];
     r = fma(tt.cJ[c], Jl, fma(tt.cA[c], Al, r));
     r = fma(tt.cJ[N - 1 - c], Jh, fma(-tt.cA[N - 1 - c], Ah, r));
+  }
+}
+
+// folded z line: rows 0..P-1 of Lf on the own line, the lo neighbour's parts, and the
+// hi neighbour's parts from the partner (its lo neighbour in its mirrored frame:
+// J' = u_hi(0), A' = sum_k d0[k] u_hi(k) -- no sign change)
+template <int N, int W>
+__device__ __forceinline__ void z_line_f(double (&w)[W], int t, const double (&uo)[N], const double (&ul)[N],
+                                         unsigned act, const TileTab<N> &tt) {
+  constexpr int P = N / 2, NN = N * N;
+  double An = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) An = fma(tt.d0[N - 1 - k], ul[k], An);
+  const double Jn = ul[N - 1];
+  const double Jp = __shfl_xor_sync(act, Jn, 16), Ap = __shfl_xor_sync(act, An, 16);
+#pragma unroll
+  for (int c = 0; c < P; ++c) {
+    double r = w[t + NN * c];
+#pragma unroll
+    for (int j = 0; j < N; ++j) r = fma(tt.Lf[csym<N>(c * N + j)], uo[j], r);
+    r = fma(tt.nJ[c], Jn, fma(tt.nA[c], An, r));
+    r = fma(tt.nJ[N - 1 - c], Jp, fma(tt.nA[N - 1 - c], Ap, r));
+    w[t + NN * c] = r;
   }
 }
 
@@ -390,7 +467,25 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
 #pragma unroll
     for (int f = 0; f < 6; ++f) Nb[f] = nbs[f] != 0xff ? S + nbs[f] * ST : Us;  // dummy source when absent
     static_assert(MODE == 0, "k_tile2: volume + SIPG only");
-    if (on) {
+    if (on && K2_FOLD) {
+      // every k_tile2 cell has six faces and no ghost penalty (host routing): folded operators
+      static_for<0, 2>([&](auto dc) {
+        constexpr int D = decltype(dc)::value;
+#pragma unroll
+        for (int cc = 0; cc < P; ++cc) {
+          const int pz = zb + zs * cc;
+          axis_plane_f<N, D>(w, Us + pz, Nb[2 * D] + pz, Nb[2 * D + 1] + pz, cc, tt);
+        }
+      });
+#pragma unroll
+      for (int t = 0; t < NN; t += 2) {
+        double u0[N], u1[N], a0[N], a1[N];
+        ld_zpair<N>(Us, t, zb, zs, u0, u1);
+        ld_zpair<N>(Nb[4], t, zb, zs, a0, a1);
+        z_line_f<N>(w, t, u0, a0, act, tt);
+        z_line_f<N>(w, t + 1, u1, a1, act, tt);
+      }
+    } else if (on) {
       {
         const double ev = vol ? 1.0 : 0.0;
         // x and y: plane-local
