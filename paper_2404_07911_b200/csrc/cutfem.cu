@@ -333,6 +333,15 @@ void build_tiletab(double h, double sipg_gamma, const double *gpg, int gp_kind, 
     tt.nJ[m] = son ? -tt.cJ[m] : 0.0;
     tt.nA[m] = son ? -tt.cA[m] : 0.0;
   }
+  {
+    std::vector<ld> Ll(n * n), Ml(n * n);
+    for (int k = 0; k < n * n; ++k) {
+      Ll[k] = tt.L[k];
+      Ml[k] = r.M[k];
+    }
+    make_eo(n, Ll, tt.Leo);
+    make_eo(n, Ml, tt.Meo);
+  }
 }
 
 template <int N>

@@ -98,6 +98,7 @@ struct TileTab {
   // d0[N-1-k] u_nb(k); the hi face mirrored); the handle's term mask is built in
   double Lf[N * N];
   double nJ[N], nA[N];
+  EO Leo, Meo;  // even-odd factors of L and M (k_uncw, n >= 5; north_star "even-odd decomposition")
 };
 
 // canonical index of a centro-symmetric n x n matrix entry
