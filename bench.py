@@ -408,11 +408,12 @@ def run_ours(args, P, cfg, rank, world, local_rank):
     bw = float(peaks.get("hbm_gbs", 6543.7)) * 1e9
     fp64 = costmodel.fp64_peak_tflops() * 1e12
     n_ = P.degree + 1
-    if n_ <= 4:
-        kname = {"structured": (f"k_tile2<{n_},0>" if n_ == 4 else f"k_tile<{n_},0>") + f" + k_gpw<{n_}>",
-                 "unstructured": f"k_cutp<{n_}>"}
+    if n_ <= 3:
+        kname = {"structured": f"k_cell<{n_}>", "unstructured": f"k_cutp<{n_}>"}
+    elif n_ == 4:
+        kname = {"structured": "k_tile2<4,0> + k_uncw<4,8>", "unstructured": "k_cutp<4>"}
     else:
-        kname = {"structured": f"k_uncw<{n_}>" if n_ in (5, 6) else f"k_uncut<{n_}>", "unstructured": f"k_cut<{n_}>"}
+        kname = {"structured": f"k_uncw<{n_}>" if n_ in (5, 6, 8) else f"k_uncut<{n_}>", "unstructured": f"k_cut<{n_}>"}
     dom = max(k_ms, key=k_ms.get)
     F_dom = work["F_uncut"] if dom == "structured" else work["F_cut"]
     B_dom = work["B_uncut"] if dom == "structured" else work["B_cut"]
