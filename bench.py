@@ -403,7 +403,8 @@ def run_ours(args, P, cfg, rank, world, local_rank):
     if world > 1:
         own = np.zeros(P.n_active, bool)
         own[g0:g0 + n_own] = True
-    work = costmodel.apply_work(st, costmodel.face_classes(P, own))
+    classes = costmodel.face_classes(P, own)
+    work = costmodel.apply_work(st, classes)
     peaks = load_peaks()
     bw = float(peaks.get("hbm_gbs", 6543.7)) * 1e9
     fp64 = costmodel.fp64_peak_tflops() * 1e12
@@ -435,7 +436,13 @@ def run_ours(args, P, cfg, rank, world, local_rank):
                           "byte_per_dof": work["B_total"] / max(op.n_dofs, 1),
                           "t_roof_ms": t_roof * 1e3, "frac": t_roof / (ms_step * 1e-3),
                           "hbm_gbs": bw / 1e9, "fp64_tflops": fp64 / 1e12},
-                "per_kernel_ms": k_ms, "scope": "rank 0" if world > 1 else "whole problem"}
+                "per_kernel_ms": k_ms, "scope": "rank 0" if world > 1 else "whole problem",
+                "work_counts": {**{k: int(st[k]) for k in ("n_uncut", "n_cut", "n_vol_pts", "n_srf_pts",
+                                                               "n_face_pts", "n_dofs", "degree")},
+                                **{k: int(v) for k, v in classes.items()}},
+                "recompute": "F_cut = n_vol_pts*vol(n) + n_srf_pts*srf(n) + 4*(cutface_side*n^3 + "
+                             "cutface_pts_side*(3n^2+4n)) + sipg_side_cut*face(n)/2 + gp_side_cut*gp(n)/2 "
+                             "(costmodel.py; DESIGN 5.4); frac = F / kernel_ms / peak"}
 
     # end to end through the public API with pinned host buffers
     uh = torch.from_numpy(ug[g0 * nd:(g0 + n_own) * nd].copy()).pin_memory()
