@@ -29,6 +29,12 @@
 #include "../../include/cutfem.h"
 #include "kernels.cuh"
 #include "tables.h"
+#ifndef CUT_ORDER
+#define CUT_ORDER 2  // measured: C5 apply 5566 -> 5457 us, C3 p=6 -1 %, p=8 neutral (pure spatial: p=8 +30 %)
+#endif
+#ifndef CUT_HEAVY_PCT
+#define CUT_HEAVY_PCT 5
+#endif
 
 namespace {
 
@@ -1401,8 +1407,25 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   {
     std::vector<int64_t> order(cd.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int64_t)i;
+    // n >= 5 (k_cut: one CTA per cut cell, in this order): CUT_ORDER 0 heaviest first;
+    // 1 spatial (block order: neighbour blocks shared by consecutive CTAs stay in L2);
+    // 2 the heaviest CUT_HEAVY_PCT % first, the rest spatial
+    const int corder = n >= 5 ? CUT_ORDER : 0;
+    std::vector<uint8_t> heavy(cd.size(), 0);
+    if (corder == 2 && !cd.empty()) {
+      std::vector<int64_t> cs(ccost.begin(), ccost.end());
+      const size_t k = std::min(cs.size() - 1, (size_t)(cs.size() * (100 - CUT_HEAVY_PCT) / 100));
+      std::nth_element(cs.begin(), cs.begin() + k, cs.end());
+      for (size_t i = 0; i < cd.size(); ++i) heavy[i] = ccost[i] > cs[k];
+    }
     std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
       if (cbnd[a] != cbnd[b]) return cbnd[a] < cbnd[b];
+      if (corder == 1) return cd[a].blk < cd[b].blk;
+      if (corder == 2) {
+        if (heavy[a] != heavy[b]) return heavy[a] > heavy[b];
+        if (heavy[a]) return ccost[a] > ccost[b];
+        return cd[a].blk < cd[b].blk;
+      }
       return ccost[a] > ccost[b];
     });
     std::vector<CDesc> s(cd.size());
