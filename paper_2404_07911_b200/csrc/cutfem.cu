@@ -575,6 +575,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     // coordinates [xi, eta, zeta, W] (normal coordinate exactly 0 or 1)
     std::vector<CDesc2> c2(cd.size());
     std::vector<double> fac;
+    std::vector<std::array<int, 6>> fcn(cd.size());  // cut-face points per face of the cell
     for (size_t i = 0; i < cd.size(); ++i) {
       const CDesc &d = cd[i];
       CDesc2 &e = c2[i];
@@ -602,8 +603,53 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
           x[3] = pb->sf_pts[3 * q + 2];
           fac.insert(fac.end(), x, x + 4);
         }
+        fcn[i][f] = (int)(pb->sf_ptr[d.sf[f] + 1] - pb->sf_ptr[d.sf[f]]);
       }
       e.nf = (int32_t)((int64_t)fac.size() / 4 - e.fb);
+    }
+    // cut-face points in LINES (k_cutp<4>, face_line_rt): per cell, line records
+    // [xg, f + 8 la, (x_t, W_t) x N] into flrec (fl0[i] = the cell's first record, -1 if
+    // some face's points are not all in lines: the cell then streams single points)
+    std::vector<double> flrec;
+    std::vector<int64_t> fl0(cd.size(), -1);
+    std::vector<int> fln(cd.size(), 0);
+    if constexpr (CutPCfg<N>::FLINES) {
+      for (size_t i = 0; i < cd.size(); ++i) {
+        const CDesc2 &e = c2[i];
+        if (e.nf <= 0) continue;
+        std::vector<double> rec;
+        bool ok = true;
+        int64_t row = e.fb;
+        for (int f = 0; f < 6 && ok; ++f) {
+          const int cnt = fcn[i][f];
+          if (cnt % N != 0) ok = false;
+          const int dd = f >> 1, e1 = dd == 0 ? 1 : 0, e2 = dd == 2 ? 1 : 2;
+          for (int g = 0; g < cnt && ok; g += N) {
+            const double *a = &fac[4 * (row + g)];
+            int la = -1;
+            for (int t = 1; t < N && ok; ++t) {
+              const double *b = &fac[4 * (row + g + t)];
+              const bool s1 = a[e1] == b[e1], s2 = a[e2] == b[e2];
+              const int v = (s1 && !s2) ? e2 : ((s2 && !s1) ? e1 : -1);
+              if (v < 0 || (la >= 0 && v != la)) ok = false;
+              la = v;
+            }
+            if (!ok) break;
+            const int ga = 3 - dd - la;
+            rec.push_back(a[ga]);
+            rec.push_back((double)(f + 8 * la));
+            for (int t = 0; t < N; ++t) {
+              rec.push_back(fac[4 * (row + g + t) + la]);
+              rec.push_back(fac[4 * (row + g + t) + 3]);
+            }
+          }
+          row += cnt;
+        }
+        if (!ok) continue;
+        fl0[i] = (int64_t)flrec.size() / (2 + 2 * N);
+        fln[i] = (int)(rec.size() / (2 + 2 * N));
+        flrec.insert(flrec.end(), rec.begin(), rec.end());
+      }
     }
     CU(cudaFuncSetAttribute(k_cutp<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutPCfg<N>::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_cutp, k_cutp<N>, 32 * CutPCfg<N>::WARPS,
@@ -632,9 +678,11 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       }
       auto cost = [&](const CDesc2 &e) {
         const int64_t i = &e - c2.data();
-        const int nf = e.nf;
-        if (isline[i]) return 2.8 * ((e.nv / N + 31) / 32) + (double)((e.ns + nf + 31) / 32) + 1.5;
-        return (double)((e.nv + e.ns + nf + 31) / 32) + 1.5;
+        // a chunk of 32 cut-face lines costs about 1.2 point chunks
+        const double fl = fl0[i] >= 0 ? 1.2 * ((fln[i] + 31) / 32) : 0.0;
+        const int nf = fl0[i] >= 0 ? 0 : e.nf;
+        if (isline[i]) return 2.8 * ((e.nv / N + 31) / 32) + (double)((e.ns + nf + 31) / 32) + fl + 1.5;
+        return (double)((e.nv + e.ns + nf + 31) / 32) + fl + 1.5;
       };
       for (int64_t i = 0; i < n; ++i) idx[i] = o + i;
       std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return cost(c2[a]) > cost(c2[b]); });
@@ -685,7 +733,20 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
             nv = 0;
             if (son) ns = 0;
           }
-          const bool fdone = false;
+          // cut-face lines of every face in chunks of <= 32 (bit 30, first record in vo)
+          int nfc = 0;
+          const bool fdone = fon && fl0[i] >= 0;
+          if (fdone) {
+            for (int l0 = 0; l0 < fln[i]; l0 += 32) {
+              CChunk r;
+              r.vo = (int32_t)(fl0[i] + l0);
+              r.so = (int32_t)e.sb;
+              r.fo = (int32_t)e.fb;
+              r.cnt = (int32_t)((1u << 30) | (uint32_t)std::min(32, fln[i] - l0));
+              chunk.push_back(r);
+              ++nfc;
+            }
+          }
           if constexpr (CutPCfg<N>::UNIFIED) {
             // one stream: volume, interface, cut-face points (any axis) in chunks of 32
             const int nf = (fon && !fdone) ? e.nf : 0;
@@ -724,9 +785,10 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
               }
             }
           }
-          if (chunk.size() - k0 > 0xffff || nlc > 0xff)
+          if (chunk.size() - k0 > 0xffff || nlc > 0xff || nfc > 0xff)
             return fail(CUTFEM_EUNSUPPORTED, "k_cutp: too many point chunks in a cell");
-          c2o[pos - 1].nchunk = (int32_t)((uint32_t)(chunk.size() - k0) | ((uint32_t)nlc << 16));
+          c2o[pos - 1].nchunk =
+              (int32_t)((uint32_t)(chunk.size() - k0) | ((uint32_t)nlc << 16) | ((uint32_t)nfc << 24));
         }
       }
       ws.push_back((int)(pos - o));
@@ -750,8 +812,12 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
       for (int k = ks[w]; k < ks[w + 1]; ++k) {
         const CChunk &r = chunk[k];
         const bool line = r.cnt < 0, lsrf = line && ((r.cnt >> 29) & 1);
-        const int cv = r.cnt & 0xff, cs = line ? 0 : (r.cnt >> 8) & 0xff, cf = line ? 0 : (r.cnt >> 16) & 0xff;
-        const int bytes = line ? 16 + (16 + 16 * N + (lsrf ? 48 : 0)) * cv : 16 + 32 * cv + 64 * cs + 32 * cf;
+        const bool fline = !line && ((r.cnt >> 30) & 1);
+        const int cv = r.cnt & 0xff, cs = (line || fline) ? 0 : (r.cnt >> 8) & 0xff,
+                  cf = (line || fline) ? 0 : (r.cnt >> 16) & 0xff;
+        const int bytes = line    ? 16 + (16 + 16 * N + (lsrf ? 48 : 0)) * cv
+                          : fline ? 16 + (16 + 16 * N) * cv
+                                  : 16 + 32 * cv + 64 * cs + 32 * cf;
         if (cur.nch > 0 && cur.bytes + bytes > CutPCfg<N>::PK) {
           pk.push_back(cur);
           cur = {(int64_t)strm.size() * 8, 0, 0};
@@ -759,6 +825,13 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         double hdr[2] = {0.0, 0.0};
         std::memcpy(hdr, &r.cnt, sizeof(int32_t));
         strm.insert(strm.end(), hdr, hdr + 2);
+        if (fline) {
+          strm.insert(strm.end(), flrec.begin() + (2 + 2 * N) * (size_t)r.vo,
+                      flrec.begin() + (2 + 2 * N) * ((size_t)r.vo + cv));
+          cur.bytes += bytes;
+          ++cur.nch;
+          continue;
+        }
         if (line) {
           // per line: the two base coordinates (ascending axes), then (coordinate, W) per point
           const int ax = (r.cnt >> 24) & 3, b1 = ax == 0 ? 1 : 0, b2 = ax == 2 ? 1 : 2;

@@ -151,6 +151,9 @@ struct __align__(16) CPacket {
 #ifndef CUTP_RW
 #define CUTP_RW 16  // rows of the reduction transpose buffer
 #endif
+#ifndef CUTP_FLINES
+#define CUTP_FLINES 1  // n = 4: cut-face points in lines (face_line_rt)
+#endif
 
 // values only (cut-face points need no in-face derivatives)
 template <int N>
@@ -226,6 +229,101 @@ __device__ __forceinline__ void face_point_rt(double (&acc)[ACC], const RefTab &
         r = fma(X[a], yz, r);
       }
     }
+}
+
+// Cut-face points in LINES (the 2-D dimension reduction on the face plane, P:45-48:
+// the q = n Gauss points of a line share the normal and one in-face coordinate).
+// Record [xg, f + 8 la, (x_t, W_t) x n]: face f = 2 d + sd, points along axis la, the
+// fixed in-face coordinate xg on the third axis g.  As for a cut-face point, the flux
+// W [(sigma J - s A/(2h)) phi - (s J/(2h)) d_d phi] (eq:unstructured_face P:489-496)
+// needs [u] = J and A = d u_own + d u_nb from the face traces: the fixed-axis sum is
+// done once per line, then n-term sums per point.  Summed over the line's points the
+// update is rank 2 on the axes (d, la, g):
+//   acc += Dv (x) R2 (x) lg  +  e_fo (x) R1 (x) lg,
+//   R2 = sum_t k2_t le(x_t),  R1 = sum_t k1_t le(x_t),  Dv = l'(face),  e_fo = l(face),
+// the axes assigned at run time through a per-lane shared-memory slot (every face of
+// a cell shares one chunk; the slot replaces ~100 selects).
+template <int N, int ACC>
+__device__ __forceinline__ void face_line_rt(double (&acc)[ACC], const RefTab &R, const double *JAB,
+                                             const double *rec, const KParams &kp, double *slot) {
+  constexpr int NN = N * N;
+  const int meta = (int)rec[1], f = meta & 7, la = meta >> 3, d = f >> 1, sd = f & 1;
+  const int g = 3 - d - la;
+  // trace index i + N j: i along the lower in-face axis, j along the upper
+  const bool lo = la < g;
+  const int sl = lo ? 1 : N, sf = lo ? N : 1;  // strides of the line index, the fixed index
+  double lg[N];
+  basis_v_sym<N>(R, rec[0], lg);
+  const double *JA = JAB + f * 2 * NN, *JB = JA + NN;
+  double rJ[N], rA[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double x = 0.0, y = 0.0;
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      x = fma(lg[m], JA[k * sl + m * sf], x);
+      y = fma(lg[m], JB[k * sl + m * sf], y);
+    }
+    rJ[k] = x;
+    rA[k] = y;
+  }
+  const double sgn = sd ? kp.i2h : -kp.i2h;
+  double R1[N], R2[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) R1[k] = R2[k] = 0.0;
+#pragma unroll
+  for (int t = 0; t < N; ++t) {
+    const double2 tw = *reinterpret_cast<const double2 *>(rec + 2 + 2 * t);
+    double le[N];
+    basis_v_sym<N>(R, tw.x, le);
+    double J = 0.0, A = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      J = fma(le[k], rJ[k], J);
+      A = fma(le[k], rA[k], A);
+    }
+    const double k1 = tw.y * fma(kp.sigma, J, -sgn * A), k2 = -tw.y * sgn * J;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      R1[k] = fma(k1, le[k], R1[k]);
+      R2[k] = fma(k2, le[k], R2[k]);
+    }
+  }
+  // slot[a N + m]: the factor on axis a; term 1 (Dv, R2, lg), then term 2 (e_fo, R1, lg)
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    slot[g * N + m] = lg[m];
+    slot[la * N + m] = R2[m];
+    slot[d * N + m] = sd ? R.d1[m] : R.d0[m];
+  }
+#pragma unroll
+  for (int term = 0; term < 2; ++term) {
+    if (term == 1) {
+#pragma unroll
+      for (int m = 0; m < N; ++m) {
+        slot[la * N + m] = R1[m];
+        slot[d * N + m] = m == (sd ? N - 1 : 0) ? 1.0 : 0.0;
+      }
+    }
+    double X[N], Y[N], Z[N];
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      X[m] = slot[m];
+      Y[m] = slot[N + m];
+      Z[m] = slot[2 * N + m];
+    }
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        const double yz = Y[b] * Z[c];
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          double &r = acc[(c * N + b) * N + a];
+          r = fma(X[a], yz, r);
+        }
+      }
+  }
 }
 
 // Volume points that come in LINES (dimension-reduction quadrature: along
@@ -356,6 +454,10 @@ struct CutPCfg {
   static constexpr bool BFLY = ACC <= CUTP_BFLY_MAXACC;
   // 64 accumulators: one butterfly level (xor 16) + a 16-lane shared-memory transpose
   static constexpr bool HYB = !BFLY && ACC == 64 && CUTP_HYB;
+  // cut-face points in lines (face_line_rt; its per-lane axis slots live in the
+  // reduction buffer, which is free until the cell's reduction)
+  static constexpr bool FLINES = N == 4 && HYB && CUTP_FLINES;
+  static_assert(!FLINES || 32 * (3 * N + 1) <= 32 * 17, "face-line slots exceed the reduction buffer");
   // bars(2 + NB) | UB[2][7][N3P] | JAB[6][2][NN] | ring[NB][2 + PK/8] (nch + packet)
   static constexpr int OFF_UB = (2 + NB + 1) & ~1;
   static constexpr int OFF_JAB = OFF_UB + 2 * 7 * N3P;
@@ -488,6 +590,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     // chunks of the cell: the first KL are volume lines
     // (lines never occur at n = 2: the host plans none, and the loop is compiled out)
     const int K = (int)((uint32_t)cd.nchunk & 0xffffu), KL = N >= 3 ? (int)(((uint32_t)cd.nchunk >> 16) & 0xffu) : 0;
+    const int KF = C::FLINES ? (int)(((uint32_t)cd.nchunk >> 24) & 0xffu) : 0;  // cut-face line chunks
     const uint32_t fm = fmask_of(cd);
     // ---- this cell's blocks
     if constexpr (C::BULK) {
@@ -669,7 +772,18 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
       __syncwarp();
       if (lane == 0 && left == 0) fence_proxy_async();
     }
-    for (int k = KL; k < K; ++k) {
+    // cut-face LINES (n = 4): chunks of <= 32 line records of any face, 2 + 2N doubles each
+    for (int k = KL; k < (C::FLINES ? KL + KF : KL); ++k) {
+      if (left == 0) next_packet();
+      const int cl = reinterpret_cast<const int *>(S + pos)[0] & 0xff;
+      const double *P = S + pos + 2;
+      --left;
+      pos += 2 + (2 + 2 * N) * cl;
+      if (lane < cl) face_line_rt<N>(acc, R, JAB, P + (2 + 2 * N) * lane, kp, base + C::OFF_RED + lane * (3 * N + 1));
+      __syncwarp();
+      if (lane == 0 && left == 0) fence_proxy_async();
+    }
+    for (int k = KL + KF; k < K; ++k) {
       if (left == 0) next_packet();
       const int cnt = reinterpret_cast<const int *>(S + pos)[0];
       const int cv = cnt & 0xff, cs = (cnt >> 8) & 0xff, cf = (cnt >> 16) & 0xff;
