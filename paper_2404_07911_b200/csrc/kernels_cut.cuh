@@ -27,6 +27,11 @@
 #ifndef CUTP_MINB
 #define CUTP_MINB 1
 #endif
+#ifdef CUTP_MAXNREG  // register cap (experiments: more warps per SM)
+#define CUTP_BOUNDS __maxnreg__(CUTP_MAXNREG)
+#else
+#define CUTP_BOUNDS __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB)
+#endif
 #ifndef CUTP_WARPS
 #define CUTP_WARPS 1  // warps (cut cells in flight) per CTA: 1 lets other kernels share SMs
 #endif
@@ -343,35 +348,54 @@ __device__ __forceinline__ constexpr int lpos(int i, int j, int k) {
   // i along AX, j along B1 < B2, k along B2 -> l = x + N y + N^2 z
   return AX == 0 ? (i + N * j + N * N * k) : (AX == 1 ? (j + N * i + N * N * k) : (j + N * k + N * N * i));
 }
-template <int N, int AX, bool SRF, int ACC>
-__device__ __forceinline__ void vol_line(double (&acc)[ACC], const RefTab &R, const double *U, const double *rec,
-                                         const KParams &kp) {
+// P_i, Q1_i, Q2_i of one volume line and its test coefficients R0, R1, R2 (every
+// point of the line, and the line's interface point when srf and its W != 0).  U is
+// the cell block in the LINE frame (i along the line, j, k along the base axes
+// B1 < B2: UL[i + N j + N^2 k]), so one instance serves the three line axes and
+// only the accumulation (vol_line_int) depends on the axis (smaller hot code).
+template <int N>
+__device__ __forceinline__ void vol_line_eval(const RefTab &R, const double *U, const double *rec, const KParams &kp,
+                                              bool srf, double (&v1)[N], double (&d1)[N], double (&v2)[N],
+                                              double (&d2)[N], double (&R0)[N], double (&R1)[N], double (&R2)[N]) {
   const double ih2 = kp.ih2;
-  double v1[N], d1[N], v2[N], d2[N];
   basis_vd_sym<N>(R, rec[0], v1, d1);
   basis_vd_sym<N>(R, rec[1], v2, d2);
   double Pp[N], Q1[N], Q2[N];
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    double p = 0.0, q1 = 0.0, q2 = 0.0;
+  for (int i = 0; i < N; ++i) Pp[i] = Q1[i] = Q2[i] = 0.0;
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double s0 = 0.0, s1 = 0.0;
+  for (int k = 0; k < N; ++k) {
+    double s0[N], s1[N];
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        const double uu = U[lpos<N, AX>(i, j, k)];
-        s0 = fma(v1[j], uu, s0);
-        s1 = fma(d1[j], uu, s1);
+    for (int i = 0; i < N; ++i) s0[i] = s1[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double row[N];
+      const double *rp = U + N * j + N * N * k;
+      if constexpr ((N % 2) == 0) {
+#pragma unroll
+        for (int i = 0; i < N; i += 2) {
+          const double2 x = *reinterpret_cast<const double2 *>(rp + i);
+          row[i] = x.x;
+          row[i + 1] = x.y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) row[i] = rp[i];
       }
-      p = fma(v2[k], s0, p);
-      q1 = fma(v2[k], s1, q1);
-      q2 = fma(d2[k], s0, q2);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        s0[i] = fma(v1[j], row[i], s0[i]);
+        s1[i] = fma(d1[j], row[i], s1[i]);
+      }
     }
-    Pp[i] = p;
-    Q1[i] = q1;
-    Q2[i] = q2;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      Pp[i] = fma(v2[k], s0[i], Pp[i]);
+      Q1[i] = fma(v2[k], s1[i], Q1[i]);
+      Q2[i] = fma(d2[k], s0[i], Q2[i]);
+    }
   }
-  double R0[N], R1[N], R2[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) R0[i] = R1[i] = R2[i] = 0.0;
 #pragma unroll
@@ -395,7 +419,7 @@ __device__ __forceinline__ void vol_line(double (&acc)[ACC], const RefTab &R, co
       R2[i] = fma(cB2, va[i], R2[i]);
     }
   }
-  if constexpr (SRF) {
+  if (srf) {
     // the line's interface (Nitsche) point, if any (W = 0 otherwise): rec[2 + 2N ..] =
     // t, W, n_ax, n_B1, n_B2 (the unit normal in the line's axes); value term folded into R0
     const double2 tw = *reinterpret_cast<const double2 *>(rec + 2 + 2 * N);
@@ -423,6 +447,13 @@ __device__ __forceinline__ void vol_line(double (&acc)[ACC], const RefTab &R, co
       }
     }
   }
+}
+
+// acc(i,j,k) += R0_i l1_j l2_k + R1_i l1'_j l2_k + R2_i l1_j l2'_k in the cell frame
+template <int N, int AX, int ACC>
+__device__ __forceinline__ void vol_line_int(double (&acc)[ACC], const double (&v1)[N], const double (&d1)[N],
+                                             const double (&v2)[N], const double (&d2)[N], const double (&R0)[N],
+                                             const double (&R1)[N], const double (&R2)[N]) {
 #pragma unroll
   for (int i = 0; i < N; ++i)
 #pragma unroll
@@ -469,13 +500,19 @@ struct CutPCfg {
   // the warp's next <= DG cell descriptors, staged by one coalesced load per group
   // (8: 640 B, what is left of the SM's shared memory at 8 warps per SM)
   static constexpr int DG = 8;
-  static constexpr int OFF_DSC = OFF_RED + (BFLY ? 0 : (HYB ? 32 * 17 : RW * 33));
-  static constexpr int WSLOT = OFF_DSC + DG * (int)(sizeof(CDesc2) / 8);
+  static constexpr int RED_SZ = BFLY ? 0 : (HYB ? 32 * 17 : RW * 33);
+  static constexpr int OFF_DSC = OFF_RED + RED_SZ;
+  // the cell block in the line frame (vol_line_eval): inside the reduction buffer after
+  // the face-line slots when it fits (both are free until the reduction), else its own
+  static constexpr int SLOTS = FLINES ? 32 * (3 * N + 1) : 0;
+  static constexpr bool UL_IN_RED = SLOTS + N3P <= RED_SZ;
+  static constexpr int OFF_UL = UL_IN_RED ? OFF_RED + SLOTS : OFF_DSC + DG * (int)(sizeof(CDesc2) / 8);
+  static constexpr int WSLOT = OFF_DSC + DG * (int)(sizeof(CDesc2) / 8) + (UL_IN_RED ? 0 : N3P);
   static constexpr int SMEM = WARPS * WSLOT * 8;
 };
 
 template <int N>
-__global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const double *__restrict__ u, double *__restrict__ v,
+__global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restrict__ v,
                                               const CDesc2 *__restrict__ desc, const CPacket *__restrict__ packets,
                                               const char *__restrict__ stream, const int *__restrict__ wstart,
                                               const int *__restrict__ pstart, KParams kp, TileTab<N> tt) {
@@ -748,6 +785,7 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
     };
     // volume LINES first (their own loop: the point loop below keeps its code
     // generation): chunks of cv lines along axis (cnt >> 24) & 3, records of 2 + 2N doubles
+    const double *UL = U;  // the block in the line frame (a copy when the lines are not along x)
     for (int k = 0; k < (N >= 3 ? KL : 0); ++k) {
       if (left == 0) next_packet();
       const int cnt = reinterpret_cast<const int *>(S + pos)[0];
@@ -757,17 +795,23 @@ __global__ void __launch_bounds__(32 * CUTP_WARPS, CUTP_MINB) k_cutp(const doubl
       const double *P = S + pos + 2;
       --left;
       pos += 2 + rs * cv;
+      if (k == 0 && ax != 0) {
+        // UL[i + N j + N^2 k] = U[lpos<AX>(i, j, k)] (every line of a cell has one axis)
+        double *Ut = base + C::OFF_UL;
+        for (int l = lane; l < N3; l += 32) {
+          const int i = l % N, j = (l / N) % N, kk = l / NN;
+          Ut[l] = U[ax == 1 ? (j + N * i + NN * kk) : (j + N * kk + NN * i)];
+        }
+        __syncwarp();
+        UL = Ut;
+      }
       if (lane < cv) {
         const double *rec = P + rs * lane;
-        if (srf) {
-          if (ax == 0) vol_line<N, 0, true>(acc, R, U, rec, kp);
-          else if (ax == 1) vol_line<N, 1, true>(acc, R, U, rec, kp);
-          else vol_line<N, 2, true>(acc, R, U, rec, kp);
-        } else {
-          if (ax == 0) vol_line<N, 0, false>(acc, R, U, rec, kp);
-          else if (ax == 1) vol_line<N, 1, false>(acc, R, U, rec, kp);
-          else vol_line<N, 2, false>(acc, R, U, rec, kp);
-        }
+        double v1[N], d1[N], v2[N], d2[N], R0[N], R1[N], R2[N];
+        vol_line_eval<N>(R, UL, rec, kp, srf, v1, d1, v2, d2, R0, R1, R2);
+        if (ax == 0) vol_line_int<N, 0>(acc, v1, d1, v2, d2, R0, R1, R2);
+        else if (ax == 1) vol_line_int<N, 1>(acc, v1, d1, v2, d2, R0, R1, R2);
+        else vol_line_int<N, 2>(acc, v1, d1, v2, d2, R0, R1, R2);
       }
       __syncwarp();
       if (lane == 0 && left == 0) fence_proxy_async();
