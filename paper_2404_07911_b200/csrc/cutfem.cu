@@ -104,7 +104,8 @@ struct cutfem_handle {
   CDesc *d_cdesc = nullptr;
   double *d_vol = nullptr, *d_srf = nullptr, *d_sfp = nullptr;
   int64_t *d_volptr = nullptr, *d_srfptr = nullptr, *d_sfptr = nullptr;
-  int32_t *d_line_srf = nullptr;  // k_cut line cells: interface point on each line (-1 none)
+  double *d_line_srf = nullptr;  // k_cut line cells: per volume line its interface point [t, W, n_ax, n_B1, n_B2, 0]
+                                 // (W = 0: none), staged with the line's points
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_started = nullptr;  // k_cutp launch completion (all CTAs begun)
@@ -1367,7 +1368,7 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   // descriptors
   std::vector<UDesc> ud;
   std::vector<CDesc> cd;
-  std::vector<int32_t> line_srf;  // k_cut: interface point per volume line of the line cells
+  std::vector<double> line_srf;  // k_cut: interface record per volume line of the line cells (6 doubles)
   std::vector<int64_t> ccost;
   if (n_compute < 0) n_compute = na;
   hd->n_own = n_compute;
@@ -1432,10 +1433,19 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
           const std::vector<int> li = srf_on_lines(pb->vol_pts + 4 * c.vb, c.nv, pb->srf_pts + 7 * c.sb, c.ns, n, lax);
           if (!li.empty()) {
             c.flags |= 1u << 27;
-            c.pad = (int32_t)line_srf.size();
-            const size_t l0 = line_srf.size();
-            line_srf.resize(l0 + c.nv / n, -1);
-            for (size_t q = 0; q < li.size(); ++q) line_srf[l0 + li[q]] = (int32_t)(c.sb + (int64_t)q);
+            c.pad = (int32_t)(line_srf.size() / 6);
+            const size_t l0 = line_srf.size() / 6;
+            line_srf.resize(6 * (l0 + c.nv / n), 0.0);
+            const int b1 = lax == 0 ? 1 : 0, b2 = lax == 2 ? 1 : 2;
+            for (size_t q = 0; q < li.size(); ++q) {
+              const double *y = pb->srf_pts + 7 * (c.sb + (int64_t)q);  // xi eta zeta nx ny nz W
+              double *r = &line_srf[6 * (l0 + li[q])];
+              r[0] = y[lax];
+              r[1] = y[6];
+              r[2] = y[3 + lax];
+              r[3] = y[3 + b1];
+              r[4] = y[3 + b2];
+            }
           }
         }
       }

@@ -609,8 +609,9 @@ struct CutCfg {
   static constexpr int LRL0 = 3 * NN + 3 * N, LRL = (LRL0 % 2 == 0) ? LRL0 + 1 : LRL0;
   static constexpr int LCL0 = (CHUNK * ROW) / LRL, LCL = LCL0 < THREADS / 2 ? LCL0 : THREADS / 2;
   static constexpr int LBUF = ROWINT ? LCL * N * 4 : 0;
+  static constexpr int LSBUF = ROWINT ? LCL * 6 : 0;  // the lines' interface records
   static constexpr int OFF_LB = OFF_PB + PBUF;  // even: 16-byte aligned
-  static constexpr int SMEM_D = OFF_LB + LBUF;
+  static constexpr int SMEM_D = OFF_LB + LBUF + LSBUF;
   static constexpr int SMEM = SMEM_D * 8;
 };
 
@@ -931,13 +932,13 @@ __device__ __forceinline__ void line_base(const double *U, int i0, const double 
 template <int N>
 __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int64_t pb, int64_t pe, int ax,
                                             const double *U, double *PS, double (&acc)[CutCfg<N>::RPT][N],
-                                            const KParams &kp, const RefTab &R, const int *__restrict__ lsrf,
-                                            const double *__restrict__ srf_pts) {
+                                            const KParams &kp, const RefTab &R, const double *__restrict__ lsrf) {
   using C = CutCfg<N>;
   constexpr int NN = C::NN, RPT = C::RPT, TG = C::TG, G = C::G;
   constexpr int RL = C::LRL, CL = C::LCL;  // row: S0 S1 S2 X0 X1 X2; lines per chunk
   constexpr int H = (N + 1) / 2;  // i values per thread
   double *LB = PS - C::OFF_PS + C::OFF_LB;  // the chunk's line points (CL N rows of 4 doubles)
+  double *LS = LB + C::LBUF;                 // the chunk's line interface records (CL rows of 6)
   const int tid = threadIdx.x, grp = tid / TG, rl = tid % TG;
   const int lq = tid >> 1, part = tid & 1, i0 = part * H;
   const double ih = 1.0 / kp.h, ih2 = ih * ih;
@@ -947,6 +948,8 @@ __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int6
     {  // stage the chunk's points (16-byte pieces; the previous chunk is done with LB)
       const double *src = pts + 4 * (pb + l0 * N);
       for (int e = tid; e < cnt * N * 2; e += C::THREADS) cp_async16(LB + 2 * e, src + 2 * e);
+      if (lsrf)  // the lines' interface records [t, W, n_ax, n_B1, n_B2, 0] (LS: CL rows of 6)
+        for (int e = tid; e < cnt * 3; e += C::THREADS) cp_async16(LS + 2 * e, lsrf + 6 * l0 + 2 * e);
       cp_async_commit();
       cp_async_wait<0>();
       __syncthreads();
@@ -1007,10 +1010,9 @@ __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int6
       if (lsrf) {
         // the line's interface (Nitsche) point, if any; every pair runs this (W = 0 when
         // absent) so the shuffles stay convergent; value term folded into R0
-        const int q = live ? lsrf[l0 + lq] : -1;
-        const double *y = srf_pts + 8 * (int64_t)(q >= 0 ? q : 0);
-        const double tc = y[ax], W = q >= 0 ? y[6] : 0.0;
-        const double nA = y[3 + ax], nB1 = y[3 + (ax == 0 ? 1 : 0)], nB2 = y[3 + (ax == 2 ? 1 : 2)];
+        const double *y = LS + 6 * (live ? lq : 0);
+        const double tc = y[0], W = live ? y[1] : 0.0;
+        const double nA = y[2], nB1 = y[3], nB2 = y[4];
         double va[N], da[N];
         basis_vd<N>(R, tc, va, da);
         double vh[H], dh[H];
@@ -1144,7 +1146,7 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
                                              const int64_t *__restrict__ srf_ptr,
                                              const double *__restrict__ sf_pts,
                                              const int64_t *__restrict__ sf_ptr, KParams kp, FaceTab ft,
-                                             TileTab<N> tt, const int *__restrict__ line_srf) {
+                                             TileTab<N> tt, const double *__restrict__ line_srf) {
   using B = Blk<N>;
   using C = CutCfg<N>;
   constexpr int NN = B::NN, N3 = B::N3, SZ = B::SZ, TH = C::THREADS;
@@ -1186,8 +1188,7 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
     if constexpr (C::ROWINT) {
       if ((dsc.flags >> 26) & 1u)  // volume points in lines along axis (flags >> 24) & 3
         line_chunks<N>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], (int)((dsc.flags >> 24) & 3u), U, PS, acc,
-                       kp, R, ((dsc.flags >> 27) & 1u) && (kp.mask & TERM_NITSCHE) ? line_srf + dsc.pad : nullptr,
-                       srf_pts);
+                       kp, R, ((dsc.flags >> 27) & 1u) && (kp.mask & TERM_NITSCHE) ? line_srf + 6 * (int64_t)dsc.pad : nullptr);
       else
         point_chunks<N, false>(vol_pts, vol_ptr[dsc.cut], vol_ptr[dsc.cut + 1], U, PS, acc, kp, R);
     } else {
@@ -1390,6 +1391,8 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
       const int64_t pb = sf_ptr[dsc.sf[f]], pe = sf_ptr[dsc.sf[f] + 1];
       constexpr int FR = C::FROW;
       constexpr int FCH = (C::CHUNK * C::ROW) / FR < TH ? (C::CHUNK * C::ROW) / FR : TH;
+      constexpr int FG = TH / NN >= 1 ? TH / NN : 1;  // thread groups over the points
+      static_assert(2 * FG * NN <= C::CHUNK * C::ROW, "partial sums fit the point rows");
       double f1 = 0.0, f2 = 0.0;
       for (int64_t c0 = pb; c0 < pe; c0 += FCH) {
         if (tid < FCH) {
@@ -1426,9 +1429,10 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
         }
         __syncthreads();
         const int cnt = (int)((pe - c0) < FCH ? (pe - c0) : FCH);
-        if (tid < NN) {
-          const int i = tid % N, j = tid / N;
-          for (int qq = 0; qq < cnt; ++qq) {
+        // FG groups of NN threads split the chunk's points (in-face node (i, j) per thread)
+        if (tid < FG * NN) {
+          const int fg = tid / NN, i = (tid % NN) % N, j = (tid % NN) / N;
+          for (int qq = fg; qq < cnt; qq += FG) {
             const double *row = PS + qq * FR;
             const double psi = row[i] * row[N + j];
             f1 = fma(psi, row[2 * N], f1);
@@ -1436,6 +1440,21 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
           }
         }
         __syncthreads();
+      }
+      if constexpr (FG > 1) {  // the groups' partial sums, added in group order
+        if (tid < FG * NN) {
+          PS[2 * tid] = f1;
+          PS[2 * tid + 1] = f2;
+        }
+        __syncthreads();
+        if (tid < NN) {
+#pragma unroll
+          for (int g = 1; g < FG; ++g) {
+            f1 += PS[2 * (g * NN + tid)];
+            f2 += PS[2 * (g * NN + tid) + 1];
+          }
+        }
+        __syncthreads();  // PS is the next face's point rows
       }
       if constexpr (C::WFACE) {
         // thread t accumulated line t's coefficients itself (NN <= THREADS): apply them
