@@ -313,6 +313,45 @@ __device__ __forceinline__ void basis_vd(const RefTab &R, double t, double (&v)[
   }
 }
 
+// The thread's half of a line's basis for the line_chunks thread pairs: entries
+// i0 + ii (ii < H, i0 = part H) of l_a(x), l_a'(x).  Even n: the GLL nodes are
+// symmetric, l_{n-1-a}(x) = l_a(1 - x), so the upper half is the lower half at 1 - x
+// in reverse order with the derivative's sign flipped: H functions and H selects
+// instead of n functions and H n selects.
+template <int N, int H>
+__device__ __forceinline__ void basis_vd_half(const RefTab &R, double x, int part, double (&vh)[H], double (&dh)[H]) {
+  static_assert(N % 2 == 0 && 2 * H == N, "even n only");
+  const double t = part ? 1.0 - x : x;
+  double d[N], pre[H], dpre[H], lv[H], ld[H];
+#pragma unroll
+  for (int m = 0; m < N; ++m) d[m] = t - R.x[m];
+  double p = 1.0, dp = 0.0;
+#pragma unroll
+  for (int a = 0; a < H; ++a) {
+    pre[a] = p;
+    dpre[a] = dp;
+    dp = fma(dp, d[a], p);
+    p *= d[a];
+  }
+  double s = 1.0, ds = 0.0;
+#pragma unroll
+  for (int a = N - 1; a >= 0; --a) {
+    if (a < H) {
+      lv[a] = R.cinv[a] * pre[a] * s;
+      ld[a] = R.cinv[a] * fma(dpre[a], s, pre[a] * ds);
+    }
+    if (a > 0) {
+      ds = fma(ds, d[a], s);
+      s *= d[a];
+    }
+  }
+#pragma unroll
+  for (int ii = 0; ii < H; ++ii) {
+    vh[ii] = part ? lv[H - 1 - ii] : lv[ii];
+    dh[ii] = part ? -ld[H - 1 - ii] : ld[ii];
+  }
+}
+
 template <int N>
 __device__ __forceinline__ void basis_v(const RefTab &R, double t, double (&v)[N]) {
   double d[N], pre[N];
@@ -453,7 +492,7 @@ __global__ void __launch_bounds__(128) k_uncut(const double *__restrict__ u, dou
         double A = 0.0;
 #pragma unroll
         for (int m = 0; m < N; ++m) A = fma(dow[m], uo[m], fma(dnb[m], un[m], A));
-        const double F1 = sipg ? h2 * (kp.sigma * J0 - sg * A / (2.0 * h)) : 0.0;
+        const double F1 = sipg ? h2 * (kp.sigma * J0 - sg * A * kp.i2h) : 0.0;
         const double F2 = sipg ? -0.5 * h * sg * J0 : 0.0;
         if (gp) {
 #pragma unroll
@@ -688,7 +727,7 @@ __device__ __forceinline__ void point_chunks(const double *__restrict__ pts, int
   const int grp = tid / TG, rl = tid % TG;
   constexpr int SPL = C::SPL, CPS = C::CPS;
   const int pq = tid / SPL, part = tid % SPL;  // point of the chunk, z-plane share
-  const double h = kp.h, ih = 1.0 / h, ih2 = ih * ih;
+  const double ih = kp.ih, ih2 = kp.ih2;  // (no divisions in the kernels)
   constexpr int RL = SURF ? 8 : 4;  // doubles per point row
   double *PB = PS - C::OFF_PS + C::OFF_PB;  // [2][CHUNK * 8] prefetch buffers (16-byte aligned)
   // rows [c, min(c + CHUNK, pe)) into buffer b: 16-byte pieces over the CTA
@@ -941,7 +980,7 @@ __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int6
   double *LS = LB + C::LBUF;                 // the chunk's line interface records (CL rows of 6)
   const int tid = threadIdx.x, grp = tid / TG, rl = tid % TG;
   const int lq = tid >> 1, part = tid & 1, i0 = part * H;
-  const double ih = 1.0 / kp.h, ih2 = ih * ih;
+  const double ih = kp.ih, ih2 = kp.ih2;
   const int64_t nl = (pe - pb) / N;
   for (int64_t l0 = 0; l0 < nl; l0 += CL) {
     const int cnt = (int)((nl - l0) < CL ? (nl - l0) : CL);
@@ -973,20 +1012,24 @@ __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int6
 #pragma unroll 1
       for (int t = 0; t < N; ++t) {
         const double tc = p[4 * t + ax], W = live ? p[4 * t + 3] : 0.0;
-        double va[N], da[N];
-        basis_vd<N>(R, tc, va, da);
         double vh[H], dh[H];  // this thread's half (i0 + ii), dummy slot zero
+        if constexpr (N % 2 == 0) {
+          basis_vd_half<N, H>(R, tc, part, vh, dh);
+        } else {
+          double va[N], da[N];
+          basis_vd<N>(R, tc, va, da);
 #pragma unroll
-        for (int ii = 0; ii < H; ++ii) {
-          double x = 0.0, y = 0.0;
+          for (int ii = 0; ii < H; ++ii) {
+            double x = 0.0, y = 0.0;
 #pragma unroll
-          for (int m = 0; m < N; ++m)
-            if (m == i0 + ii) {
-              x = va[m];
-              y = da[m];
-            }
-          vh[ii] = x;
-          dh[ii] = y;
+            for (int m = 0; m < N; ++m)
+              if (m == i0 + ii) {
+                x = va[m];
+                y = da[m];
+              }
+            vh[ii] = x;
+            dh[ii] = y;
+          }
         }
         double uA = 0.0, uB1 = 0.0, uB2 = 0.0;
 #pragma unroll
@@ -1013,20 +1056,24 @@ __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int6
         const double *y = LS + 6 * (live ? lq : 0);
         const double tc = y[0], W = live ? y[1] : 0.0;
         const double nA = y[2], nB1 = y[3], nB2 = y[4];
-        double va[N], da[N];
-        basis_vd<N>(R, tc, va, da);
         double vh[H], dh[H];
+        if constexpr (N % 2 == 0) {
+          basis_vd_half<N, H>(R, tc, part, vh, dh);
+        } else {
+          double va[N], da[N];
+          basis_vd<N>(R, tc, va, da);
 #pragma unroll
-        for (int ii = 0; ii < H; ++ii) {
-          double x = 0.0, z = 0.0;
+          for (int ii = 0; ii < H; ++ii) {
+            double x = 0.0, z = 0.0;
 #pragma unroll
-          for (int m = 0; m < N; ++m)
-            if (m == i0 + ii) {
-              x = va[m];
-              z = da[m];
-            }
-          vh[ii] = x;
-          dh[ii] = z;
+            for (int m = 0; m < N; ++m)
+              if (m == i0 + ii) {
+                x = va[m];
+                z = da[m];
+              }
+            vh[ii] = x;
+            dh[ii] = z;
+          }
         }
         double u0 = 0.0, uA = 0.0, uB1 = 0.0, uB2 = 0.0;
 #pragma unroll
@@ -1355,7 +1402,7 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
       FC1[t] = 0.0;
       FC2[t] = 0.0;
       if (structured) {
-        const double F1 = ss ? h2 * (kp.sigma * J0 - sg * A / (2.0 * h)) : 0.0;
+        const double F1 = ss ? h2 * (kp.sigma * J0 - sg * A * kp.i2h) : 0.0;
         const double F2 = ss ? -0.5 * h * sg * J0 : 0.0;
 #pragma unroll
         for (int m = 0; m < N; ++m) {
@@ -1424,8 +1471,8 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
             row[i] = ls[i];
             row[N + i] = lt[i];
           }
-          row[2 * N] = W * (kp.sigma * J0 - sg * A / (2.0 * h));
-          row[2 * N + 1] = -W * sg * J0 / (2.0 * h);
+          row[2 * N] = W * (kp.sigma * J0 - sg * A * kp.i2h);
+          row[2 * N + 1] = -W * sg * J0 * kp.i2h;
         }
         __syncthreads();
         const int cnt = (int)((pe - c0) < FCH ? (pe - c0) : FCH);
