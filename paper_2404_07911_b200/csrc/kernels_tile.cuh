@@ -771,7 +771,7 @@ __global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, doubl
       }
       __syncwarp();
     });
-    __syncthreads();  // all w final; all slot reads done (the next tile's copies may start)
+    __syncthreads();  // all w final
     // ---- v += w (the warp's 8 cells; v rows were loaded at the start of the tile)
 #pragma unroll
     for (int c = 0; c < CPW; ++c) {
@@ -828,28 +828,34 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
   }
   __syncthreads();
   uint32_t it = 0;
+  // bulk path: software pipeline -- the next tile's blocks are copied while this tile's
+  // mass sweeps and write-back run (the slots are free once the axis terms are done)
+  auto issue = [&](int tl) {
+    const TileRec<TC_::SMAX> *Tn = tiles + tl;
+    const int ns = Tn->nslot;
+    fence_proxy_async();  // this thread's generic reads of the slots precede the bulk writes
+    __syncthreads();
+    if (tid == 0) mbar_expect_tx(bar, (uint32_t)(ns * N3 * 8));
+    __syncthreads();
+    for (int sl = tid; sl < ns; sl += C::THREADS) bulk_g2s(S + sl * ST, u + (size_t)Tn->blk[sl] * N3, N3 * 8, bar);
+  };
+  if constexpr (TC_::BULK) {
+    if ((int)blockIdx.x < ntiles) issue(blockIdx.x);
+  }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const TileRec<TC_::SMAX> *T = tiles + tile;
     const int nslot = T->nslot, ncell = T->ncell;
     const bool on = cell < ncell;
     const uint2 ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[on ? cell : 0][0]);
-    // ---- stage the tile's blocks
-    if constexpr (TC_::BULK) {
-      fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) mbar_expect_tx(bar, (uint32_t)(nslot * N3 * 8));
-      __syncthreads();
-      for (int sl = tid; sl < nslot; sl += C::THREADS) bulk_g2s(S + sl * ST, u + (size_t)T->blk[sl] * N3, N3 * 8, bar);
-    } else {
+    // ---- the tile's blocks (bulk: issued during the previous tile)
+    if constexpr (!TC_::BULK) {
       __syncthreads();
       for (int sl = 0; sl < nslot; ++sl) {
         const double *src = u + (size_t)T->blk[sl] * N3;
         for (int l = tid; l < N3; l += C::THREADS) S[sl * ST + l] = __ldg(src + l);
       }
     }
-    double *W = Wb + (on ? cell : 0) * WST;
-    if (on)
-      for (int l = r; l < N3; l += TPC) W[l] = 0.0;
+    double *W = Wb + (on ? cell : 0) * WST;  // (axis 0 stores, the other axes accumulate)
     if constexpr (TC_::BULK) mbar_wait(bar, it & 1);
     __syncthreads();
     int nbs[6];
@@ -935,11 +941,17 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
             }
           });
 #pragma unroll
-          for (int m = 0; m < N; ++m) W[b0 + m * str] += out[m];
+          for (int m = 0; m < N; ++m) {
+            if (D == 0) W[b0 + m * str] = out[m];  // axis 0's lines cover every position once
+            else W[b0 + m * str] += out[m];
+          }
         }
       }
       __syncwarp();  // the next axis updates other threads' positions
     });
+    if constexpr (TC_::BULK) {
+      if (tile + (int)gridDim.x < ntiles) issue(tile + (int)gridDim.x);
+    }
     // ---- v = (M (x) M (x) M) w, sweeps in shared memory
     static_for<0, 3>([&](auto dc) {
       constexpr int D = decltype(dc)::value;
@@ -969,7 +981,7 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
       }
       __syncwarp();
     });
-    __syncthreads();  // all w final; all slot reads done (the next tile's copies may start)
+    __syncthreads();  // all w final
     for (int e = tid; e < ncell * N3; e += C::THREADS) {
       const int c = e / N3, l = e - c * N3;
       v[(size_t)T->blk[c] * N3 + l] = Wb[c * WST + l];
