@@ -314,13 +314,15 @@ __device__ __forceinline__ void basis_vd(const RefTab &R, double t, double (&v)[
 }
 
 // The thread's half of a line's basis for the line_chunks thread pairs: entries
-// i0 + ii (ii < H, i0 = part H) of l_a(x), l_a'(x).  Even n: the GLL nodes are
-// symmetric, l_{n-1-a}(x) = l_a(1 - x), so the upper half is the lower half at 1 - x
-// in reverse order with the derivative's sign flipped: H functions and H selects
-// instead of n functions and H n selects.
+// i0 + ii (ii < H = ceil(n/2), i0 = part H; an index >= n is a zero dummy) of l_a(x),
+// l_a'(x).  The GLL nodes are symmetric, l_{n-1-a}(x) = l_a(1 - x), so the upper half
+// is the lower half at 1 - x in reverse order with the derivative's sign flipped
+// (odd n: shifted by one, the middle function belongs to the lower half): H
+// functions and H selects instead of n functions and H n selects.
 template <int N, int H>
 __device__ __forceinline__ void basis_vd_half(const RefTab &R, double x, int part, double (&vh)[H], double (&dh)[H]) {
-  static_assert(N % 2 == 0 && 2 * H == N, "even n only");
+  static_assert(H == (N + 1) / 2, "H = ceil(n / 2)");
+  constexpr int SH = N % 2;  // odd n: part 1's entry ii is l_{H-2-ii}(1 - x), the last a dummy
   const double t = part ? 1.0 - x : x;
   double d[N], pre[H], dpre[H], lv[H], ld[H];
 #pragma unroll
@@ -347,8 +349,9 @@ __device__ __forceinline__ void basis_vd_half(const RefTab &R, double x, int par
   }
 #pragma unroll
   for (int ii = 0; ii < H; ++ii) {
-    vh[ii] = part ? lv[H - 1 - ii] : lv[ii];
-    dh[ii] = part ? -ld[H - 1 - ii] : ld[ii];
+    const int m = H - 1 - SH - ii;  // mirrored index (< 0: the odd-n dummy)
+    vh[ii] = part ? (m >= 0 ? lv[m >= 0 ? m : 0] : 0.0) : lv[ii];
+    dh[ii] = part ? (m >= 0 ? -ld[m >= 0 ? m : 0] : 0.0) : ld[ii];
   }
 }
 
@@ -1013,24 +1016,7 @@ __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int6
       for (int t = 0; t < N; ++t) {
         const double tc = p[4 * t + ax], W = live ? p[4 * t + 3] : 0.0;
         double vh[H], dh[H];  // this thread's half (i0 + ii), dummy slot zero
-        if constexpr (N % 2 == 0) {
-          basis_vd_half<N, H>(R, tc, part, vh, dh);
-        } else {
-          double va[N], da[N];
-          basis_vd<N>(R, tc, va, da);
-#pragma unroll
-          for (int ii = 0; ii < H; ++ii) {
-            double x = 0.0, y = 0.0;
-#pragma unroll
-            for (int m = 0; m < N; ++m)
-              if (m == i0 + ii) {
-                x = va[m];
-                y = da[m];
-              }
-            vh[ii] = x;
-            dh[ii] = y;
-          }
-        }
+        basis_vd_half<N, H>(R, tc, part, vh, dh);
         double uA = 0.0, uB1 = 0.0, uB2 = 0.0;
 #pragma unroll
         for (int ii = 0; ii < H; ++ii) {
@@ -1057,24 +1043,7 @@ __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int6
         const double tc = y[0], W = live ? y[1] : 0.0;
         const double nA = y[2], nB1 = y[3], nB2 = y[4];
         double vh[H], dh[H];
-        if constexpr (N % 2 == 0) {
-          basis_vd_half<N, H>(R, tc, part, vh, dh);
-        } else {
-          double va[N], da[N];
-          basis_vd<N>(R, tc, va, da);
-#pragma unroll
-          for (int ii = 0; ii < H; ++ii) {
-            double x = 0.0, z = 0.0;
-#pragma unroll
-            for (int m = 0; m < N; ++m)
-              if (m == i0 + ii) {
-                x = va[m];
-                z = da[m];
-              }
-            vh[ii] = x;
-            dh[ii] = z;
-          }
-        }
+        basis_vd_half<N, H>(R, tc, part, vh, dh);
         double u0 = 0.0, uA = 0.0, uB1 = 0.0, uB2 = 0.0;
 #pragma unroll
         for (int ii = 0; ii < H; ++ii) {
