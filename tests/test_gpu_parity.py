@@ -274,10 +274,11 @@ def test_cg_matches_oracle_cg(cf, cutgen_mod):
     from oracle.operator import cg as oracle_cg
     P = cutgen_mod.config("C1")
     op = cf.CutFEM(P)
-    b = op.rhs_const(1.0)
-    x, hist = op.cg(b, iters=30)
     O = Oracle(P)
-    xo, it = oracle_cg(O.apply, b.cpu().numpy(), tol=0.0, maxiter=30)
+    bo = O.rhs(lambda x: np.ones(len(x)))  # the oracle's RHS feeds both sides
+    b = torch.from_numpy(bo).cuda()
+    x, hist = op.cg(b, iters=30)
+    xo, it = oracle_cg(O.apply, bo, tol=0.0, maxiter=30)
     assert len(hist) == 31 and it == 30
     xg = x.cpu().numpy()
     assert np.abs(xg - xo).max() <= 1e-8 * np.abs(xo).max()

@@ -50,10 +50,12 @@ def test_h1_diag_matches_oracle(cf, cutgen_mod, p):
 def test_dg_jacobi_pcg_matches_oracle(cf, cutgen_mod):
     P = cutgen_mod.config("C1")
     op = cf.CutFEM(P)
-    b = op.rhs_const(1.0)
+    O = Oracle(P)
+    bo = O.rhs(lambda x: np.ones(len(x)))  # the oracle's RHS feeds both sides
+    b = torch.from_numpy(bo).cuda()
     x, hist = op.cg(b, iters=30, precond="jacobi")
-    M = Oracle(P).assemble_csr()
-    xo, it = oracle_cg(lambda y: M @ y, b.cpu().numpy(), tol=0.0, maxiter=30, M=1.0 / M.diagonal())
+    M = O.assemble_csr()
+    xo, it = oracle_cg(lambda y: M @ y, bo, tol=0.0, maxiter=30, M=1.0 / M.diagonal())
     assert it == 30 and len(hist) == 31
     assert np.abs(x.cpu().numpy() - xo).max() <= 1e-8 * np.abs(xo).max()
     r = b - op.apply(x)
@@ -75,11 +77,12 @@ def test_dg_jacobi_reduces_residual_faster(cf, cutgen_mod):
 def test_h1_pcg_matches_oracle_and_converges(cf, cutgen_mod):
     P = cutgen_mod.config("C1")
     op = cf.CutFEMH1(P)
-    b = op.rhs_const(1.0)
-    x, hist = op.cg(b, iters=25, precond="jacobi")
     O = OracleH1(P)
+    bo = O.rhs(lambda x: np.ones(len(x)))  # the oracle's RHS feeds both sides
+    b = torch.from_numpy(bo).cuda()
+    x, hist = op.cg(b, iters=25, precond="jacobi")
     M = O.assemble_csr()
-    xo, _ = oracle_cg(lambda y: M @ y, b.cpu().numpy(), tol=0.0, maxiter=25, M=1.0 / M.diagonal())
+    xo, _ = oracle_cg(lambda y: M @ y, bo, tol=0.0, maxiter=25, M=1.0 / M.diagonal())
     assert np.abs(x.cpu().numpy() - xo).max() <= 1e-8 * np.abs(xo).max()
     x2, h2 = op.cg(b, iters=3000, tol=1e-10, precond="jacobi")
     assert h2[-1] <= 1e-10 * float(b.norm())
