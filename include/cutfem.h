@@ -265,6 +265,71 @@ int cutfem_h1_pcg(cutfem_h1 *h, const double *b_dev, double *x_dev, int iters, d
 int cutfem_h1_diag(cutfem_h1 *h, double *d_dev, void *cuda_stream);
 int cutfem_h1_destroy(cutfem_h1 *h);
 
+/* ---- Chebyshev smoothing and polynomial multigrid (PAPER §3.5
+ * "a preconditioned conjugate gradient iteration ... polynomial multigrid
+ * (p-transfer) ... a Chebyshev smoother with an additive Schwarz inner
+ * preconditioner ... inverses of the diagonal blocks").  Oracle: oracle/solver.py.
+ *
+ * A cutfem_mg holds n_levels DG handles of ONE mesh (same n_cells, lower, h; not
+ * distributed), levels[0] the coarsest, degrees strictly increasing.  Each level
+ * smooths with the Chebyshev iteration (degree smooth_degree, interval
+ * [lam_max / smooth_range, lam_max] of D^-1 A) around an inner preconditioner D^-1:
+ *   CUTFEM_INNER_JACOBI  D = diag(A) (probed, as cutfem_diag);
+ *   CUTFEM_INNER_BLOCK   D = the (p+1)^3 x (p+1)^3 diagonal cell blocks A_KK (additive
+ *     Schwarz on the cells): probed with the (i+j+k) mod 2 checkerboard (2 (p+1)^3
+ *     applies), inverted on the device (in-place Gauss-Jordan sweep; the blocks are
+ *     SPD); every uncut cell whose six neighbours are active and uncut has the SAME
+ *     block (translation invariance), stored once; the other cells one each
+ *     ((p+1)^6 doubles per cell: memory grows with the number of cut cells and their
+ *     neighbours).
+ * Transfers (p-transfer): prolongation interpolates a cell's degree-p_c
+ * polynomial at the degree-p_f GLL nodes (cells matched by (i,j,k); a fine cell
+ * without a coarse counterpart gets 0), restriction is its transpose.  The
+ * coarsest level runs coarse_degree Chebyshev steps on [lam_max / coarse_range,
+ * lam_max] (a fixed polynomial: the V-cycle stays linear and symmetric).
+ * lam_max per level: eig_safety x the largest Ritz value of eig_iters Lanczos steps
+ * (the D^-1-preconditioned CG coefficients from a fixed pseudo-random start), or set
+ * by the caller (cutfem_mg_set_lambda).
+ *
+ * cutfem_mg_setup: probes / inverts, estimates lam_max (if eig_iters > 0); stream
+ *   ordered, synchronises once.  The handles must outlive the cutfem_mg.
+ * cutfem_mg_vcycle: z = B r on the finest level (device vectors, n_dofs of
+ *   levels[n_levels-1], 16-byte aligned, no alias).  One level: B is the coarse
+ *   Chebyshev iteration (Chebyshev-preconditioned CG).
+ * cutfem_mg_pcg: CG on A x = b (finest handle) preconditioned by the V-cycle; x_dev
+ *   in/out; res_hist (host, may be NULL) >= iters+1 entries: ||r_k||_2; stops once
+ *   ||r|| <= tol ||b|| when tol > 0.
+ * cutfem_mg_smooth: `degree` Chebyshev steps on level `level` for A x = r on
+ *   [lam_min, lam_max] (x_dev in/out; x0_given = 0: the start is 0).  For tests.
+ * cutfem_mg_transfer: dir 0: dst (level) = P src (level-1); dir 1: dst (level-1) =
+ *   P^T src (level).  For tests.
+ * Errors: CUTFEM_EINVAL (arguments, mismatched meshes / degrees, alignment),
+ * CUTFEM_ENOMEM, CUTFEM_EUNSUPPORTED (distributed handles), CUTFEM_ECUDA. */
+#define CUTFEM_INNER_JACOBI 0
+#define CUTFEM_INNER_BLOCK 1
+typedef struct {
+  int32_t inner;          /* CUTFEM_INNER_JACOBI | CUTFEM_INNER_BLOCK */
+  int32_t smooth_degree;  /* Chebyshev steps per pre- and post-smoothing (>= 1) */
+  double smooth_range;    /* > 1 */
+  int32_t coarse_degree;  /* Chebyshev steps on the coarsest level (>= 1) */
+  double coarse_range;    /* > 1 */
+  int32_t eig_iters;      /* Lanczos steps for lam_max (0: the caller sets them) */
+  double eig_safety;      /* lam_max = eig_safety x largest Ritz value (>= 1) */
+} cutfem_mg_params;
+typedef struct cutfem_mg cutfem_mg;
+int cutfem_mg_setup(cutfem_handle *const *levels, int32_t n_levels, const cutfem_mg_params *prm, void *cuda_stream,
+                    cutfem_mg **out);
+int cutfem_mg_lambda(const cutfem_mg *mg, double *lam_max);      /* host [n_levels] out */
+int cutfem_mg_set_lambda(cutfem_mg *mg, const double *lam_max);  /* host [n_levels] in */
+int cutfem_mg_vcycle(cutfem_mg *mg, const double *r_dev, double *z_dev, void *cuda_stream);
+int cutfem_mg_pcg(cutfem_mg *mg, const double *b_dev, double *x_dev, int iters, double tol, double *res_hist,
+                  int *iters_done, void *cuda_stream);
+int cutfem_mg_smooth(cutfem_mg *mg, int32_t level, const double *r_dev, double *x_dev, int32_t degree,
+                     double lam_max, double lam_min, int32_t x0_given, void *cuda_stream);
+int cutfem_mg_transfer(cutfem_mg *mg, int32_t level, int32_t dir, const double *src_dev, double *dst_dev,
+                       void *cuda_stream);
+int cutfem_mg_destroy(cutfem_mg *mg);
+
 int cutfem_stats(const cutfem_handle *hd, cutfem_stats_t *out);
 const char *cutfem_last_error(void);
 int cutfem_destroy(cutfem_handle *hd);

@@ -157,16 +157,22 @@ def pcg(apply, b, prec, iters: int, x0=None):
 
 
 def jacobi(A):
-    """Point Jacobi D^-1 = 1 / diag(A)."""
-    dinv = 1.0 / A.diagonal()
-    return lambda r: dinv * r
+    """Point Jacobi D^-1 = 1 / diag(A) (``.D``: the matrix D)."""
+    dg = A.diagonal()
+    dinv = 1.0 / dg
+
+    def minv(r):
+        return dinv * r
+    minv.D = np.diag(dg)
+    return minv
 
 
 def block_jacobi(A, nd: int):
     """Cell-block Jacobi (additive Schwarz on the cells): D = the n^3 x n^3
-    diagonal blocks A_KK, D^-1 r applied through their Cholesky factors."""
+    diagonal blocks A_KK, D^-1 r applied through their Cholesky factors (``.D``: D)."""
     Ad = A.tocsr()
-    facs = [np.linalg.cholesky(Ad[i:i + nd, i:i + nd].toarray()) for i in range(0, A.shape[0], nd)]
+    blocks = [Ad[i:i + nd, i:i + nd].toarray() for i in range(0, A.shape[0], nd)]
+    facs = [np.linalg.cholesky(B) for B in blocks]
 
     def minv(r):
         rb = np.asarray(r).reshape(-1, nd)
@@ -174,12 +180,17 @@ def block_jacobi(A, nd: int):
         for K, L in enumerate(facs):
             out[K] = np.linalg.solve(L.T, np.linalg.solve(L, rb[K]))
         return out.reshape(-1)
+    D = np.zeros(A.shape)
+    for K, B in enumerate(blocks):
+        D[K * nd:(K + 1) * nd, K * nd:(K + 1) * nd] = B
+    minv.D = D
     return minv
 
 
 def dense_lambda_max(A, minv) -> float:
-    """The largest eigenvalue of D^-1 A (dense: D^-1 A is similar to a symmetric matrix,
-    its eigenvalues are real)."""
+    """The largest eigenvalue of D^-1 A: the largest of the generalized symmetric
+    problem A x = lam D x (D = ``minv.D``, SPD), dense."""
+    import scipy.linalg as sl
     Ad = A.toarray() if hasattr(A, "toarray") else np.asarray(A)
-    MA = np.column_stack([minv(Ad[:, j]) for j in range(Ad.shape[1])])
-    return float(np.max(np.linalg.eigvals(MA).real))
+    n = Ad.shape[0]
+    return float(sl.eigh(Ad, minv.D, eigvals_only=True, subset_by_index=[n - 1, n - 1])[0])

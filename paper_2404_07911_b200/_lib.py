@@ -85,10 +85,19 @@ EXPORTS = ["cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_
            "cutfem_local_build", "cutfem_local_free", "cutfem_nccl_unique_id", "cutfem_setup_dist",
            "cutfem_dist_info", "cutfem_rhs_const", "cutfem_cg", "cutfem_h1_setup", "cutfem_h1_ndofs",
            "cutfem_h1_map", "cutfem_h1_apply", "cutfem_h1_rhs_const", "cutfem_h1_stats", "cutfem_h1_destroy",
-           "cutfem_pcg", "cutfem_diag", "cutfem_h1_pcg", "cutfem_h1_diag"]
+           "cutfem_pcg", "cutfem_diag", "cutfem_h1_pcg", "cutfem_h1_diag", "cutfem_mg_setup", "cutfem_mg_lambda",
+           "cutfem_mg_set_lambda", "cutfem_mg_vcycle", "cutfem_mg_pcg", "cutfem_mg_smooth", "cutfem_mg_transfer",
+           "cutfem_mg_destroy"]
 
 
 PRECOND = {"none": 0, "jacobi": 1}
+INNER = {"jacobi": 0, "block": 1}
+
+
+class MGParams(ctypes.Structure):
+    _fields_ = [("inner", ctypes.c_int32), ("smooth_degree", ctypes.c_int32), ("smooth_range", ctypes.c_double),
+                ("coarse_degree", ctypes.c_int32), ("coarse_range", ctypes.c_double),
+                ("eig_iters", ctypes.c_int32), ("eig_safety", ctypes.c_double)]
 
 
 class _Local(ctypes.Structure):
@@ -146,6 +155,19 @@ def load(path: str | None = None):
     L.cutfem_h1_pcg.argtypes = pcg_args
     L.cutfem_diag.argtypes = [vp, vp, vp]
     L.cutfem_h1_diag.argtypes = [vp, vp, vp]
+    L.cutfem_mg_setup.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, ctypes.POINTER(MGParams), vp,
+                                  ctypes.POINTER(vp)]
+    L.cutfem_mg_lambda.argtypes = [vp, vp]
+    L.cutfem_mg_set_lambda.argtypes = [vp, vp]
+    L.cutfem_mg_vcycle.argtypes = [vp, vp, vp, vp]
+    L.cutfem_mg_pcg.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_double, vp, ctypes.POINTER(ctypes.c_int), vp]
+    L.cutfem_mg_smooth.argtypes = [vp, ctypes.c_int32, vp, vp, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                   ctypes.c_int32, vp]
+    L.cutfem_mg_transfer.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, vp, vp, vp]
+    L.cutfem_mg_destroy.argtypes = [vp]
+    for name in ("cutfem_mg_setup", "cutfem_mg_lambda", "cutfem_mg_set_lambda", "cutfem_mg_vcycle", "cutfem_mg_pcg",
+                 "cutfem_mg_smooth", "cutfem_mg_transfer", "cutfem_mg_destroy"):
+        getattr(L, name).restype = i32
     for name in ("cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_host", "cutfem_csr_assemble",
                  "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_download", "cutfem_stats",
                  "cutfem_destroy", "cutfem_partition_x", "cutfem_local_build", "cutfem_nccl_unique_id",
@@ -484,3 +506,76 @@ class CutFEMDist(CutFEM):
         self._keep = (src_lo, src_hi)
         tp = lambda t: t.data_ptr() if t is not None and t.numel() else None  # noqa: E731
         _check(self._L.cutfem_debug_loopback(self._h, tp(src_lo), tp(src_hi)))
+
+
+class CutFEMMG:
+    """Chebyshev-smoothed polynomial multigrid over DG handles of one mesh
+    (include/cutfem.h cutfem_mg_*).  ``levels``: CutFEM handles, coarsest first,
+    degrees increasing.  One level = Chebyshev-preconditioned CG."""
+
+    def __init__(self, levels, inner: str = "block", smooth_degree: int = 3, smooth_range: float = 15.0,
+                 coarse_degree: int = 8, coarse_range: float = 40.0, eig_iters: int = 20, eig_safety: float = 1.1,
+                 stream=None):
+        L = load()
+        self._L = L
+        self.levels = list(levels)  # keeps the handles alive
+        prm = MGParams(INNER[inner], int(smooth_degree), float(smooth_range), int(coarse_degree),
+                       float(coarse_range), int(eig_iters), float(eig_safety))
+        arr = (ctypes.c_void_p * len(self.levels))(*[lv._h for lv in self.levels])
+        h = ctypes.c_void_p()
+        _check(L.cutfem_mg_setup(arr, len(self.levels), ctypes.byref(prm), _stream_ptr(stream), ctypes.byref(h)))
+        self._h = h
+        self.device = self.levels[-1].device
+        self.n_dofs = self.levels[-1].n_dofs
+
+    def lambdas(self) -> np.ndarray:
+        out = np.zeros(len(self.levels))
+        _check(self._L.cutfem_mg_lambda(self._h, out.ctypes.data))
+        return out
+
+    def set_lambdas(self, lam):
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        assert lam.size == len(self.levels)
+        _check(self._L.cutfem_mg_set_lambda(self._h, lam.ctypes.data))
+
+    def vcycle(self, r, z=None, stream=None):
+        import torch
+        if z is None:
+            z = torch.empty_like(r)
+        _check(self._L.cutfem_mg_vcycle(self._h, r.data_ptr(), z.data_ptr(), _stream_ptr(stream)))
+        return z
+
+    def pcg(self, b, x=None, iters: int = 50, tol: float = 0.0, stream=None):
+        """CG on A x = b (finest handle) preconditioned by one V-cycle per iteration.
+        Returns (x, ||r_k||, k = 0..done)."""
+        import torch
+        if x is None:
+            x = torch.zeros_like(b)
+        hist = np.zeros(int(iters) + 1, dtype=np.float64)
+        done = ctypes.c_int()
+        _check(self._L.cutfem_mg_pcg(self._h, b.data_ptr(), x.data_ptr(), int(iters), float(tol), hist.ctypes.data,
+                                     ctypes.byref(done), _stream_ptr(stream)))
+        return x, hist[:done.value + 1]
+
+    def smooth(self, level: int, r, x, degree: int, lam_max: float, lam_min: float, x0_given: bool = False,
+               stream=None):
+        _check(self._L.cutfem_mg_smooth(self._h, int(level), r.data_ptr(), x.data_ptr(), int(degree),
+                                        float(lam_max), float(lam_min), int(bool(x0_given)), _stream_ptr(stream)))
+        return x
+
+    def transfer(self, level: int, direction: str, src, dst, stream=None):
+        """direction "prolong": dst (level) = P src (level-1); "restrict": dst (level-1) = P^T src (level)."""
+        _check(self._L.cutfem_mg_transfer(self._h, int(level), {"prolong": 0, "restrict": 1}[direction],
+                                          src.data_ptr(), dst.data_ptr(), _stream_ptr(stream)))
+        return dst
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.cutfem_mg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

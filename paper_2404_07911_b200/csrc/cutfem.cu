@@ -125,6 +125,9 @@ struct cutfem_handle {
   int64_t dev_bytes = 0;
   cutfem_cg_work *cg = nullptr;  // CG work vectors (lazy)
   std::vector<int32_t> blk_ijk;  // cell of every block (owned, then ghosts): probe colouring
+  std::vector<uint8_t> blk_cut;  // is_cut of every block (owned, then ghosts): multigrid block classes
+  int32_t n_cells[3] = {0, 0, 0};
+  double lower[3] = {0, 0, 0};
 };
 
 namespace {
@@ -1250,6 +1253,11 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   hd->n_active = na;
   hd->mask = pb->term_mask ? pb->term_mask : CUTFEM_TERM_ALL;
   if (na > 0) hd->blk_ijk.assign(pb->active_ijk, pb->active_ijk + 3 * na);
+  if (na > 0) hd->blk_cut.assign(pb->is_cut, pb->is_cut + na);
+  for (int i = 0; i < 3; ++i) {
+    hd->n_cells[i] = pb->n_cells[i];
+    hd->lower[i] = pb->lower[i];
+  }
   CU(cudaSetDevice(device));
   // grid -> block map
   std::vector<int32_t> grid((size_t)(nx * ny * nz), -1);
@@ -1717,3 +1725,4 @@ int cutfem_destroy(cutfem_handle *hd) {
 #include "dist.inl"
 #include "cg.inl"
 #include "h1.inl"
+#include "mg.inl"
