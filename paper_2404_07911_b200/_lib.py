@@ -514,7 +514,7 @@ class CutFEMMG:
     degrees increasing.  One level = Chebyshev-preconditioned CG."""
 
     def __init__(self, levels, inner: str = "block", smooth_degree: int = 3, smooth_range: float = 15.0,
-                 coarse_degree: int = 8, coarse_range: float = 40.0, eig_iters: int = 20, eig_safety: float = 1.1,
+                 coarse_degree: int = 16, coarse_range: float = 40.0, eig_iters: int = 20, eig_safety: float = 1.1,
                  stream=None):
         L = load()
         self._L = L

@@ -112,6 +112,54 @@ __global__ void __launch_bounds__(MG_THREADS)
   }
 }
 
+// The cell-block step for a compile-time block size N3 = n^3: a CTA takes groups of
+// CPB = max(1, 256 / N3) cells, stages e = r - q of the group in shared memory, and each
+// thread forms rows a of t = Binv[slot K] e_K (8-way unrolled column sweep, four
+// independent sums: the block reads are the only HBM traffic, each entry read once),
+// then d = c1 d + c2 t, x (+)= d as k_mg_cheb.
+template <int N3>
+__global__ void __launch_bounds__(MG_THREADS)
+    k_mg_chebb(double *x, double *d, const double *__restrict__ r, const double *__restrict__ q,
+               const double *__restrict__ blocks, const int32_t *__restrict__ slot, int64_t nblk, double c1,
+               double c2, int xadd) {
+  constexpr int CPB = N3 >= MG_THREADS ? 1 : MG_THREADS / N3;
+  __shared__ double e[CPB * N3];
+  for (int64_t g0 = (int64_t)blockIdx.x * CPB; g0 < nblk; g0 += (int64_t)gridDim.x * CPB) {
+    const int nc = (int)(nblk - g0 < CPB ? nblk - g0 : CPB);
+    const int64_t base = g0 * N3;
+    for (int i = threadIdx.x; i < nc * N3; i += MG_THREADS) e[i] = q ? r[base + i] - q[base + i] : r[base + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < nc * N3; i += MG_THREADS) {
+      const int c = i / N3, a = i - c * N3;
+      const double *B = blocks + (int64_t)slot[g0 + c] * N3 * N3 + a;
+      const double *ec = e + c * N3;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int j = 0;
+#pragma unroll 2
+      for (; j + 8 <= N3; j += 8) {
+        double b[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) b[k] = B[(int64_t)(j + k) * N3];
+        s0 = fma(b[0], ec[j], s0);
+        s1 = fma(b[1], ec[j + 1], s1);
+        s2 = fma(b[2], ec[j + 2], s2);
+        s3 = fma(b[3], ec[j + 3], s3);
+        s0 = fma(b[4], ec[j + 4], s0);
+        s1 = fma(b[5], ec[j + 5], s1);
+        s2 = fma(b[6], ec[j + 6], s2);
+        s3 = fma(b[7], ec[j + 7], s3);
+      }
+      for (; j < N3; ++j) s0 = fma(B[(int64_t)j * N3], ec[j], s0);
+      const double t = (s0 + s1) + (s2 + s3);
+      const int64_t gi = base + i;
+      const double di = c1 == 0.0 ? c2 * t : fma(c1, d[gi], c2 * t);
+      d[gi] = di;
+      x[gi] = xadd ? x[gi] + di : di;
+    }
+    __syncthreads();
+  }
+}
+
 // x_f (+)= P x_c: thread per fine entry (K, a = ax + nf ay + nf^2 az):
 //   sum_b I[ax][bx] I[ay][by] I[az][bz] x_c[cmap K][b]   (0 when cmap K < 0)
 __global__ void __launch_bounds__(MG_THREADS)
@@ -301,9 +349,26 @@ int mg_pcg_cap(cutfem_mg *mg, int iters) {
 int mg_cheb_kernel(cutfem_mg *mg, cutfem_mg_level &L, double *x, double *d, const double *r, const double *q,
                    double c1, double c2, int xadd, cudaStream_t st) {
   const unsigned g = mg_grid(L.hd, L.ndof);
-  if (mg->prm.inner == CUTFEM_INNER_BLOCK)
-    k_mg_cheb<true><<<g, MG_THREADS, 0, st>>>(x, d, r, q, nullptr, L.blocks, L.slot, L.ndof, L.n3, c1, c2, xadd);
-  else
+  if (mg->prm.inner == CUTFEM_INNER_BLOCK) {
+    const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(L.nblk, 16 * L.hd->sm_count));
+#define MG_CHEBB(NN)                                                                                         \
+  case NN:                                                                                                   \
+    k_mg_chebb<NN * NN * NN><<<gb, MG_THREADS, 0, st>>>(x, d, r, q, L.blocks, L.slot, L.nblk, c1, c2, xadd); \
+    break;
+    switch (L.n) {
+      MG_CHEBB(2)
+      MG_CHEBB(3)
+      MG_CHEBB(4)
+      MG_CHEBB(5)
+      MG_CHEBB(6)
+      MG_CHEBB(7)
+      MG_CHEBB(8)
+      MG_CHEBB(9)
+      default:
+        k_mg_cheb<true><<<g, MG_THREADS, 0, st>>>(x, d, r, q, nullptr, L.blocks, L.slot, L.ndof, L.n3, c1, c2, xadd);
+    }
+#undef MG_CHEBB
+  } else
     k_mg_cheb<false><<<g, MG_THREADS, 0, st>>>(x, d, r, q, L.dinv, nullptr, nullptr, L.ndof, L.n3, c1, c2, xadd);
   CU(cudaGetLastError());
   return 0;

@@ -49,7 +49,7 @@ for label, lv, inner in (("chebyshev-block-pcg", ops[-1:], "block"), ("pmg-block
                          ("pmg-jacobi-pcg", ops, "jacobi")):
     torch.cuda.synchronize()
     t = time.time()
-    mg = cf.CutFEMMG(lv, inner=inner, smooth_degree=3, coarse_degree=8, eig_iters=20)
+    mg = cf.CutFEMMG(lv, inner=inner, smooth_degree=3, coarse_degree=16, eig_iters=20)
     torch.cuda.synchronize()
     ts = time.time() - t
     rec = run(label, lambda: mg.pcg(b, iters=maxit, tol=1e-8))
@@ -58,3 +58,35 @@ for label, lv, inner in (("chebyshev-block-pcg", ops[-1:], "block"), ("pmg-block
     out["runs"].append(rec)
     del mg
 print(json.dumps(out))
+
+
+def ev_ms(fn, reps=10):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn()
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+if len(sys.argv) > 3 and sys.argv[3] == "grid":
+    mg = cf.CutFEMMG(ops, inner="block", eig_iters=20)
+    lam = mg.lambdas()
+    r = torch.rand(P.n_dofs, dtype=torch.float64, device="cuda")
+    z = torch.empty_like(r)
+    parts = {"apply_fine_ms": ev_ms(lambda: ops[-1].apply(r, z)),
+             "apply_coarse_ms": ev_ms(lambda: ops[0].apply(torch.zeros(ops[0].n_dofs, dtype=torch.float64,
+                                                                       device="cuda"))),
+             "block_step_fine_ms": ev_ms(lambda: mg.smooth(len(ops) - 1, r, z, 1, lam[-1], lam[-1] / 15)),
+             "vcycle_ms": ev_ms(lambda: mg.vcycle(r, z))}
+    grid = []
+    for sd in (2, 3, 5):
+        for cdg in (4, 8, 16):
+            mg = cf.CutFEMMG(ops, inner="block", smooth_degree=sd, coarse_degree=cdg, eig_iters=20)
+            rec = run(f"pmg-block sd={sd} cd={cdg}", lambda: mg.pcg(b, iters=maxit, tol=1e-8))
+            grid.append(rec)
+            del mg
+    print(json.dumps({"parts": parts, "grid": grid}))
