@@ -680,13 +680,33 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         const CDesc2 &e = c2[o + i];
         isline[o + i] = N >= 3 && e.nv > 0 && vol_line_axis(pb->vol_pts + 4 * e.vb, e.nv, N) >= 0;
       }
+#ifndef CUTP_C_LINE
+#define CUTP_C_LINE 2.8
+#endif
+#ifndef CUTP_C_FLINE
+#define CUTP_C_FLINE 1.2
+#endif
+#ifndef CUTP_C_CELL
+#define CUTP_C_CELL 1.5
+#endif
+#ifndef CUTP_C_SAX
+#define CUTP_C_SAX 0.0
+#endif
+#ifndef CUTP_C_TRACE
+#define CUTP_C_TRACE 0.0
+#endif
       auto cost = [&](const CDesc2 &e) {
         const int64_t i = &e - c2.data();
-        // a chunk of 32 cut-face lines costs about 1.2 point chunks
-        const double fl = fl0[i] >= 0 ? 1.2 * ((fln[i] + 31) / 32) : 0.0;
+        // a chunk of 32 cut-face lines costs about CUTP_C_FLINE point chunks
+        const double fl = fl0[i] >= 0 ? CUTP_C_FLINE * ((fln[i] + 31) / 32) : 0.0;
         const int nf = fl0[i] >= 0 ? 0 : e.nf;
-        if (isline[i]) return 2.8 * ((e.nv / N + 31) / 32) + (double)((e.ns + nf + 31) / 32) + fl + 1.5;
-        return (double)((e.nv + e.ns + nf + 31) / 32) + fl + 1.5;
+        // per cell: a fixed part, the axes with structured (GP / full-face SIPG) faces, the
+        // cut faces' traces
+        const uint32_t st = (e.smask & 0x3fu) | ((e.smask >> 8) & 0x3fu);
+        const int sax = ((st & 3u) != 0) + ((st & 12u) != 0) + ((st & 48u) != 0);
+        const double cell = CUTP_C_CELL + CUTP_C_SAX * sax + CUTP_C_TRACE * __builtin_popcount(e.fmask);
+        if (isline[i]) return CUTP_C_LINE * ((e.nv / N + 31) / 32) + (double)((e.ns + nf + 31) / 32) + fl + cell;
+        return (double)((e.nv + e.ns + nf + 31) / 32) + fl + cell;
       };
       for (int64_t i = 0; i < n; ++i) idx[i] = o + i;
       std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return cost(c2[a]) > cost(c2[b]); });
@@ -1686,15 +1706,15 @@ int cutfem_debug_timeline(int reset, unsigned long long *out) {
       h[k][1] = 0;
     }
     CU(cudaMemcpyToSymbol(g_tl, h, sizeof(h)));
-    std::vector<unsigned long long> z(8192, 0);
-    CU(cudaMemcpyToSymbol(g_tlw, z.data(), sizeof(unsigned long long) * 8192));
+    std::vector<unsigned long long> z(3 * 8192, 0);
+    CU(cudaMemcpyToSymbol(g_tlw, z.data(), sizeof(unsigned long long) * 3 * 8192));
   } else {
     CU(cudaMemcpyFromSymbol(h, g_tl, sizeof(h)));
     for (int k = 0; k < 8; ++k) {
       out[2 * k] = h[k][0];
       out[2 * k + 1] = h[k][1];
     }
-    CU(cudaMemcpyFromSymbol(out + 16, g_tlw, sizeof(unsigned long long) * 8192));
+    CU(cudaMemcpyFromSymbol(out + 16, g_tlw, sizeof(unsigned long long) * 3 * 8192));
   }
   return 0;
 #else

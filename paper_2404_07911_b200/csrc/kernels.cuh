@@ -31,9 +31,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-__device__ unsigned long long g_tlw[8192];  // k_cutp: per-warp end time
+__device__ unsigned long long g_tlw[3][8192];  // k_cutp: per-warp end time, start time, SM id
 #define TL_WARP_END(gw) \
-  if ((threadIdx.x & 31) == 0 && (gw) < 8192) g_tlw[gw] = gtimer();
+  if ((threadIdx.x & 31) == 0 && (gw) < 8192) g_tlw[0][gw] = gtimer();
+#define TL_WARP_BEGIN(gw)                                 \
+  if ((threadIdx.x & 31) == 0 && (gw) < 8192) {           \
+    unsigned sm;                                          \
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));       \
+    g_tlw[1][gw] = gtimer();                              \
+    g_tlw[2][gw] = sm;                                    \
+  }
 #define TL_BEGIN(k) \
   if (threadIdx.x == 0) atomicMin(&g_tl[k][0], gtimer());
 #define TL_END(k) \
@@ -42,6 +49,7 @@ __device__ unsigned long long g_tlw[8192];  // k_cutp: per-warp end time
 #define TL_BEGIN(k)
 #define TL_END(k)
 #define TL_WARP_END(gw)
+#define TL_WARP_BEGIN(gw)
 #endif
 #ifndef CUTFEM_USE_BULK
 #define CUTFEM_USE_BULK 1

@@ -533,6 +533,7 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
   const int c0w = wstart[gw], c1w = wstart[gw + 1];
   if (c0w >= c1w) return;
   TL_BEGIN(0);
+  TL_WARP_BEGIN(gw);
   const int p0w = pstart[gw], p1w = pstart[gw + 1];
   double *base = smem + warp * C::WSLOT;
   uint64_t *bar = reinterpret_cast<uint64_t *>(base);  // 0,1: block sets; 2..2+NB: chunk ring
