@@ -45,8 +45,12 @@ def run(label, fn):
 out = {"config": name, "degree": pf, "levels": degs, "n_dofs": P.n_dofs, "gen_s": tgen, "runs": []}
 ops[-1].cg(b, iters=1, precond="jacobi")  # probe the diagonal outside the timing
 out["runs"].append(run("jacobi-pcg", lambda: ops[-1].cg(b, iters=maxit, tol=1e-8, precond="jacobi")))
+out["runs"].append(run("cg", lambda: ops[-1].cg(b, iters=maxit, tol=1e-8)))
+inners = os.environ.get("MG_INNER", "block,jacobi").split(",")
 for label, lv, inner in (("chebyshev-block-pcg", ops[-1:], "block"), ("pmg-block-pcg", ops, "block"),
-                         ("pmg-jacobi-pcg", ops, "jacobi")):
+                         ("chebyshev-jacobi-pcg", ops[-1:], "jacobi"), ("pmg-jacobi-pcg", ops, "jacobi")):
+    if inner not in inners:
+        continue
     torch.cuda.synchronize()
     t = time.time()
     mg = cf.CutFEMMG(lv, inner=inner, smooth_degree=3, coarse_degree=16, eig_iters=20)
