@@ -1,6 +1,6 @@
 """H1 (continuous Galerkin) operator throughput and the Jacobi-PCG solve (SURVEY
 §8(f) f2, f4): CUDA events on the stream, L2 flushed before every apply.
-usage: python tools/h1_bench.py [CFG ...]   (one JSON line per config)"""
+usage: python tools/h1_bench.py [CFG|C3:p ...]   (one JSON line per config; NO_CG=1: apply only)"""
 import json
 import os
 import sys
@@ -29,7 +29,8 @@ def timed(fn, K=20):
 
 
 for cfg in (sys.argv[1:] or ["C2", "C5"]):
-    P = cutgen.config(cfg)
+    name, _, deg = cfg.partition(":")  # "C3:p" = the degree sweep mesh of degree p
+    P = cutgen.config(name, degree=int(deg) if deg else None)
     t0 = time.time()
     h1 = cf.CutFEMH1(P)
     t_setup = time.time() - t0
@@ -46,7 +47,7 @@ for cfg in (sys.argv[1:] or ["C2", "C5"]):
            "what": "H1 apply = gather + block kernels without SIPG + fixed-order scatter"}
     # PCG: iterations to ||r|| <= 1e-6 ||b|| (DG), plain vs Jacobi
     b = dg.rhs_const(1.0)
-    for pc in ("none", "jacobi"):
+    for pc in (() if os.environ.get("NO_CG") else ("none", "jacobi")):
         torch.cuda.synchronize()
         t0 = time.time()
         x, hist = dg.cg(b, iters=3000, tol=1e-6, precond=pc)
