@@ -27,6 +27,9 @@
 #include <vector>
 
 #include "../../include/cutfem.h"
+#ifndef CUTFEM_CUT1_MAXN
+#define CUTFEM_CUT1_MAXN 2  // n <= this: one thread per cut cell (k_cut1) instead of a warp (k_cutp)
+#endif
 #include "kernels.cuh"
 #include "tables.h"
 #ifndef CUT_ORDER
@@ -574,7 +577,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
   }
   int rc = upload(hd, reinterpret_cast<char **>(&hd->d_tiles), all.data(), all.size());
   if (rc) return rc;
-  {
+  if (N > CUTFEM_CUT1_MAXN) {  // (n <= CUTFEM_CUT1_MAXN: k_cut1 reads the descriptors directly)
     // k_cutp: per cut cell its own list of cut-face points in its reference
     // coordinates [xi, eta, zeta, W] (normal coordinate exactly 0 or 1)
     std::vector<CDesc2> c2(cd.size());
@@ -1039,7 +1042,15 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
   const int64_t ncell = (which & 1) ? hd->r_cnt[part][0] + hd->r_cnt[part][1] : 0;
   bool pdl = false;  // the first kernel of the apply is a normal launch
   int rc;
-  if (nc > 0) {
+  if constexpr (NT <= CUTFEM_CUT1_MAXN) {
+    if (nc > 0) {
+      if ((rc = launch_k(k_cut1<NT>, (unsigned)((nc + 127) / 128), 128, 0, st, pdl, u, v,
+                         hd->d_cdesc + hd->r_off[part][2], (int)nc, hd->d_vol, hd->d_srf, hd->d_sfp, hd->d_sfptr,
+                         hd->kp, *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data()))))
+        return rc;
+      pdl = true;
+    }
+  } else if (nc > 0) {
     using CP = CutPCfg<NT>;
     // part 0 = the interior list then the slab-boundary list (each with its own warp schedule)
     for (int pt = 1; pt <= 2; ++pt) {

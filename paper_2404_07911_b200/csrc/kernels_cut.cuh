@@ -1,5 +1,6 @@
-// k_cutp<N> (N = p+1 <= 4): the unstructured terms of the cut cells (Alg. 1
-// "intersected" branch), included by kernels.cuh.
+// k_cutp<N> (N = p+1 = 3, 4) and k_cut1<N> (N = 2, at the end of this file): the
+// unstructured terms of the cut cells (Alg. 1 "intersected" branch),
+// included by kernels.cuh.
 //
 // One warp per cut cell, lanes = quadrature points (the paper's vectorisation
 // over points), persistent: every warp walks its own list of cells, the
@@ -979,3 +980,252 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
   TL_END(0);
 }
 
+
+// ======================================================= cut cells, p = 1 (k_cut1)
+// One THREAD per cut cell (k_cell's layout for the uncut cells): at p = 1 a cut cell
+// has ~30 points and 8 DoFs, so a warp per cell (k_cutp) spends most of its time in
+// per-cell work done by a few lanes (traces, structured faces, the cross-lane
+// reduction); here 32 cells run side by side in SIMT and every accumulator is the
+// thread's own.  Cells come heavy-first in the descriptor list, so a warp's cells
+// have similar point counts.  Per cell (all FP64, same formulas as k_cutp):
+//   1. structured faces (ghost penalty, full-face SIPG) in w-space with the
+//      M^-1-premultiplied line operators (k_cell), then w <- (M (x) M (x) M) w; acc = w
+//   2. volume points   acc += W/h^2 grad u . grad phi               (eq:unstructured_cell)
+//   3. interface points acc += Nitsche W [-(d_n phi) u - phi d_n u + tau phi u]
+//   4. cut faces: traces [u], d u_own + d u_nb on the n^2 in-face nodes, per point
+//      the 2-D interpolation and the flux coefficients summed per in-face node, then
+//      applied along the face normal (eq:unstructured_face P:489-496)
+// Neighbour values are read straight from global memory (L1 / L2 hits).
+template <int N>
+__global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, double *__restrict__ v,
+                                              const CDesc *__restrict__ desc, int ncut,
+                                              const double *__restrict__ vol_pts, const double *__restrict__ srf_pts,
+                                              const double *__restrict__ sf_pts, const int64_t *__restrict__ sf_ptr,
+                                              KParams kp, TileTab<N> tt) {
+  constexpr int NN = N * N, N3 = NN * N;
+  const RefTab &R = c_ref[N - 2];
+  pdl_trigger();  // every CTA has begun -> the uncut-cell kernels may start
+  if (blockIdx.x == 0 && threadIdx.x == 0) pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncut) return;
+  const CDesc d = desc[i];
+  const bool cell_on = (kp.mask & TERM_CELL) != 0, sipg_on = (kp.mask & TERM_SIPG) != 0,
+             nit_on = (kp.mask & TERM_NITSCHE) != 0, gp_on = (kp.mask & TERM_GP) != 0;
+  double uo[N3], acc[N3];
+  {
+    const double *ub = u + (size_t)d.blk * N3;
+#pragma unroll
+    for (int k = 0; k < N3; ++k) uo[k] = __ldg(ub + k);
+  }
+  // ---- 1. structured faces in w-space
+#pragma unroll
+  for (int l = 0; l < N3; ++l) acc[l] = 0.0;
+  bool any_st = false;
+  static_for<0, 6>([&](auto fc) {
+    constexpr int F = decltype(fc)::value, D = F / 2, SS = F % 2;
+    const bool g = gp_on && d.nb[F] >= 0 && ((d.flags >> F) & 1u);
+    const bool sp = sipg_on && d.nb[F] >= 0 && ((d.flags >> (6 + F)) & 1u);
+    if (!(g || sp)) return;
+    any_st = true;
+    const double *nbp = u + (size_t)d.nb[F] * N3;
+#pragma unroll
+    for (int t = 0; t < NN; ++t) {
+      double o[N], n_[N], out[N];
+#pragma unroll
+      for (int m = 0; m < N; ++m) {
+        o[m] = uo[lix<N, D>(t, m)];
+        n_[m] = __ldg(nbp + lix<N, D>(t, m));
+        out[m] = 0.0;
+      }
+      if (g) {
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          double x = 0.0;
+#pragma unroll
+          for (int a = 0; a < N; ++a) {
+            const int k = SS ? (N - 1 - m) * N + (N - 1 - a) : m * N + a;
+            x = fma(tt.Goo[k], o[a], fma(tt.Gon[k], n_[a], x));
+          }
+          out[m] = x;
+        }
+      }
+      if (sp) {
+        double A0 = 0.0, A1 = 0.0;
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          if (SS == 0) {
+            A0 = fma(tt.d0[m], o[m], A0);
+            A1 = fma(-tt.d0[N - 1 - m], n_[m], A1);
+          } else {
+            A0 = fma(-tt.d0[N - 1 - m], o[m], A0);
+            A1 = fma(tt.d0[m], n_[m], A1);
+          }
+        }
+        const double J = SS ? (o[N - 1] - n_[0]) : (o[0] - n_[N - 1]);
+        const double A = A0 + A1;
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          if (SS == 0) out[m] = fma(tt.cJ[m], J, fma(tt.cA[m], A, out[m]));
+          else out[m] = fma(tt.cJ[N - 1 - m], J, fma(-tt.cA[N - 1 - m], A, out[m]));
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < N; ++m) acc[lix<N, D>(t, m)] += out[m];
+    }
+  });
+  if (any_st) {  // acc <- (M (x) M (x) M) acc
+    static_for<0, 3>([&](auto dc) {
+      constexpr int D = decltype(dc)::value;
+#pragma unroll
+      for (int t = 0; t < NN; ++t) {
+        double x[N];
+#pragma unroll
+        for (int m = 0; m < N; ++m) x[m] = acc[lix<N, D>(t, m)];
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          double y = 0.0;
+#pragma unroll
+          for (int b = 0; b < N; ++b) y = fma(tt.M[csym<N>(a * N + b)], x[b], y);
+          acc[lix<N, D>(t, a)] = y;
+        }
+      }
+    });
+  }
+  // ---- 2./3. volume and interface points: value + reference gradient, the point
+  //      coefficients, the rank-update of acc (c0 on phi, c1..c3 on d_x, d_y, d_z phi)
+  auto point = [&](double xi, double eta, double zeta, double W, bool nit, double nx, double ny, double nz) {
+    double vx[N], dvx[N], vy[N], dvy[N], vz[N], dvz[N];
+    basis_vd_sym<N>(R, xi, vx, dvx);
+    basis_vd_sym<N>(R, eta, vy, dvy);
+    basis_vd_sym<N>(R, zeta, vz, dvz);
+    double u0 = 0.0, ux = 0.0, uy = 0.0, uz = 0.0;
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double t00 = 0.0, t10 = 0.0, t01 = 0.0;
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+          s0 = fma(vx[a], uo[(c * N + b) * N + a], s0);
+          s1 = fma(dvx[a], uo[(c * N + b) * N + a], s1);
+        }
+        t00 = fma(vy[b], s0, t00);
+        t10 = fma(dvy[b], s0, t10);
+        t01 = fma(vy[b], s1, t01);
+      }
+      u0 = fma(vz[c], t00, u0);
+      uz = fma(dvz[c], t00, uz);
+      uy = fma(vz[c], t10, uy);
+      ux = fma(vz[c], t01, ux);
+    }
+    double c0 = 0.0, c1, c2, c3;
+    if (nit) {
+      const double un = (nx * ux + ny * uy + nz * uz) * kp.ih;  // physical normal derivative
+      c0 = W * (kp.tau * u0 - un);
+      const double g = -W * u0 * kp.ih;
+      c1 = g * nx;
+      c2 = g * ny;
+      c3 = g * nz;
+    } else {
+      const double sw = W * kp.ih2;
+      c1 = sw * ux;
+      c2 = sw * uy;
+      c3 = sw * uz;
+    }
+#pragma unroll
+    for (int cz = 0; cz < N; ++cz) {
+      const double T0 = fma(c0, vz[cz], c3 * dvz[cz]);
+      const double T1 = c2 * vz[cz];
+      const double T2 = c1 * vz[cz];
+#pragma unroll
+      for (int by = 0; by < N; ++by) {
+        const double S0 = fma(vy[by], T0, dvy[by] * T1);
+        const double S1 = vy[by] * T2;
+#pragma unroll
+        for (int ax = 0; ax < N; ++ax) {
+          double &r = acc[(cz * N + by) * N + ax];
+          r = fma(vx[ax], S0, fma(dvx[ax], S1, r));
+        }
+      }
+    }
+  };
+  if (cell_on) {
+    const double *p = vol_pts + 4 * d.vb;
+    for (int q = 0; q < d.nv; ++q, p += 4) {
+      const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+      const double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+      point(a.x, a.y, b.x, b.y, false, 0.0, 0.0, 0.0);
+    }
+  }
+  if (nit_on) {
+    const double *p = srf_pts + 8 * d.sb;
+    for (int q = 0; q < d.ns; ++q, p += 8) {
+      const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+      const double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+      const double2 c = __ldg(reinterpret_cast<const double2 *>(p) + 2);
+      const double2 e = __ldg(reinterpret_cast<const double2 *>(p) + 3);
+      point(a.x, a.y, b.x, e.x, true, b.y, c.x, c.y);
+    }
+  }
+  // ---- 4. cut faces
+  if (sipg_on) {
+    static_for<0, 6>([&](auto fc) {
+      constexpr int F = decltype(fc)::value, D = F / 2, SS = F % 2;
+      if (!(d.nb[F] >= 0 && ((d.flags >> (12 + F)) & 1u))) return;
+      const double *nbp = u + (size_t)d.nb[F] * N3;
+      constexpr int fo = SS ? N - 1 : 0, fn = SS ? 0 : N - 1;
+      const double *dow = SS ? R.d1 : R.d0;
+      const double *dnb = SS ? R.d0 : R.d1;
+      double JA[NN], JB[NN], F1[NN], F2[NN];
+#pragma unroll
+      for (int t = 0; t < NN; ++t) {
+        double A = 0.0;
+#pragma unroll
+        for (int m = 0; m < N; ++m) A = fma(dow[m], uo[lix<N, D>(t, m)], fma(dnb[m], __ldg(nbp + lix<N, D>(t, m)), A));
+        JA[t] = uo[lix<N, D>(t, fo)] - __ldg(nbp + lix<N, D>(t, fn));
+        JB[t] = A;
+        F1[t] = F2[t] = 0.0;
+      }
+      const double sg = SS ? 1.0 : -1.0;
+      const int64_t pb = sf_ptr[d.sf[F]], pe = sf_ptr[d.sf[F] + 1];
+      for (int64_t q = pb; q < pe; ++q) {
+        const double2 st = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * q));
+        const double W = __ldg(sf_pts + 4 * q + 2);
+        double ls[N], lt[N];
+        basis_v_sym<N>(R, st.x, ls);
+        basis_v_sym<N>(R, st.y, lt);
+        double J0 = 0.0, A = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+          for (int a = 0; a < N; ++a) {
+            r0 = fma(ls[a], JA[a + N * j], r0);
+            r1 = fma(ls[a], JB[a + N * j], r1);
+          }
+          J0 = fma(lt[j], r0, J0);
+          A = fma(lt[j], r1, A);
+        }
+        const double k1 = W * (kp.sigma * J0 - sg * A * kp.i2h), k2 = -W * sg * J0 * kp.i2h;
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+#pragma unroll
+          for (int a = 0; a < N; ++a) {
+            const double psi = ls[a] * lt[j];
+            F1[a + N * j] = fma(psi, k1, F1[a + N * j]);
+            F2[a + N * j] = fma(psi, k2, F2[a + N * j]);
+          }
+      }
+#pragma unroll
+      for (int t = 0; t < NN; ++t) {
+#pragma unroll
+        for (int m = 0; m < N; ++m) acc[lix<N, D>(t, m)] = fma(dow[m], F2[t], acc[lix<N, D>(t, m)]);
+        acc[lix<N, D>(t, fo)] += F1[t];
+      }
+    });
+  }
+  double *vb = v + (size_t)d.blk * N3;
+#pragma unroll
+  for (int k = 0; k < N3; ++k) vb[k] = acc[k];
+}

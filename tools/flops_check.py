@@ -36,6 +36,6 @@ for b in blocks:
             m.get("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", 0) + \
             m.get("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", 0)
         t = m.get("gpu__time_duration.sum", 0) * 1e-9
-        fam = "F_cut" if ("cutp" in name or "k_cut<" in name) else "F_uncut"
+        fam = "F_cut" if ("cutp" in name or "k_cut<" in name or "k_cut1" in name) else "F_uncut"
         alg = w[fam]
         print(f"{cfg:>10} {name:>16} {t * 1e6:9.1f} {ex / 1e9:11.3f} {alg / 1e9:10.3f} {ex / alg:9.2f} {ex / t / 1e12 if t else 0:10.2f}")
