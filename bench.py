@@ -410,7 +410,7 @@ def run_ours(args, P, cfg, rank, world, local_rank):
     fp64 = costmodel.fp64_peak_tflops() * 1e12
     n_ = P.degree + 1
     if n_ <= 3:
-        kname = {"structured": f"k_cell<{n_}>", "unstructured": f"k_cut1<{n_}>" if n_ == 2 else f"k_cutp<{n_}>"}
+        kname = {"structured": f"k_cell<{n_}>", "unstructured": f"k_cut1<{n_}>"}
     elif n_ == 4:
         kname = {"structured": "k_tile2<4,0> + k_uncw<4,8>", "unstructured": "k_cutp<4>"}
     else:

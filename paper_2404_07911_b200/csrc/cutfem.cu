@@ -28,7 +28,13 @@
 
 #include "../../include/cutfem.h"
 #ifndef CUTFEM_CUT1_MAXN
-#define CUTFEM_CUT1_MAXN 2  // n <= this: one thread per cut cell (k_cut1) instead of a warp (k_cutp)
+#define CUTFEM_CUT1_MAXN 3  // n <= this: a few threads per cut cell (k_cut1) instead of a warp (k_cutp)
+#endif
+#ifndef CUT1_TPC2
+#define CUT1_TPC2 1  // k_cut1 threads per cut cell at n = 2 (2: kernel alone 69.7 -> 57.3 us, apply 119.9 -> 121.9)
+#endif
+#ifndef CUT1_TPC3
+#define CUT1_TPC3 2  // ... at n = 3 (C3 p=2 apply: 1 thread 246, 2: 213, 4: 236, 8: 282 us; k_cutp<3> 238)
 #endif
 #include "kernels.cuh"
 #include "tables.h"
@@ -577,7 +583,7 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
   }
   int rc = upload(hd, reinterpret_cast<char **>(&hd->d_tiles), all.data(), all.size());
   if (rc) return rc;
-  if (N > CUTFEM_CUT1_MAXN) {  // (n <= CUTFEM_CUT1_MAXN: k_cut1 reads the descriptors directly)
+  if constexpr (N > CUTFEM_CUT1_MAXN) {  // (n <= CUTFEM_CUT1_MAXN: k_cut1 reads the descriptors directly)
     // k_cutp: per cut cell its own list of cut-face points in its reference
     // coordinates [xi, eta, zeta, W] (normal coordinate exactly 0 or 1)
     std::vector<CDesc2> c2(cd.size());
@@ -729,10 +735,8 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         for (int64_t i : lists[w]) {
           const CDesc2 &e = c2[i];
           c2o[pos++] = e;
-          // the chunks of this cell.  n <= CUTP_UNIFIED_MAXN: every point kind in one stream;
-          // else [volume | interface] points in chunks of 32, then the cut-face points axis
-          // by axis (a chunk never mixes a face point with another kind or face axis: one
-          // code path per chunk, which pays at n = 4 where registers are tight)
+          // the chunks of this cell (a chunk never mixes a cut-face point with another kind:
+          // one code path per chunk, which pays at n = 4 where registers are tight)
           int nv = (hd->mask & CUTFEM_TERM_CELL) ? e.nv : 0;
           int ns = (hd->mask & CUTFEM_TERM_NITSCHE) ? e.ns : 0;
           const bool fon = (hd->mask & CUTFEM_TERM_SIPG) != 0;
@@ -774,42 +778,26 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
               ++nfc;
             }
           }
-          if constexpr (CutPCfg<N>::UNIFIED) {
-            // one stream: volume, interface, cut-face points (any axis) in chunks of 32
-            const int nf = (fon && !fdone) ? e.nf : 0;
-            for (int q0 = 0; q0 < nv + ns + nf; q0 += 32) {
-              const int cv = std::max(0, std::min(32, nv - q0));
-              const int qs = std::max(0, q0 - nv), cs = std::max(0, std::min(32 - cv, ns - qs));
-              const int qf = std::max(0, q0 - nv - ns), cf = std::max(0, std::min(32 - cv - cs, nf - qf));
+          // [volume | interface] points in chunks of 32, then the cut-face points (one
+          // stream over every face axis: runtime-axis update)
+          for (int q0 = 0; q0 < nv + ns; q0 += 32) {
+            const int cv = std::max(0, std::min(32, nv - q0));
+            const int qs = std::max(0, q0 - nv), cs = std::max(0, std::min(32 - cv, ns - qs));
+            CChunk r;
+            r.vo = (int32_t)(e.vb + q0);
+            r.so = (int32_t)(e.sb + qs);
+            r.fo = (int32_t)e.fb;
+            r.cnt = cv | (cs << 8);
+            chunk.push_back(r);
+          }
+          if (fon && !fdone) {  // every face axis in one stream (runtime-axis update)
+            for (int q0 = 0; q0 < e.nf; q0 += 32) {
               CChunk r;
-              r.vo = (int32_t)(e.vb + std::min(q0, nv));
-              r.so = (int32_t)(e.sb + qs);
-              r.fo = (int32_t)(e.fb + qf);
-              r.cnt = cv | (cs << 8) | (cf << 16);
+              r.vo = (int32_t)e.vb;
+              r.so = (int32_t)e.sb;
+              r.fo = (int32_t)(e.fb + q0);
+              r.cnt = std::min(32, e.nf - q0) << 16;
               chunk.push_back(r);
-            }
-          } else {
-            for (int q0 = 0; q0 < nv + ns; q0 += 32) {
-              const int cv = std::max(0, std::min(32, nv - q0));
-              const int qs = std::max(0, q0 - nv), cs = std::max(0, std::min(32 - cv, ns - qs));
-              CChunk r;
-              r.vo = (int32_t)(e.vb + q0);
-              r.so = (int32_t)(e.sb + qs);
-              r.fo = (int32_t)e.fb;
-              r.cnt = cv | (cs << 8);
-              chunk.push_back(r);
-            }
-            int64_t fo = e.fb;
-            (void)fo;
-            if (fon && !fdone) {  // every face axis in one stream (runtime-axis update)
-              for (int q0 = 0; q0 < e.nf; q0 += 32) {
-                CChunk r;
-                r.vo = (int32_t)e.vb;
-                r.so = (int32_t)e.sb;
-                r.fo = (int32_t)(e.fb + q0);
-                r.cnt = std::min(32, e.nf - q0) << 16;
-                chunk.push_back(r);
-              }
             }
           }
           if (chunk.size() - k0 > 0xffff || nlc > 0xff || nfc > 0xff)
@@ -1044,7 +1032,8 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
   int rc;
   if constexpr (NT <= CUTFEM_CUT1_MAXN) {
     if (nc > 0) {
-      if ((rc = launch_k(k_cut1<NT>, (unsigned)((nc + 127) / 128), 128, 0, st, pdl, u, v,
+      constexpr int TPC = NT == 2 ? CUT1_TPC2 : CUT1_TPC3;
+      if ((rc = launch_k(k_cut1<NT, TPC>, (unsigned)((nc * TPC + 127) / 128), 128, 0, st, pdl, u, v,
                          hd->d_cdesc + hd->r_off[part][2], (int)nc, hd->d_vol, hd->d_srf, hd->d_sfp, hd->d_sfptr,
                          hd->kp, *reinterpret_cast<const TileTab<NT> *>(hd->ttab.data()))))
         return rc;

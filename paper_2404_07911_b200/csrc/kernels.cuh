@@ -1522,52 +1522,6 @@ __global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__re
   for (int l = tid; l < N3; l += TH) vb[l] = Rb[B::pad(l)];
 }
 
-// ======================================================= cut cells, p <= 3
-// One WARP per cut cell; lanes = quadrature points (the paper's vectorisation
-// over points, "combining the operations of several quadrature points of
-// an entity into the SIMD lanes").  Each lane accumulates the integration into
-// all n^3 <= 64 DoFs in registers (so the reduction over points never touches
-// shared memory); one butterfly reduce-scatter over the warp at the end.  Volume
-// and interface points form one stream (no partially filled round per kind).
-// The cell block and its six neighbour blocks are fetched with cp.async at
-// kernel entry, overlapping the point work.
-
-
-// Warp reduce-scatter of L per-lane partial sums (L a power of two <= 64).
-// Afterwards value j of lane l is the warp sum of entry idx(l, j) =
-// (l >> (5 - S)) * (L >> S) + j with S = min(log2 L, 5).
-template <int L, int O, int LEN>
-__device__ __forceinline__ void bfly_round(double (&a)[L], int lane) {
-  if constexpr (O >= 1) {
-    if constexpr (LEN > 1) {
-      constexpr int h = LEN / 2;
-      const bool up = (lane & O) != 0;
-#pragma unroll
-      for (int i = 0; i < h; ++i) {
-        const double send = up ? a[i] : a[i + h];
-        const double keep = up ? a[i + h] : a[i];
-        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
-      }
-      bfly_round<L, O / 2, h>(a, lane);
-    } else {
-      a[0] += __shfl_xor_sync(0xffffffffu, a[0], O);
-      bfly_round<L, O / 2, 1>(a, lane);
-    }
-  }
-}
-template <int L>
-__device__ __forceinline__ void butterfly(double (&a)[L], int lane) {
-  bfly_round<L, 16, L>(a, lane);
-}
-template <int L>
-struct BF {
-  static constexpr int S = (L >= 32) ? 5 : (L == 16 ? 4 : (L == 8 ? 3 : (L == 4 ? 2 : (L == 2 ? 1 : 0))));
-  static constexpr int LF = L >> S;  // values left per lane
-  __device__ static __forceinline__ int idx(int lane, int j) { return (lane >> (5 - S)) * LF + j; }
-  // lanes holding a duplicate of the same entry (full-reduce rounds) write only once
-  __device__ static __forceinline__ bool writer(int lane) { return (lane & ((1 << (5 - S)) - 1)) == 0; }
-};
-
 // ------------------------------------------------------------ helpers
 template <int V>
 struct IC {

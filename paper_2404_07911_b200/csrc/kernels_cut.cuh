@@ -1,4 +1,4 @@
-// k_cutp<N> (N = p+1 = 3, 4) and k_cut1<N> (N = 2, at the end of this file): the
+// k_cutp<N> (N = p+1 = 4) and k_cut1<N, TPC> (N = 2, 3, at the end of this file): the
 // unstructured terms of the cut cells (Alg. 1 "intersected" branch),
 // included by kernels.cuh.
 //
@@ -144,18 +144,6 @@ struct __align__(16) CPacket {
 #endif
 #ifndef CUTP_NB
 #define CUTP_NB 3  // packet ring depth
-#endif
-#ifndef CUTP_UNIFIED_MAXN
-#define CUTP_UNIFIED_MAXN 3  // n <= this: a chunk mixes every point kind and face axis
-#endif
-#ifndef CUTP_BFLY_MAXACC
-#define CUTP_BFLY_MAXACC 32  // accumulators <= this: shuffle reduce-scatter instead of the transpose
-#endif
-#ifndef CUTP_HYB
-#define CUTP_HYB 1
-#endif
-#ifndef CUTP_RW
-#define CUTP_RW 16  // rows of the reduction transpose buffer
 #endif
 #ifndef CUTP_FLINES
 #define CUTP_FLINES 1  // n = 4: cut-face points in lines (face_line_rt)
@@ -476,19 +464,13 @@ struct CutPCfg {
   static constexpr int PK = CUTP_PK;  // packet capacity in bytes (>= the largest chunk)
   // largest chunks: 32 interface rows (64 B), 32 volume lines with their interface point
   static_assert(PK >= 16 + 32 * 64 && PK >= 16 + 32 * 8 * (2 + 2 * N + 6), "CUTP_PK below the largest chunk");
+  static_assert(N == 4, "k_cutp serves n = 4 (n = 2, 3: k_cut1; n >= 5: k_cut)");
   static constexpr int NN = N * N, N3 = N * N * N, N3P = (N3 + 1) & ~1;
-  static constexpr int ACC = N == 4 ? 64 : (N == 3 ? 32 : 8);  // padded n^3 (power of two)
-  // one chunk stream per cell mixing volume, interface and cut-face points (any face
-  // axis: runtime-axis face update); else chunks are kind- and axis-homogeneous
-  static constexpr bool UNIFIED = N <= CUTP_UNIFIED_MAXN;
-  // not unified: the cut-face points of a cell still form ONE stream over all face axes
-  // (runtime-axis update)
-  static constexpr bool BFLY = ACC <= CUTP_BFLY_MAXACC;
-  // 64 accumulators: one butterfly level (xor 16) + a 16-lane shared-memory transpose
-  static constexpr bool HYB = !BFLY && ACC == 64 && CUTP_HYB;
+  static constexpr int ACC = 64;  // n^3 accumulators per lane
+  // the reduction: one butterfly level (xor 16) + a 16-lane shared-memory transpose
   // cut-face points in lines (face_line_rt; its per-lane axis slots live in the
   // reduction buffer, which is free until the cell's reduction)
-  static constexpr bool FLINES = N == 4 && HYB && CUTP_FLINES;
+  static constexpr bool FLINES = CUTP_FLINES;
   static_assert(!FLINES || 32 * (3 * N + 1) <= 32 * 17, "face-line slots exceed the reduction buffer");
   // bars(2 + NB) | UB[2][7][N3P] | JAB[6][2][NN] | ring[NB][2 + PK/8] (nch + packet)
   static constexpr int OFF_UB = (2 + NB + 1) & ~1;
@@ -496,12 +478,11 @@ struct CutPCfg {
   static constexpr int OFF_RING = OFF_JAB + ((6 * 2 * NN + 1) & ~1);
   static constexpr int RSLOT = 2 + PK / 8;
   static constexpr int OFF_WS = OFF_RING + NB * RSLOT;  // w of the structured faces (n^3)
-  static constexpr int OFF_RED = OFF_WS + ((N3 + 1) & ~1);  // reduction transpose [RW][33]
-  static constexpr int RW = ACC < CUTP_RW ? ACC : CUTP_RW;      // accumulators per reduction pass
+  static constexpr int OFF_RED = OFF_WS + ((N3 + 1) & ~1);  // reduction transpose [32][17]
   // the warp's next <= DG cell descriptors, staged by one coalesced load per group
   // (8: 640 B, what is left of the SM's shared memory at 8 warps per SM)
   static constexpr int DG = 8;
-  static constexpr int RED_SZ = BFLY ? 0 : (HYB ? 32 * 17 : RW * 33);
+  static constexpr int RED_SZ = 32 * 17;
   static constexpr int OFF_DSC = OFF_RED + RED_SZ;
   // the cell block in the line frame (vol_line_eval): inside the reduction buffer after
   // the face-line slots when it fits (both are free until the reduction), else its own
@@ -517,7 +498,6 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
                                               const CDesc2 *__restrict__ desc, const CPacket *__restrict__ packets,
                                               const char *__restrict__ stream, const int *__restrict__ wstart,
                                               const int *__restrict__ pstart, KParams kp, TileTab<N> tt) {
-  static_assert(2 * N * N <= 32, "k_cutp needs N <= 4");
   using C = CutPCfg<N>;
   using LN = BlkU<N>;
   constexpr int NN = C::NN, N3 = C::N3, N3P = C::N3P, NB = C::NB;
@@ -628,7 +608,7 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
     counts(cd, nv, ns, nf);
     // chunks of the cell: the first KL are volume lines
     // (lines never occur at n = 2: the host plans none, and the loop is compiled out)
-    const int K = (int)((uint32_t)cd.nchunk & 0xffffu), KL = N >= 3 ? (int)(((uint32_t)cd.nchunk >> 16) & 0xffu) : 0;
+    const int K = (int)((uint32_t)cd.nchunk & 0xffffu), KL = (int)(((uint32_t)cd.nchunk >> 16) & 0xffu);
     const int KF = C::FLINES ? (int)(((uint32_t)cd.nchunk >> 24) & 0xffu) : 0;  // cut-face line chunks
     const uint32_t fm = fmask_of(cd);
     // ---- this cell's blocks
@@ -788,7 +768,7 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
     // volume LINES first (their own loop: the point loop below keeps its code
     // generation): chunks of cv lines along axis (cnt >> 24) & 3, records of 2 + 2N doubles
     const double *UL = U;  // the block in the line frame (a copy when the lines are not along x)
-    for (int k = 0; k < (N >= 3 ? KL : 0); ++k) {
+    for (int k = 0; k < KL; ++k) {
       if (left == 0) next_packet();
       const int cnt = reinterpret_cast<const int *>(S + pos)[0];
       const int cv = cnt & 0xff, ax = (cnt >> 24) & 3;
@@ -905,28 +885,15 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
       __syncwarp();  // every lane is done with the ring slot before it is refilled
       if (lane == 0 && left == 0) fence_proxy_async();
     }
-    // ---- reduce over the warp and write the block (every cut cell block written once)
-    // padded shared-memory transpose, RW entries per pass: lane l < RW sums entry
-    // RW pass + l over the 32 lanes (fixed order)
+    // ---- reduce over the warp and write the block (every cut cell block written once):
+    // lanes l, l^16 exchange halves (xor 16): half h = lane >> 4 then holds entries
+    // 32 h + i summed over the pair; two passes transpose 16 of them over the 16 lanes
+    // of each half through shared memory, lane l summing entry 32 (l >> 4) + 16 ps + (l & 15)
+    // over the 16 lanes in a fixed order
     double *RED = base + C::OFF_RED;
     double *vb = v + (size_t)cd.blk * N3;
     const bool st_on = (gm | sm) != 0;
-    constexpr int RW = C::RW;
-    if constexpr (C::BFLY) {
-      // shuffle reduce-scatter (fixed order), then the writer lanes store
-      butterfly<C::ACC>(acc, lane);
-      if (BF<C::ACC>::writer(lane)) {
-#pragma unroll
-        for (int jj = 0; jj < BF<C::ACC>::LF; ++jj) {
-          const int l = BF<C::ACC>::idx(lane, jj);
-          if (l < N3) vb[l] = acc[jj] + (st_on ? WS[l] : 0.0);
-        }
-      }
-    }
-    if constexpr (C::HYB) {
-      // lanes l, l^16 exchange halves (xor 16): half h = lane >> 4 then holds entries
-      // 32 h + i summed over the pair; two passes transpose 16 of them over the 16 lanes
-      // of each half through shared memory, lane l summing entry 32 (l >> 4) + 16 ps + (l & 15)
+    {
       const bool up = (lane & 16) != 0;
       double a32[32];
 #pragma unroll
@@ -954,25 +921,6 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
         __syncwarp();
       }
     }
-#pragma unroll
-    for (int ps = 0; ps < ((C::BFLY || C::HYB) ? 0 : C::ACC / RW); ++ps) {
-#pragma unroll
-      for (int i = 0; i < RW; ++i) RED[i * 33 + lane] = acc[ps * RW + i];
-      __syncwarp();
-      const int l = ps * RW + lane;
-      if (lane < RW && l < N3) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 32; k += 4) {
-          s0 += RED[lane * 33 + k];
-          s1 += RED[lane * 33 + k + 1];
-          s2 += RED[lane * 33 + k + 2];
-          s3 += RED[lane * 33 + k + 3];
-        }
-        vb[l] = ((s0 + s1) + (s2 + s3)) + (st_on ? WS[l] : 0.0);
-      }
-      __syncwarp();
-    }
     if constexpr (!C::BULK) __syncwarp();
     if (has_next) cd = nd;
   }
@@ -981,12 +929,12 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
 }
 
 
-// ======================================================= cut cells, p = 1 (k_cut1)
-// One THREAD per cut cell (k_cell's layout for the uncut cells): at p = 1 a cut cell
-// has ~30 points and 8 DoFs, so a warp per cell (k_cutp) spends most of its time in
-// per-cell work done by a few lanes (traces, structured faces, the cross-lane
-// reduction); here 32 cells run side by side in SIMT and every accumulator is the
-// thread's own.  Cells come heavy-first in the descriptor list, so a warp's cells
+// ======================================================= cut cells, p = 1, 2 (k_cut1)
+// One THREAD (p = 1) or a thread PAIR (p = 2) per cut cell (k_cell's layout for the
+// uncut cells): at p = 1, 2 a cut cell has ~30 / ~85 points and 8 / 27 DoFs, so a warp
+// per cell (k_cutp) spends most of its time in per-cell work done by a few lanes
+// (traces, structured faces, the cross-lane reduction); here 32 / 16 cells run side by
+// side in SIMT and every accumulator is the thread's own.  Cells come heavy-first in the descriptor list, so a warp's cells
 // have similar point counts.  Per cell (all FP64, same formulas as k_cutp):
 //   1. structured faces (ghost penalty, full-face SIPG) in w-space with the
 //      M^-1-premultiplied line operators (k_cell), then w <- (M (x) M (x) M) w; acc = w
@@ -996,18 +944,31 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
 //      the 2-D interpolation and the flux coefficients summed per in-face node, then
 //      applied along the face normal (eq:unstructured_face P:489-496)
 // Neighbour values are read straight from global memory (L1 / L2 hits).
-template <int N>
+// TPC > 1: a cell on TPC consecutive lanes (k = lane % TPC): face F's structured part on
+// lane F % TPC, every TPC-th point of each kind on each lane, the cut faces' traces on
+// all of them; each lane applies M (x) M (x) M to its own structured part (linear), and
+// the TPC partial accumulators are summed by an xor butterfly (commutative: every lane
+// of the group gets the same bits); lane k writes the entries l = k mod TPC.
+template <int N, int TPC>
 __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, double *__restrict__ v,
                                               const CDesc *__restrict__ desc, int ncut,
                                               const double *__restrict__ vol_pts, const double *__restrict__ srf_pts,
                                               const double *__restrict__ sf_pts, const int64_t *__restrict__ sf_ptr,
                                               KParams kp, TileTab<N> tt) {
   constexpr int NN = N * N, N3 = NN * N;
+  static_assert(TPC >= 1 && TPC <= 32 && (32 % TPC) == 0, "TPC divides the warp");
   const RefTab &R = c_ref[N - 2];
   pdl_trigger();  // every CTA has begun -> the uncut-cell kernels may start
   if (blockIdx.x == 0 && threadIdx.x == 0) pdl_wait();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ncut) return;
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x, kk = gi % TPC;
+  const int i0 = gi / TPC;
+  if constexpr (TPC == 1) {
+    if (i0 >= ncut) return;
+  } else {
+    if (__all_sync(0xffffffffu, i0 >= ncut)) return;  // (the butterfly needs whole warps)
+  }
+  const bool valid = i0 < ncut;
+  const int i = valid ? i0 : ncut - 1;
   const CDesc d = desc[i];
   const bool cell_on = (kp.mask & TERM_CELL) != 0, sipg_on = (kp.mask & TERM_SIPG) != 0,
              nit_on = (kp.mask & TERM_NITSCHE) != 0, gp_on = (kp.mask & TERM_GP) != 0;
@@ -1025,7 +986,7 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
     constexpr int F = decltype(fc)::value, D = F / 2, SS = F % 2;
     const bool g = gp_on && d.nb[F] >= 0 && ((d.flags >> F) & 1u);
     const bool sp = sipg_on && d.nb[F] >= 0 && ((d.flags >> (6 + F)) & 1u);
-    if (!(g || sp)) return;
+    if (!(g || sp) || (F % TPC) != kk) return;
     any_st = true;
     const double *nbp = u + (size_t)d.nb[F] * N3;
 #pragma unroll
@@ -1150,22 +1111,30 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
       }
     }
   };
-  if (cell_on) {
-    const double *p = vol_pts + 4 * d.vb;
-    for (int q = 0; q < d.nv; ++q, p += 4) {
-      const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
-      const double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
-      point(a.x, a.y, b.x, b.y, false, 0.0, 0.0, 0.0);
+  if (cell_on && kk < d.nv) {
+    const double2 *p = reinterpret_cast<const double2 *>(vol_pts + 4 * d.vb);
+    double2 a = __ldg(p + 2 * kk), b = __ldg(p + 2 * kk + 1);
+    for (int q = kk; q < d.nv; q += TPC) {
+      const double2 ca = a, cb = b;
+      if (q + TPC < d.nv) {  // the next point's row in flight while this one is evaluated
+        a = __ldg(p + 2 * (q + TPC));
+        b = __ldg(p + 2 * (q + TPC) + 1);
+      }
+      point(ca.x, ca.y, cb.x, cb.y, false, 0.0, 0.0, 0.0);
     }
   }
-  if (nit_on) {
-    const double *p = srf_pts + 8 * d.sb;
-    for (int q = 0; q < d.ns; ++q, p += 8) {
-      const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
-      const double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
-      const double2 c = __ldg(reinterpret_cast<const double2 *>(p) + 2);
-      const double2 e = __ldg(reinterpret_cast<const double2 *>(p) + 3);
-      point(a.x, a.y, b.x, e.x, true, b.y, c.x, c.y);
+  if (nit_on && kk < d.ns) {
+    const double2 *p = reinterpret_cast<const double2 *>(srf_pts + 8 * d.sb);
+    double2 a = __ldg(p + 4 * kk), b = __ldg(p + 4 * kk + 1), c = __ldg(p + 4 * kk + 2), e = __ldg(p + 4 * kk + 3);
+    for (int q = kk; q < d.ns; q += TPC) {
+      const double2 ca = a, cb = b, cc = c, ce = e;
+      if (q + TPC < d.ns) {
+        a = __ldg(p + 4 * (q + TPC));
+        b = __ldg(p + 4 * (q + TPC) + 1);
+        c = __ldg(p + 4 * (q + TPC) + 2);
+        e = __ldg(p + 4 * (q + TPC) + 3);
+      }
+      point(ca.x, ca.y, cb.x, ce.x, true, cb.y, cc.x, cc.y);
     }
   }
   // ---- 4. cut faces
@@ -1189,9 +1158,18 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
       }
       const double sg = SS ? 1.0 : -1.0;
       const int64_t pb = sf_ptr[d.sf[F]], pe = sf_ptr[d.sf[F] + 1];
-      for (int64_t q = pb; q < pe; ++q) {
-        const double2 st = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * q));
-        const double W = __ldg(sf_pts + 4 * q + 2);
+      double2 nst = make_double2(0.5, 0.5), nw = make_double2(0.0, 0.0);
+      if (pb + kk < pe) {
+        nst = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * (pb + kk)));
+        nw = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * (pb + kk)) + 1);
+      }
+      for (int64_t q = pb + kk; q < pe; q += TPC) {
+        const double2 st = nst;
+        const double W = nw.x;
+        if (q + TPC < pe) {  // the next point's row in flight while this one is evaluated
+          nst = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * (q + TPC)));
+          nw = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * (q + TPC)) + 1);
+        }
         double ls[N], lt[N];
         basis_v_sym<N>(R, st.x, ls);
         basis_v_sym<N>(R, st.y, lt);
@@ -1225,7 +1203,15 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
       }
     });
   }
+  if constexpr (TPC > 1) {
+#pragma unroll
+    for (int o = 1; o < TPC; o <<= 1)
+#pragma unroll
+      for (int k = 0; k < N3; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+  }
+  if (!valid) return;
   double *vb = v + (size_t)d.blk * N3;
 #pragma unroll
-  for (int k = 0; k < N3; ++k) vb[k] = acc[k];
+  for (int k = 0; k < N3; ++k)
+    if (TPC == 1 || k % TPC == kk) vb[k] = acc[k];
 }
