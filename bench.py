@@ -414,7 +414,7 @@ def run_ours(args, P, cfg, rank, world, local_rank):
     elif n_ == 4:
         kname = {"structured": "k_tile2<4,0> + k_uncw<4,8>", "unstructured": "k_cutp<4>"}
     else:
-        kname = {"structured": f"k_uncw<{n_}>" if n_ in (5, 6, 8) else f"k_uncut<{n_}>", "unstructured": f"k_cut<{n_}>"}
+        kname = {"structured": f"k_uncw<{n_}>", "unstructured": f"k_cut<{n_}>"}
     dom = max(k_ms, key=k_ms.get)
     F_dom = work["F_uncut"] if dom == "structured" else work["F_cut"]
     B_dom = work["B_uncut"] if dom == "structured" else work["B_cut"]

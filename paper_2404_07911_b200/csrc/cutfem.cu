@@ -936,8 +936,8 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
   return 0;
 }
 
-// N = 5, 6: uncut cells through k_uncw (every structured term, GP included); cut
-// cells stay on k_cut.  (N = 7: one 121 KB tile per SM is slower than k_uncut.)
+// N = 5..9: uncut cells through k_uncw (every structured term, GP included); cut
+// cells stay on k_cut.
 template <int N>
 int setup_uncw(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<UDesc> &ud) {
   using C = TileCfg<N>;
@@ -988,9 +988,11 @@ int dispatch_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vecto
     case 4: return setup_tiles<4>(hd, pb, ud, cd);
     case 5: return setup_uncw<5>(hd, pb, ud);
     case 6: return setup_uncw<6>(hd, pb, ud);
-    // n = 8: k_uncw (measured faster than k_uncut); n = 7 (neutral) and n = 9 (slower:
-    // 140 KB of tile data, one CTA per SM) stay on k_uncut
+    // n = 5..9: k_uncw (pipelined tiles; odd n by 8-byte cp.async: C3 p=6 structured
+    // 323 -> 139 us, p=8 376 -> 195 us against round 1's warp-per-line k_uncut)
+    case 7: return setup_uncw<7>(hd, pb, ud);
     case 8: return setup_uncw<8>(hd, pb, ud);
+    case 9: return setup_uncw<9>(hd, pb, ud);
   }
   return 0;
 }
@@ -1110,7 +1112,6 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
   else {
   const int64_t np = (which & 1) ? hd->r_cnt[part][0] : 0, ng = (which & 1) ? hd->r_cnt[part][1] : 0;
   const int64_t nc = (which & 2) ? hd->r_cnt[part][2] : 0;
-  const UDesc *dp = hd->d_udesc + hd->r_off[part][0], *dg = hd->d_udesc + hd->r_off[part][1];
   const CDesc *dc = hd->d_cdesc + hd->r_off[part][2];
   const int64_t nu = np + ng;
   const bool fork = nc > 0 && nu > 0;
@@ -1142,18 +1143,9 @@ int launch(cutfem_handle *hd, const double *u, double *v, cudaStream_t st, int w
     }
     CU(cudaGetLastError());
   }
-  if (nu > 0 && hd->d_tiles) {
-    launch_uncw();  // n = 5, 6, 8
-  } else if (nu > 0) {  // n = 7, 9
-    using C = UncutCfg<N>;
-    const int per_block = C::WARPS * C::CPW;
-    if (np > 0)
-      k_uncut<N><<<(unsigned)((np + per_block - 1) / per_block), 32 * C::WARPS, C::SMEM, st>>>(u, v, dp, (int)np,
-                                                                                             hd->kp, hd->ft);
-    if (ng > 0)
-      k_uncut<N><<<(unsigned)((ng + per_block - 1) / per_block), 32 * C::WARPS, C::SMEM, st>>>(u, v, dg, (int)ng,
-                                                                                             hd->kp, hd->ft);
-    CU(cudaGetLastError());
+  if (nu > 0) {
+    if (!hd->d_tiles) return fail(CUTFEM_ECUDA, "uncut-cell tiles missing");
+    launch_uncw();  // n = 5..9
   }
   if (fork) {
     CU(cudaEventRecord(hd->ev_join, hd->side));
@@ -1167,8 +1159,6 @@ template <int N>
 int set_attrs() {
   if constexpr (N >= 5) {
     CU(cudaFuncSetAttribute(k_cut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CutCfg<N>::SMEM));
-    if constexpr (N == 7 || N == 9)
-      CU(cudaFuncSetAttribute(k_uncut<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, UncutCfg<N>::SMEM));
   }
   return 0;
 }

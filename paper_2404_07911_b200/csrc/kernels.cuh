@@ -7,9 +7,8 @@
 // side of the six faces (SIPG, ghost penalty, cut-face SIPG), reading the
 // neighbour blocks from L2.
 //
-//   k_uncut<N>: structured cells (Alg. 1 "inside" branch): a warp
-//     holds 32/N^2 cells, one lane per 1-D line; sum factorisation with the
-//     even-odd decomposition of every n x n line operator (S, K_c, S^T, M).
+//   structured cells (Alg. 1 "inside" branch): kernels_tile.cuh
+//     (k_tile2, k_uncw, k_cell);
 //   k_cut<N>:   unstructured cells (Alg. 1 "intersected" branch):
 //     one CTA per cut cell, one thread per quadrature point for the per-point
 //     tensor evaluation (eq:unstructured_cell), then a DoF-parallel
@@ -379,195 +378,6 @@ __device__ __forceinline__ void basis_v(const RefTab &R, double t, double (&v)[N
   for (int a = N - 1; a >= 0; --a) {
     v[a] = R.cinv[a] * pre[a] * s;
     s *= d[a];
-  }
-}
-
-// ============================================================ uncut cells
-template <int N>
-struct UncutCfg {
-  static constexpr int NN = N * N;
-  static constexpr int LPS = NN <= 32 ? NN : 32;  // lanes per cell slot
-  static constexpr int CPW = NN <= 32 ? 32 / NN : 1;  // cells per warp
-  static constexpr int WARPS = 4;
-  static constexpr int SLOT = 4 * Blk<N>::SZ + 2 * NN;  // U, Q/T, R, NB, FA, FB
-  static constexpr int SMEM = WARPS * CPW * SLOT * 8;
-};
-
-template <int N>
-__global__ void __launch_bounds__(128) k_uncut(const double *__restrict__ u, double *__restrict__ v,
-                                               const UDesc *__restrict__ desc, int ncell, KParams kp,
-                                               FaceTab ft) {
-  using B = Blk<N>;
-  using C = UncutCfg<N>;
-  constexpr int NN = B::NN, N3 = B::N3, SZ = B::SZ, LPS = C::LPS;
-  const RefTab &R = c_ref[N - 2];
-  extern __shared__ double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot = lane / LPS, t0 = lane % LPS;
-  const int cell = (blockIdx.x * C::WARPS + warp) * C::CPW + slot;
-  const bool valid = slot < C::CPW && cell < ncell;
-  double *base = smem + (warp * C::CPW + (slot < C::CPW ? slot : 0)) * C::SLOT;
-  double *U = base, *Q = base + SZ, *Rb = base + 2 * SZ, *NB = base + 3 * SZ;
-  double *FA = base + 4 * SZ, *FB = FA + NN;
-  double *T = Q;
-
-  UDesc dsc;
-  if (valid) dsc = desc[cell];
-  else dsc.blk = -1;
-  if (valid) {
-    const double *ub = u + (size_t)dsc.blk * N3;
-    for (int l = t0; l < N3; l += LPS) U[B::pad(l)] = __ldg(ub + l);
-  }
-  __syncwarp();
-  const double h = kp.h;
-  if (kp.mask & TERM_CELL) {
-    // E: GLL -> Gauss values (S in x, y, z)
-    if (valid)
-      for (int t = t0; t < NN; t += LPS) {
-        int b0, st;
-        B::line(0, t, b0, st);
-        sweep_line<N, 0>(U, Q, b0, st, R.S, 1.0);
-      }
-    __syncwarp();
-#pragma unroll
-    for (int d = 1; d < 3; ++d) {
-      if (valid)
-        for (int t = t0; t < NN; t += LPS) {
-          int b0, st;
-          B::line(d, t, b0, st);
-          sweep_line<N, 0>(Q, Q, b0, st, R.S, 1.0);
-        }
-      __syncwarp();
-    }
-    // B: per direction collocation derivative, quadrature weight h*w*w*w and
-    // transposed derivative folded into K_c = D^T W D (Cartesian metric)
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      if (valid)
-        for (int t = t0; t < NN; t += LPS) {
-          int b0, st;
-          B::line(d, t, b0, st);
-          const double s = h * R.gw[t % N] * R.gw[t / N];
-          if (d == 0) sweep_line<N, 2>(Q, Rb, b0, st, R.Kc, s);
-          else sweep_line<N, 1>(Q, Rb, b0, st, R.Kc, s);
-        }
-      __syncwarp();
-    }
-    // I: Gauss -> GLL (S^T in x, y, z)
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      if (valid)
-        for (int t = t0; t < NN; t += LPS) {
-          int b0, st;
-          B::line(d, t, b0, st);
-          sweep_line<N, 0>(Rb, Rb, b0, st, R.St, 1.0);
-        }
-      __syncwarp();
-    }
-  } else {
-    if (valid)
-      for (int l = t0; l < SZ; l += LPS) Rb[l] = 0.0;
-    __syncwarp();
-  }
-
-  // ---- faces (element-centric, own side only)
-  const double h2 = h * h;
-  for (int f = 0; f < 6; ++f) {
-    const int nbk = valid ? dsc.nb[f] : -1;
-    const bool gp = nbk >= 0 && ((dsc.flags >> f) & 1u) && (kp.mask & TERM_GP);
-    const bool sipg = nbk >= 0 && (kp.mask & TERM_SIPG);
-    const bool doit = gp || sipg;
-    if (doit) {
-      const double *nbp = u + (size_t)nbk * N3;
-      for (int l = t0; l < N3; l += LPS) NB[B::pad(l)] = __ldg(nbp + l);
-    }
-    __syncwarp();
-    const int dd = f >> 1, side = f & 1;
-    const int fo = side ? N - 1 : 0, fn = side ? 0 : N - 1;
-    const double sg = side ? 1.0 : -1.0;
-    const double *dow = side ? R.d1 : R.d0;
-    const double *dnb = side ? R.d0 : R.d1;
-    const double *Goo = ft.Goo[side ? 0 : 1];
-    const double *Gon = ft.Gon[side ? 0 : 1];
-    if (doit)
-      for (int t = t0; t < NN; t += LPS) {
-        int b0, st;
-        B::line(dd, t, b0, st);
-        double uo[N], un[N];
-#pragma unroll
-        for (int m = 0; m < N; ++m) {
-          uo[m] = U[b0 + m * st];
-          un[m] = NB[b0 + m * st];
-        }
-        const double J0 = uo[fo] - un[fn];
-        double A = 0.0;
-#pragma unroll
-        for (int m = 0; m < N; ++m) A = fma(dow[m], uo[m], fma(dnb[m], un[m], A));
-        const double F1 = sipg ? h2 * (kp.sigma * J0 - sg * A * kp.i2h) : 0.0;
-        const double F2 = sipg ? -0.5 * h * sg * J0 : 0.0;
-        if (gp) {
-#pragma unroll
-          for (int m = 0; m < N; ++m) {
-            double F = 0.0;
-#pragma unroll
-            for (int a = 0; a < N; ++a) F = fma(Goo[m * N + a], uo[a], fma(-Gon[m * N + a], un[a], F));
-            F = fma(dow[m], F2, F);
-            if (m == fo) F += F1;
-            T[b0 + m * st] = F;
-          }
-        } else {
-          FA[t] = F1;
-          FB[t] = F2;
-        }
-      }
-    __syncwarp();
-    // in-face mass M (x) M (reference; h^2 already folded into F)
-    const int e1 = (dd == 0) ? 1 : 0, e2 = (dd == 2) ? 1 : 2;
-    if (gp) {
-      for (int t = t0; t < NN; t += LPS) {
-        int b0, st;
-        B::line(e1, t, b0, st);
-        sweep_line<N, 0>(T, T, b0, st, R.M, 1.0);
-      }
-    } else if (doit) {
-      for (int k = t0; k < 2 * N; k += LPS) {
-        double *F = (k < N) ? FA : FB;
-        sweep_line<N, 0>(F, F, (k % N) * N, 1, R.M, 1.0);
-      }
-    }
-    __syncwarp();
-    if (gp) {
-      for (int t = t0; t < NN; t += LPS) {
-        int b0, st;
-        B::line(e2, t, b0, st);
-        sweep_line<N, 0>(T, T, b0, st, R.M, 1.0);
-      }
-    } else if (doit) {
-      for (int k = t0; k < 2 * N; k += LPS) {
-        double *F = (k < N) ? FA : FB;
-        sweep_line<N, 0>(F, F, k % N, N, R.M, 1.0);
-      }
-    }
-    __syncwarp();
-    if (doit)
-      for (int t = t0; t < NN; t += LPS) {
-        int b0, st;
-        B::line(dd, t, b0, st);
-        if (gp) {
-#pragma unroll
-          for (int m = 0; m < N; ++m) Rb[b0 + m * st] += T[b0 + m * st];
-        } else {
-          const double fa = FA[t], fb = FB[t];
-#pragma unroll
-          for (int m = 0; m < N; ++m) Rb[b0 + m * st] = fma(dow[m], fb, Rb[b0 + m * st]);
-          Rb[b0 + fo * st] += fa;
-        }
-      }
-    __syncwarp();
-  }
-  if (valid) {
-    double *vb = v + (size_t)dsc.blk * N3;
-    for (int l = t0; l < N3; l += LPS) vb[l] = Rb[B::pad(l)];
   }
 }
 

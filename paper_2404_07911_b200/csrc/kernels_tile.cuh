@@ -839,24 +839,32 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
     __syncthreads();
     for (int sl = tid; sl < ns; sl += C::THREADS) bulk_g2s(S + sl * ST, u + (size_t)Tn->blk[sl] * N3, N3 * 8, bar);
   };
+  // odd n (blocks not a 16-byte multiple): the same pipeline with 8-byte cp.async
+  // (every slot entry in flight at once, one wait_group per tile)
+  auto issue_async = [&](int tl) {
+    const TileRec<TC_::SMAX> *Tn = tiles + tl;
+    const int ns = Tn->nslot;
+    __syncthreads();  // every thread is done reading the slots
+    for (int e = tid; e < ns * N3; e += C::THREADS) {
+      const int sl = e / N3, l = e - sl * N3;
+      cp_async8(S + sl * ST + l, u + (size_t)Tn->blk[sl] * N3 + l);
+    }
+    cp_async_commit();
+  };
   if constexpr (TC_::BULK) {
     if ((int)blockIdx.x < ntiles) issue(blockIdx.x);
+  } else {
+    if ((int)blockIdx.x < ntiles) issue_async(blockIdx.x);
   }
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const TileRec<TC_::SMAX> *T = tiles + tile;
-    const int nslot = T->nslot, ncell = T->ncell;
+    const int ncell = T->ncell;
     const bool on = cell < ncell;
     const uint2 ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[on ? cell : 0][0]);
-    // ---- the tile's blocks (bulk: issued during the previous tile)
-    if constexpr (!TC_::BULK) {
-      __syncthreads();
-      for (int sl = 0; sl < nslot; ++sl) {
-        const double *src = u + (size_t)T->blk[sl] * N3;
-        for (int l = tid; l < N3; l += C::THREADS) S[sl * ST + l] = __ldg(src + l);
-      }
-    }
+    // ---- the tile's blocks (issued during the previous tile)
     double *W = Wb + (on ? cell : 0) * WST;  // (axis 0 stores, the other axes accumulate)
     if constexpr (TC_::BULK) mbar_wait(bar, it & 1);
+    else cp_async_wait<0>();
     __syncthreads();
     int nbs[6];
 #pragma unroll
@@ -949,8 +957,9 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
       }
       __syncwarp();  // the next axis updates other threads' positions
     });
-    if constexpr (TC_::BULK) {
-      if (tile + (int)gridDim.x < ntiles) issue(tile + (int)gridDim.x);
+    if (tile + (int)gridDim.x < ntiles) {
+      if constexpr (TC_::BULK) issue(tile + (int)gridDim.x);
+      else issue_async(tile + (int)gridDim.x);
     }
     // ---- v = (M (x) M (x) M) w, sweeps in shared memory
     static_for<0, 3>([&](auto dc) {

@@ -1,7 +1,6 @@
 """Small applies through every kernel family, for compute-sanitizer (racecheck /
-synccheck / memcheck): p = 1, 2 (k_cutp<2,3>, k_cell), p = 3 (k_cutp<4>, k_tile2,
-k_uncw<4>), p = 4, 5 (k_cut, k_uncw), p = 6 (k_cut<7>, k_uncut<7>), p = 7 (k_uncw<8>),
-p = 8 (k_cut<9>, k_uncut<9>), the H1 gather / scatter and a Jacobi-PCG step.
+synccheck / memcheck): p = 1, 2 (k_cut1, k_cell), p = 3 (k_cutp<4>, k_tile2,
+k_uncw<4>), p = 4..8 (k_cut, k_uncw), the H1 gather / scatter and a Jacobi-PCG step.
 usage: python tools/sanitize_cases.py"""
 import os
 import sys
