@@ -46,7 +46,8 @@ def test_sass_is_sm100a_and_atomic_free():
     out = subprocess.run(["cuobjdump", "-sass", m.build()], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     funcs = re.split(r"\n\s*Function : ", out)
-    hot = [f for f in funcs if re.match(r"_Z\d+k_(uncut|cut|tile|gpw|cell)", f)]
-    assert len(hot) >= 16
+    hot = [f for f in funcs if re.match(r"_Z\d+k_(uncw|cut|tile|cell)", f)]
+    # k_cut1<2,3>, k_cell<2,3>, k_cutp<4>, k_tile2<4>, k_uncw<4..9>, k_cut<5..9>
+    assert len(hot) >= 17
     for f in hot:
         assert not re.search(r"\b(ATOM|ATOMS|ATOMG|RED)\b", f), f.split("\n")[0]
