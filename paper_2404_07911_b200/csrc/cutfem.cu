@@ -1617,8 +1617,11 @@ int setup_impl(const cutfem_problem *pb, int device, cutfem_handle *hd, int64_t 
   s.n_ext_dofs = na * n * n * n;
   s.degree = p;
   s.device = device;
-  s.launches_per_apply = hd->d_tiles ? (hd->n_cut > 0) + (hd->t_cnt[0][0] > 0) + (hd->t_cnt[1][0] > 0)
-                                     : (hd->n_cut > 0) + (hd->n_plain > 0) + (hd->n_uncut - hd->n_plain > 0);
+  // kernels per apply (single-GPU handle): the cut-cell kernel, then n <= 3 one k_cell
+  // launch, n = 4 k_tile2 and / or k_uncw<4,8>, n >= 5 one k_uncw launch
+  s.launches_per_apply = (hd->n_cut > 0) + (hd->n <= 3 ? (hd->n_uncut > 0)
+                                            : hd->n == 4 ? (hd->t_cnt[0][0] > 0) + (hd->t_cnt[1][0] > 0)
+                                                         : (hd->n_uncut > 0));
   return 0;
 }
 
