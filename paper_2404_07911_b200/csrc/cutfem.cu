@@ -95,7 +95,7 @@ struct cutfem_handle {
   // thread-per-cell structured kernel (N <= 4): warp-tiles per part (0 all, 1 interior, 2 boundary)
   // tile sets: [0] uncut cells, volume + SIPG (v = ...); [1] cells with ghost-
   // penalty faces (cut cells and their uncut neighbours) + the cut cells'
-  // full-face SIPG (v += ..., k_gpw)
+  // full-face SIPG
   void *d_tiles = nullptr;
   int64_t t_off[3][3] = {{0}}, t_cnt[3][3] = {{0}};
   int occ_tile[3] = {1, 1, 1};
@@ -532,34 +532,15 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
         c.gp = d.flags & nbm & 0x3fu;
         c.sipg = nbm;  // faces of an uncut cell are inside the domain: full SIPG
         c.vol = true;
-#if STRUCT4_GPW
-        if (c.gp) {
-          TCell g = c;
-          g.sipg = 0;
-          g.vol = false;
-          set[1][pt - 1].push_back(g);
-        }
-        c.gp = 0;
-        set[0][pt - 1].push_back(c);
-#else
-#ifdef UNCW4_ALL
-        set[1][pt - 1].push_back(c);
-#else
         // k_tile2 (folded operators) takes the cells with all six faces and no ghost
         // penalty; the rest (next to cut cells, on the box boundary) go to k_uncw<4>
         set[(c.gp || nbm != 0x3fu) ? 1 : 0][pt - 1].push_back(c);
-#endif
-#endif
       }
 
   }
   // set 0: k_tile2 tiles (Tile2Cfg<4>::T); set 1: k_uncw<4> tiles (TileCfg<4>).
   // Offsets are in BYTES.
-#if STRUCT4_GPW
-  using CG = typename GpwCfg<N>::T;
-#else
   using CG = typename std::conditional<N == 4, TileCfgX<N, UNCW4_TC>, C>::type;
-#endif
   using CK = typename std::conditional<N == 4, typename Tile2Cfg<4>::T, C>::type;
   std::vector<char> all;
   // (n <= 3: the uncut cells run k_cell from their descriptors; no tiles)
@@ -922,15 +903,9 @@ int setup_tiles(cutfem_handle *hd, const cutfem_problem *pb, const std::vector<U
     using C2 = Tile2Cfg<N>;
     CU(cudaFuncSetAttribute(k_tile2<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[0], k_tile2<N, 0>, C2::THREADS, C2::SMEM));
-#if STRUCT4_GPW
-    CU(cudaFuncSetAttribute(k_gpw<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, GpwCfg<N>::SMEM));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_gpw<N>, GpwCfg<N>::THREADS,
-                                                     GpwCfg<N>::SMEM));
-#else
     using CU4 = UncwCfg<N, UNCW4_TC>;
     CU(cudaFuncSetAttribute(k_uncw<N, UNCW4_TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, CU4::SMEM));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hd->occ_tile[1], k_uncw<N, UNCW4_TC>, CU4::THREADS, CU4::SMEM));
-#endif
   }
   for (int k = 0; k < 3; ++k) hd->occ_tile[k] = std::max(1, hd->occ_tile[k]);
   return 0;
@@ -1064,19 +1039,6 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
                                     (int)ng, tt, hd->kp.mask)))
       return rc;
   } else {
-#ifdef CUTFEM_UNCW_FIRST
-    if (n1 > 0) {  // cells next to cut cells: volume + SIPG + ghost penalty
-      const unsigned grid = (unsigned)std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count);
-      const auto *t1 = reinterpret_cast<const TileRec<TileCfgX<NT, UNCW4_TC>::SMAX> *>(tb + hd->t_off[1][part]);
-      if ((rc = launch_k(k_uncw<NT, UNCW4_TC>, grid, UncwCfg<NT, UNCW4_TC>::THREADS, UncwCfg<NT, UNCW4_TC>::SMEM, st,
-                         pdl, u, v, t1, (int)n1, tt, hd->kp.mask)))
-        return rc;
-      pdl = true;
-    }
-    const int64_t n1x = 0;
-#else
-    const int64_t n1x = n1;
-#endif
     if (n0 > 0) {  // cells without ghost-penalty faces: volume + SIPG
       const unsigned grid = (unsigned)std::min<int64_t>(n0, (int64_t)hd->occ_tile[0] * hd->sm_count);
       const auto *t0 = reinterpret_cast<const TileRec<Tile2Cfg<NT>::SMAX> *>(tb + hd->t_off[0][part]);
@@ -1085,19 +1047,12 @@ int launch_tiles(cutfem_handle *hd, const double *u, double *v, cudaStream_t st,
         return rc;
       pdl = true;
     }
-    if (n1x > 0) {  // cells next to cut cells: volume + SIPG + ghost penalty
+    if (n1 > 0) {  // cells next to cut cells: volume + SIPG + ghost penalty
       const unsigned grid = (unsigned)std::min<int64_t>(n1, (int64_t)hd->occ_tile[1] * hd->sm_count);
-#if STRUCT4_GPW
-      const auto *t1 = reinterpret_cast<const TileRec<GpwCfg<NT>::SMAX> *>(tb + hd->t_off[1][part]);
-      if ((rc = launch_k(k_gpw<NT>, grid, GpwCfg<NT>::THREADS, GpwCfg<NT>::SMEM, st, pdl, u, v, t1, (int)n1, tt,
-                         hd->kp.mask)))
-        return rc;
-#else
       const auto *t1 = reinterpret_cast<const TileRec<TileCfgX<NT, UNCW4_TC>::SMAX> *>(tb + hd->t_off[1][part]);
       if ((rc = launch_k(k_uncw<NT, UNCW4_TC>, grid, UncwCfg<NT, UNCW4_TC>::THREADS, UncwCfg<NT, UNCW4_TC>::SMEM, st,
                          pdl, u, v, t1, (int)n1, tt, hd->kp.mask)))
         return rc;
-#endif
     }
   }
   return 0;

@@ -41,13 +41,6 @@
 #define TILE8_SMAX 36  // slots of an 8-cell tile (a full 2x2x2 brick needs 32; merged partial bricks
                        // more; 32 measured: k_uncw<6> 3 CTAs/SM instead of 2, same time)
 #endif
-#ifndef STRUCT4_GPW
-#define STRUCT4_GPW 0  // n = 4 uncut cells: 0 = k_tile2 (plain cells) + k_uncw<4> (cells next to cut
-                       // cells); 1 = k_tile2 (all, volume + SIPG) then k_gpw (+ ghost penalty)
-#endif
-#ifndef GPW_TC4
-#define GPW_TC4 8
-#endif
 #ifndef UNCW4_TC
 #define UNCW4_TC 8  // cells per k_uncw<4> tile (the cells next to cut cells at n = 4)
 #endif
@@ -585,209 +578,6 @@ __global__ void __launch_bounds__(64, T2MINB) k_tile2(const double *__restrict__
   TL_END(1);
   if (blockIdx.x == 0) pdl_wait();  // complete only after the primary (k_cutp) has
 }
-
-#if STRUCT4_GPW
-// ===================================================================== k_gpw
-// k_gpw<N> (N <= 4): ghost penalty of every cell next to a cut cell plus the
-// full-face SIPG of the cut cells (their faces shared with uncut cells),
-// v += result.  Runs after k_tile*<0> and k_cutp have written v.
-// Same w-space arithmetic as k_tile2 (w += M^{-1}-premultiplied line operators,
-// v += (M (x) M (x) M) w), organised for SMALL CODE: 4 threads per cell, each
-// taking every 4th line of a face in a runtime loop, the accumulator w in
-// shared memory (disjoint lines per thread within one axis; a __syncwarp between
-// axes), faces unrolled only over their 6 (axis, side) variants so the line
-// operators stay warp-uniform constant-bank operands.
-template <int N>
-struct GpwCfg {
-  // small tiles: ~one tile per CTA is in flight, so shorter tiles mean a shorter kernel
-  static constexpr int TC = N == 4 ? GPW_TC4 : (N == 3 ? 16 : 32);
-  using T = TileCfgX<N, TC>;
-  static constexpr bool BULK = T::BULK;
-  static constexpr int N3 = N * N * N, ST = T::ST, SMAX = T::SMAX;
-  static constexpr int WST = N3 + 2;  // w row stride (doubles): consecutive cells on different banks
-  static constexpr int THREADS = 128;
-  static constexpr int TPC = THREADS / TC;  // threads per cell
-  static constexpr int CPW = TC / 4;        // cells per warp in the write-back
-  static constexpr int SMEM = 16 + SMAX * ST * 8 + TC * WST * 8;
-};
-
-template <int N>
-__global__ void __launch_bounds__(128) k_gpw(const double *__restrict__ u, double *__restrict__ v,
-                                             const TileRec<GpwCfg<N>::SMAX> *__restrict__ tiles, int ntiles,
-                                             TileTab<N> tt, uint32_t mask) {
-  using C = GpwCfg<N>;
-  constexpr int NN = N * N, N3 = C::N3, ST = C::ST, WST = C::WST;
-  extern __shared__ __align__(16) double smem[];
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-  double *S = smem + 2;
-  double *Wb = S + C::SMAX * ST;
-  constexpr int TPC = C::TPC, CPW = C::CPW;
-  const int tid = threadIdx.x, cell = tid / TPC, r = tid % TPC;
-  const bool sipg_on = (mask & TERM_SIPG) != 0, gp_on = (mask & TERM_GP) != 0;
-  pdl_trigger();
-  pdl_wait();  // v += ...: k_tile2 (the primary) must have written v
-  if (C::BULK && tid == 0) {
-    mbar_init(bar, 1);
-    mbar_fence_init();
-  }
-  TL_BEGIN(2);
-  __syncthreads();
-  uint32_t it = 0;
-  const int wrp = tid >> 5, ln32 = tid & 31;
-  constexpr int PER = (N3 + 31) / 32;  // elements of a block per lane in the write-back
-  // tile record fields, prefetched one tile ahead
-  int nx_nslot = 0, nx_ncell = 0, nx_bl = 0;
-  uint2 nx_ln = make_uint2(0, 0);
-  auto fetch = [&](int tl) {
-    const TileRec<C::SMAX> *T = tiles + tl;
-    nx_nslot = T->nslot;
-    nx_ncell = T->ncell;
-    nx_ln = *reinterpret_cast<const uint2 *>(&T->lane_nb[cell][0]);
-    nx_bl = (ln32 < CPW && CPW * wrp + ln32 < nx_ncell) ? T->blk[CPW * wrp + ln32] : 0;
-  };
-  if ((int)blockIdx.x < ntiles) fetch(blockIdx.x);
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const TileRec<C::SMAX> *T = tiles + tile;
-    const int nslot = nx_nslot, ncell = nx_ncell, bl = nx_bl;
-    const bool on = cell < ncell;
-    const uint2 ln = nx_ln;
-    // the v rows this warp adds to, loaded now and consumed at the end of the tile
-    double xv[CPW][PER];
-    size_t o[CPW];
-#pragma unroll
-    for (int c = 0; c < CPW; ++c) {
-      o[c] = (size_t)__shfl_sync(0xffffffffu, bl, c) * N3;
-      const bool cv = CPW * wrp + c < ncell;
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const int l = ln32 + 32 * k;
-        xv[c][k] = (cv && l < N3) ? v[o[c] + l] : 0.0;
-      }
-    }
-    // ---- stage the tile's blocks
-    if constexpr (C::BULK) {
-      fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) mbar_expect_tx(bar, (uint32_t)(nslot * N3 * 8));
-      __syncthreads();
-      for (int s = tid; s < nslot; s += C::THREADS) bulk_g2s(S + s * ST, u + (size_t)T->blk[s] * N3, N3 * 8, bar);
-    } else {
-      __syncthreads();
-      for (int e = tid; e < nslot * N3; e += C::THREADS) {
-        const int s = e / N3, l = e - s * N3;
-        S[s * ST + l] = __ldg(u + (size_t)T->blk[s] * N3 + l);
-      }
-    }
-    double *W = Wb + cell * WST;
-    for (int l = r; l < N3; l += TPC) W[l] = 0.0;
-    if (tile + (int)gridDim.x < ntiles) fetch(tile + gridDim.x);
-    if constexpr (C::BULK) mbar_wait(bar, it & 1);
-    __syncthreads();
-    int nbs[6];
-#pragma unroll
-    for (int f = 0; f < 4; ++f) nbs[f] = (ln.x >> (8 * f)) & 0xff;
-    nbs[4] = ln.y & 0xff;
-    nbs[5] = (ln.y >> 8) & 0xff;
-    const uint32_t gpb = (on && gp_on) ? (ln.y >> 16) & 0x3fu : 0u;
-    const uint32_t spb = (on && sipg_on) ? (ln.y >> 24) & 0x3fu : 0u;
-    const double *Us = S + (on ? cell : 0) * ST;
-    static_for<0, 6>([&](auto fc) {
-      constexpr int F = decltype(fc)::value, D = F / 2, SS = F % 2;
-      constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
-      const bool g = (gpb >> F) & 1u, sp = (spb >> F) & 1u;
-      const bool anyg = __any_sync(0xffffffffu, g), anys = __any_sync(0xffffffffu, sp);
-      if (anyg || anys) {
-        const double eg = g ? 1.0 : 0.0, es = sp ? 1.0 : 0.0;
-        const double *Nf = (g || sp) ? S + nbs[F] * ST : Us;
-#pragma unroll 1
-        for (int t = r; t < NN; t += TPC) {
-          const int t0 = t % N, t1 = t / N;
-          const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
-          double uo[N], un[N], out[N];
-#pragma unroll
-          for (int m = 0; m < N; ++m) {
-            uo[m] = Us[b0 + m * str];
-            un[m] = Nf[b0 + m * str];
-            out[m] = 0.0;
-          }
-          if (anyg) {
-#pragma unroll
-            for (int m = 0; m < N; ++m) {
-              double x = 0.0;
-#pragma unroll
-              for (int a = 0; a < N; ++a) {
-                const int k = SS ? (N - 1 - m) * N + (N - 1 - a) : m * N + a;
-                x = fma(tt.Goo[k], uo[a], fma(tt.Gon[k], un[a], x));
-              }
-              out[m] = eg * x;
-            }
-          }
-          if (anys) {
-            double A0 = 0.0, A1 = 0.0;
-#pragma unroll
-            for (int m = 0; m < N; ++m) {
-              if (SS == 0) {
-                A0 = fma(tt.d0[m], uo[m], A0);
-                A1 = fma(-tt.d0[N - 1 - m], un[m], A1);
-              } else {
-                A0 = fma(-tt.d0[N - 1 - m], uo[m], A0);
-                A1 = fma(tt.d0[m], un[m], A1);
-              }
-            }
-            const double J = es * (SS ? (uo[N - 1] - un[0]) : (uo[0] - un[N - 1]));
-            const double A = es * (A0 + A1);
-#pragma unroll
-            for (int m = 0; m < N; ++m) {
-              if (SS == 0) out[m] = fma(tt.cJ[m], J, fma(tt.cA[m], A, out[m]));
-              else out[m] = fma(tt.cJ[N - 1 - m], J, fma(-tt.cA[N - 1 - m], A, out[m]));
-            }
-          }
-#pragma unroll
-          for (int m = 0; m < N; ++m) W[b0 + m * str] += out[m];
-        }
-      }
-      if (SS == 1) __syncwarp();  // the next axis updates other threads' positions
-    });
-    // ---- v += (M (x) M (x) M) w, sweeps in shared memory
-    static_for<0, 3>([&](auto dc) {
-      constexpr int D = decltype(dc)::value;
-      constexpr int str = D == 0 ? 1 : (D == 1 ? N : NN);
-#pragma unroll 1
-      for (int t = r; t < NN; t += TPC) {
-        const int t0 = t % N, t1 = t / N;
-        const int b0 = D == 0 ? N * t0 + NN * t1 : (D == 1 ? t0 + NN * t1 : t0 + N * t1);
-        double x[N], y[N];
-#pragma unroll
-        for (int m = 0; m < N; ++m) x[m] = W[b0 + m * str];
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-          double s = 0.0;
-#pragma unroll
-          for (int j = 0; j < N; ++j) s = fma(tt.M[csym<N>(i * N + j)], x[j], s);
-          y[i] = s;
-        }
-#pragma unroll
-        for (int m = 0; m < N; ++m) W[b0 + m * str] = y[m];
-      }
-      __syncwarp();
-    });
-    __syncthreads();  // all w final
-    // ---- v += w (the warp's 8 cells; v rows were loaded at the start of the tile)
-#pragma unroll
-    for (int c = 0; c < CPW; ++c) {
-      const bool cv = CPW * wrp + c < ncell;
-#pragma unroll
-      for (int k = 0; k < PER; ++k) {
-        const int l = ln32 + 32 * k;
-        if (cv && l < N3) v[o[c] + l] = xv[c][k] + Wb[(CPW * wrp + c) * WST + l];
-      }
-    }
-  }
-  TL_END(2);
-}
-
-
-#endif
 
 // ===================================================================== k_uncw
 // k_uncw<N> (N = 5..9): uncut cells at high degree, every structured term (volume,
