@@ -978,6 +978,17 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
 #pragma unroll
     for (int k = 0; k < N3; ++k) uo[k] = __ldg(ub + k);
   }
+  // n = 3: the cut faces' point ranges requested now (consumed in step 4, so the dependent
+  // loads stay off that step's critical path; C3 p=2 apply 213 -> 210 us).  n = 2: at the
+  // face (the 24 extra registers cost k_cell's co-running warps more: 120 -> 124 us)
+  constexpr bool HOIST = N >= 3;
+  int64_t fpb[6], fpe[6];
+#pragma unroll
+  for (int F = 0; F < 6; ++F) {
+    const bool cf = HOIST && sipg_on && d.nb[F] >= 0 && ((d.flags >> (12 + F)) & 1u);
+    fpb[F] = cf ? __ldg(sf_ptr + d.sf[F]) : 0;
+    fpe[F] = cf ? __ldg(sf_ptr + d.sf[F] + 1) : 0;
+  }
   // ---- 1. structured faces in w-space
 #pragma unroll
   for (int l = 0; l < N3; ++l) acc[l] = 0.0;
@@ -1157,7 +1168,7 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
         F1[t] = F2[t] = 0.0;
       }
       const double sg = SS ? 1.0 : -1.0;
-      const int64_t pb = sf_ptr[d.sf[F]], pe = sf_ptr[d.sf[F] + 1];
+      const int64_t pb = HOIST ? fpb[F] : sf_ptr[d.sf[F]], pe = HOIST ? fpe[F] : sf_ptr[d.sf[F] + 1];
       double2 nst = make_double2(0.5, 0.5), nw = make_double2(0.0, 0.0);
       if (pb + kk < pe) {
         nst = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * (pb + kk)));
