@@ -143,6 +143,16 @@ int cutfem_apply_kernel(cutfem_handle *hd, int which, const double *u_dev, doubl
  * blocks of a distributed handle (n_ext_dofs), which the halo exchange fills. */
 int cutfem_apply_host(cutfem_handle *hd, const double *u_host, double *v_host, void *cuda_stream);
 
+/* Batch of independent applies with HOST buffers, pipelined: v_k = A u_k for
+ * k = 0..nbatch-1, u_host[k] / v_host[k] host pointers to n_dofs doubles each
+ * (page-locked memory lets the copies run asynchronously; the same pointer may repeat).
+ * Two device buffer pairs: the host->device copy of u_{k+1} (copy stream) and the
+ * device->host copy of v_{k-1} (second copy stream) overlap the apply of u_k (cuda_stream);
+ * every u_k is copied in and every v_k copied out.  Returns when all v_k are in host
+ * memory.  Single-GPU handles only (CUTFEM_EUNSUPPORTED on distributed ones). */
+int cutfem_apply_host_batch(cutfem_handle *hd, const double *const *u_host, double *const *v_host, int64_t nbatch,
+                            void *cuda_stream);
+
 /* Sparse-matrix comparison path (P:224-227 eq:matrixbasedop).
  * cutfem_csr_assemble builds the global CSR matrix ON THE DEVICE from the same
  * operator by probing (local matrices column by column through unit vectors,

@@ -79,7 +79,8 @@ class Stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
-EXPORTS = ["cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_host", "cutfem_csr_assemble",
+EXPORTS = ["cutfem_setup", "cutfem_apply", "cutfem_apply_kernel", "cutfem_apply_host", "cutfem_apply_host_batch",
+           "cutfem_csr_assemble",
            "cutfem_csr_setup", "cutfem_csr_apply", "cutfem_csr_nnz", "cutfem_csr_download",
            "cutfem_stats", "cutfem_last_error", "cutfem_destroy", "cutfem_partition_x",
            "cutfem_local_build", "cutfem_local_free", "cutfem_nccl_unique_id", "cutfem_setup_dist",
@@ -121,6 +122,8 @@ def load(path: str | None = None):
     L.cutfem_setup.argtypes = [ctypes.POINTER(_Problem), i32, ctypes.POINTER(vp)]
     L.cutfem_apply.argtypes = [vp, vp, vp, vp]
     L.cutfem_apply_host.argtypes = [vp, vp, vp, vp]
+    L.cutfem_apply_host_batch.argtypes = [vp, vp, vp, ctypes.c_int64, vp]
+    L.cutfem_apply_host_batch.restype = i32
     L.cutfem_apply_kernel.argtypes = [vp, ctypes.c_int, vp, vp, vp]
     L.cutfem_csr_assemble.argtypes = [vp, ctypes.POINTER(i64)]
     L.cutfem_csr_setup.argtypes = [vp, i64, vp, vp, vp]
@@ -352,6 +355,17 @@ class CutFEM:
         _check(self._L.cutfem_apply_host(self._h, u.ctypes.data, v.ctypes.data,
                                          _stream_ptr(stream) if stream else None))
         return v
+
+    def apply_host_batch(self, us, vs, stream=0):
+        """Pipelined end-to-end path: vs[k] = A us[k] for a list of host arrays (page-locked
+        memory lets the copies overlap the applies); synchronous."""
+        assert len(us) == len(vs)
+        for a in list(us) + list(vs):
+            assert a.dtype == np.float64 and a.size == self.n_dofs and a.flags.c_contiguous
+        up = (ctypes.c_void_p * len(us))(*[a.ctypes.data for a in us])
+        vp = (ctypes.c_void_p * len(vs))(*[a.ctypes.data for a in vs])
+        _check(self._L.cutfem_apply_host_batch(self._h, up, vp, len(us), _stream_ptr(stream) if stream else None))
+        return vs
 
     def rhs_const(self, f: float = 1.0, b=None, stream=None):
         """b = f * int_Omega phi_i (device, owned blocks)."""

@@ -118,8 +118,11 @@ struct cutfem_handle {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_started = nullptr;  // k_cutp launch completion (all CTAs begun)
-  // host path buffers
+  // host path buffers (the batched path: two pairs, copy streams, events)
   double *d_u = nullptr, *d_v = nullptr;
+  double *d_ub[2] = {nullptr, nullptr}, *d_vb[2] = {nullptr, nullptr};
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   // CSR
   int64_t csr_nnz = 0;
   bool csr_i64 = false;
@@ -1180,6 +1183,15 @@ void free_handle(cutfem_handle *hd) {
   cudaFree(hd->d_sfptr);
   cudaFree(hd->d_u);
   cudaFree(hd->d_v);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(hd->d_ub[b]);
+    cudaFree(hd->d_vb[b]);
+    if (hd->ev_in[b]) cudaEventDestroy(hd->ev_in[b]);
+    if (hd->ev_done[b]) cudaEventDestroy(hd->ev_done[b]);
+    if (hd->ev_out[b]) cudaEventDestroy(hd->ev_out[b]);
+  }
+  if (hd->s_h2d) cudaStreamDestroy(hd->s_h2d);
+  if (hd->s_d2h) cudaStreamDestroy(hd->s_d2h);
   cudaFree(hd->d_rowptr);
   cudaFree(hd->d_col);
   cudaFree(hd->d_val);
@@ -1639,6 +1651,54 @@ int cutfem_apply_host(cutfem_handle *hd, const double *u_host, double *v_host, v
   int rc = dispatch_apply(hd, hd->d_u, hd->d_v, st);
   if (rc) return rc;
   CU(cudaMemcpyAsync(v_host, hd->d_v, bytes, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int cutfem_apply_host_batch(cutfem_handle *hd, const double *const *u_host, double *const *v_host, int64_t nbatch,
+                            void *cuda_stream) {
+  if (!hd) return fail(CUTFEM_EINVAL, "null handle");
+  if (hd->dist) return fail(CUTFEM_EUNSUPPORTED, "batched host applies on a distributed handle");
+  if (nbatch < 0 || (nbatch > 0 && (!u_host || !v_host))) return fail(CUTFEM_EINVAL, "batch arrays");
+  for (int64_t k = 0; k < nbatch; ++k)
+    if (hd->stats.n_dofs > 0 && (!u_host[k] || !v_host[k])) return fail(CUTFEM_EINVAL, "null vector in the batch");
+  CU(cudaSetDevice(hd->device));
+  const size_t bytes = sizeof(double) * (size_t)hd->stats.n_dofs;
+  if (!hd->d_ub[0]) {
+    for (int b = 0; b < 2; ++b) {
+      CU(cudaMalloc(&hd->d_ub[b], std::max<size_t>(bytes, 16)));
+      CU(cudaMalloc(&hd->d_vb[b], std::max<size_t>(bytes, 16)));
+      CU(cudaEventCreateWithFlags(&hd->ev_in[b], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&hd->ev_done[b], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&hd->ev_out[b], cudaEventDisableTiming));
+    }
+    CU(cudaStreamCreateWithFlags(&hd->s_h2d, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&hd->s_d2h, cudaStreamNonBlocking));
+    hd->dev_bytes += (int64_t)(4 * bytes);
+  }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  // the copy streams start after the caller's prior work on st
+  CU(cudaEventRecord(hd->ev_done[0], st));
+  CU(cudaStreamWaitEvent(hd->s_h2d, hd->ev_done[0], 0));
+  CU(cudaStreamWaitEvent(hd->s_d2h, hd->ev_done[0], 0));
+  for (int64_t k = 0; k < nbatch; ++k) {
+    const int b = (int)(k & 1);
+    // u_k into buffer b once apply k-2 (the last reader of d_ub[b]) is done
+    if (k >= 2) CU(cudaStreamWaitEvent(hd->s_h2d, hd->ev_done[b], 0));
+    CU(cudaMemcpyAsync(hd->d_ub[b], u_host[k], bytes, cudaMemcpyHostToDevice, hd->s_h2d));
+    CU(cudaEventRecord(hd->ev_in[b], hd->s_h2d));
+    // apply k once u_k has landed and v_{k-2} has left d_vb[b]
+    CU(cudaStreamWaitEvent(st, hd->ev_in[b], 0));
+    if (k >= 2) CU(cudaStreamWaitEvent(st, hd->ev_out[b], 0));
+    int rc = dispatch_apply(hd, hd->d_ub[b], hd->d_vb[b], st);
+    if (rc) return rc;
+    CU(cudaEventRecord(hd->ev_done[b], st));
+    // v_k out once apply k is done
+    CU(cudaStreamWaitEvent(hd->s_d2h, hd->ev_done[b], 0));
+    CU(cudaMemcpyAsync(v_host[k], hd->d_vb[b], bytes, cudaMemcpyDeviceToHost, hd->s_d2h));
+    CU(cudaEventRecord(hd->ev_out[b], hd->s_d2h));
+  }
+  CU(cudaStreamSynchronize(hd->s_d2h));
   CU(cudaStreamSynchronize(st));
   return 0;
 }

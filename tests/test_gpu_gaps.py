@@ -186,3 +186,17 @@ def test_nccl_loopback_cg_allreduce(cf, cutgen_mod):
     d.debug_loopback(None, None)
     x1, h1 = d.cg(b, iters=20)
     assert torch.equal(x0[:P.n_dofs], x1[:P.n_dofs]) and np.array_equal(h0, h1)
+
+
+def test_apply_host_batch_matches_device_apply(cf, cutgen_mod):
+    """The pipelined host path (cutfem_apply_host_batch): every v_k equals the device
+    apply of u_k, with distinct inputs, a repeated input pointer and an odd batch."""
+    P = cutgen_mod.generate(cutgen_mod.SPHERE, 10, -1.0, 1.0, 3)
+    op = cf.CutFEM(P)
+    us = [torch.from_numpy(P.seeded_u(s)).pin_memory().numpy() for s in (1, 2, 3)]
+    batch_u = [us[0], us[1], us[2], us[1], us[0]]
+    vs = [torch.empty(P.n_dofs, dtype=torch.float64).pin_memory().numpy() for _ in batch_u]
+    op.apply_host_batch(batch_u, vs)
+    for uk, vk in zip(batch_u, vs):
+        vd = op.apply(torch.from_numpy(uk).cuda()).cpu().numpy()
+        assert np.array_equal(vk, vd)
