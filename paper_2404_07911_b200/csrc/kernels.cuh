@@ -395,7 +395,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // ============================================================== cut cells
 #ifndef CUT_PREF_MAXN
-#define CUT_PREF_MAXN 7
+#define CUT_PREF_MAXN 9  // neighbour blocks by cp.async at entry up to this n (round 2: 7 -> 9,
+                         // with the w-space faces: C3 p=7 apply 1139 -> 998 us, p=8 2225 -> 2024 us)
 #endif
 // CTAs per SM the register allocation of k_cut<n> must allow (ptxas's own choice
 // without a bound gave these at n = 5..9; an explicit 1 lets it take up to 255
@@ -414,7 +415,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
                          // full up to n = 7, none above: measured)
 #endif
 #ifndef CUT_WFACE_MASK
-#define CUT_WFACE_MASK 0xe0
+#define CUT_WFACE_MASK 0x3e0  // bit n: structured faces in w-space (n = 5..9)
 #endif
 #ifndef CUT_PPF_MASK
 #define CUT_PPF_MASK 0x300  // bit n: prefetch the point rows (n = 8, 9: measured faster; 6, 7 slower)
