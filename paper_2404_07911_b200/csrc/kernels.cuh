@@ -402,7 +402,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // without a bound gave these at n = 5..9; an explicit 1 lets it take up to 255
 // registers and was measured 15 % slower at n = 5, 7)
 #ifndef CUT_MINB5
-#define CUT_MINB5 4
+#define CUT_MINB5 6
 #endif
 #ifndef CUT_MINB6
 #define CUT_MINB6 3
@@ -432,14 +432,26 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef CUT_SPLIT_MASK
 #define CUT_SPLIT_MASK 0x2ff  // bit n: split the point phase over THREADS / CHUNK threads (not n = 8: measured slower)
 #endif
+#ifndef CUT_TH5
+#define CUT_TH5 64  // threads per k_cut<5> CTA (one cut cell per CTA; 128 -> 64 with 6 CTAs / SM: C3 p=4 k_cut 426 -> 397 us)
+#endif
+#ifndef CUT_CH5
+#define CUT_CH5 32  // points per chunk at n = 5 (THREADS / CHUNK = SPL threads per point)
+#endif
+#ifndef CUT_TH6
+#define CUT_TH6 128
+#endif
+#ifndef CUT_CH6
+#define CUT_CH6 64
+#endif
 template <int N>
 struct CutCfg {
-  static constexpr int THREADS = 128;
+  static constexpr int THREADS = N == 5 ? CUT_TH5 : (N == 6 ? CUT_TH6 : 128);
   static constexpr int MINB = N <= 4 ? 1 : (N == 5 ? CUT_MINB5 : (N == 6 ? CUT_MINB6 : (N == 7 ? CUT_MINB7 : 2)));
   static constexpr int NN = N * N, N3 = N * N * N;
   static constexpr int ROW0 = 2 * NN + 2 * N;
   static constexpr int ROW = (ROW0 % 2 == 0) ? ROW0 + 1 : ROW0;  // odd stride: no bank conflicts
-  static constexpr int CHUNK = N <= 4 ? 128 : (N <= 6 ? 64 : 32);
+  static constexpr int CHUNK = N <= 4 ? 128 : (N == 5 ? CUT_CH5 : (N == 6 ? CUT_CH6 : 32));
   static constexpr int FROW = 2 * N + 3;  // cut-face point row: l(s), l(t), c1, c2 (+pad)
   static constexpr int KPT = (N3 + THREADS - 1) / THREADS;
   // integration phase: each thread owns RPT x-rows (b, c) of the block (sharing the
@@ -973,7 +985,7 @@ __device__ __forceinline__ void line_chunks(const double *__restrict__ pts, int6
 }
 
 template <int N>
-__global__ void __launch_bounds__(128, CutCfg<N>::MINB) k_cut(const double *__restrict__ u, double *__restrict__ v,
+__global__ void __launch_bounds__(CutCfg<N>::THREADS, CutCfg<N>::MINB) k_cut(const double *__restrict__ u, double *__restrict__ v,
                                              const CDesc *__restrict__ desc, int ncut,
                                              const double *__restrict__ vol_pts,
                                              const int64_t *__restrict__ vol_ptr,
