@@ -417,6 +417,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef CUT_WFACE_MASK
 #define CUT_WFACE_MASK 0x3e0  // bit n: structured faces in w-space (n = 5..9)
 #endif
+#ifndef CUT_BFACE_MASK
+#define CUT_BFACE_MASK 0x1c0  // bit n: the cut faces batched (n = 6, 7, 8)
+#endif
 #ifndef CUT_PPF_MASK
 #define CUT_PPF_MASK 0x300  // bit n: prefetch the point rows (n = 8, 9: measured faster; 6, 7 slower)
 #endif
@@ -470,6 +473,10 @@ struct CutCfg {
   // structured faces in w-space (one parallel pass + one M (x) M (x) M sweep) instead
   // of face by face; needs the prefetched neighbours (measured faster at n = 5, 6, 7)
   static constexpr bool WFACE = PREF && ((CUT_WFACE_MASK >> N) & 1);
+  // (w-space degrees) every cut face of the cell in one batched pass instead of face by
+  // face with its barriers (C3 p=5 cut kernel 444 -> 401 us, p=6 767 -> 750, p=7 888 -> 866;
+  // p=4 398 -> 403, p=8 1861 -> 1895: off there)
+  static constexpr bool BFACE = WFACE && ((CUT_BFACE_MASK >> N) & 1);
   // U, T, R, NB[NBN] (padded blocks) + JA, JB, FC1, FC2 (NN each) + point rows
   // point rows of the next chunk prefetched (cp.async, double buffer of 8 doubles a
   // point) while the current one is processed
@@ -1166,6 +1173,138 @@ __global__ void __launch_bounds__(CutCfg<N>::THREADS, CutCfg<N>::MINB) k_cut(con
       }
     }
   }
+  if constexpr (C::BFACE) {
+    // cut faces (eq:unstructured_face P:491-496), all of the cell's faces in one pass:
+    // traces of every cut face, then the faces' points as one concatenated stream in
+    // chunks, each (face, in-face node) item summed by one thread, then one pass over
+    // the DoFs adds every face's line coefficients and writes v (no per-face barriers)
+    uint32_t scm = 0;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      bool gp, ss, sc;
+      if (face_on(f, gp, ss, sc) && sc) scm |= 1u << f;
+    }
+    double *vb = v + (size_t)dsc.blk * N3;
+    if (!scm) {
+      for (int l = tid; l < N3; l += TH) vb[l] = Rb[B::pad(l)];
+      return;
+    }
+    constexpr int FR = C::FROW, FCH = TH;
+    double *JAa = PS, *JBa = PS + 6 * NN, *F1a = PS + 12 * NN, *F2a = PS + 18 * NN, *RW = PS + 24 * NN;
+    long long *PBs = reinterpret_cast<long long *>(RW + FCH * FR);  // [6] first point, [7] prefix offsets
+    static_assert(24 * NN + FCH * FR + 13 <= C::CHUNK * C::ROW, "cut-face buffers fit the point rows");
+    const int nsc = __popc(scm);
+    auto kth = [&](int k) {  // the k-th cut face (k < nsc)
+      uint32_t m = scm;
+      for (int i = 0; i < k; ++i) m &= m - 1;
+      return __ffs(m) - 1;
+    };
+    if (tid == 0) {  // the faces' first points and prefix offsets in the concatenation
+      long long cu = 0;
+#pragma unroll
+      for (int f = 0; f < 6; ++f) {
+        long long b = 0, c = 0;
+        if ((scm >> f) & 1u) {
+          b = __ldg(sf_ptr + dsc.sf[f]);
+          c = __ldg(sf_ptr + dsc.sf[f] + 1) - b;
+        }
+        PBs[f] = b;
+        PBs[6 + f] = cu;
+        cu += c;
+      }
+      PBs[12] = cu;
+    }
+    for (int it = tid; it < nsc * NN; it += TH) {
+      const int k = it / NN, t = it - k * NN, f = kth(k);
+      const int dd = f >> 1, side = f & 1;
+      const double *NBf = NBs + f * SZ;
+      const double *dow = side ? R.d1 : R.d0, *dnb = side ? R.d0 : R.d1;
+      int b0, st;
+      B::line(dd, t, b0, st);
+      double A = 0.0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) A = fma(dow[m], U[b0 + m * st], fma(dnb[m], NBf[b0 + m * st], A));
+      JAa[f * NN + t] = side ? U[b0 + (N - 1) * st] - NBf[b0] : U[b0] - NBf[b0 + (N - 1) * st];
+      JBa[f * NN + t] = A;
+      F1a[f * NN + t] = 0.0;
+      F2a[f * NN + t] = 0.0;
+    }
+    __syncthreads();
+    const long long *cum = PBs + 6;
+    const long long Q = cum[6];
+    for (long long c0 = 0; c0 < Q; c0 += FCH) {
+      {
+        const long long g = c0 + tid;
+        if (g < Q) {
+          int f = 0;
+#pragma unroll
+          for (int i = 1; i < 6; ++i) f += g >= cum[i];
+          const long long q = PBs[f] + (g - cum[f]);
+          const double s = __ldg(sf_pts + 4 * q), tq = __ldg(sf_pts + 4 * q + 1), W = __ldg(sf_pts + 4 * q + 2);
+          const double sg = (f & 1) ? 1.0 : -1.0;
+          double ls[N], lt[N];
+          basis_v<N>(R, s, ls);
+          basis_v<N>(R, tq, lt);
+          const double *JA = JAa + f * NN, *JB = JBa + f * NN;
+          double J0 = 0.0, A = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+              r0 = fma(ls[i], JA[i + N * j], r0);
+              r1 = fma(ls[i], JB[i + N * j], r1);
+            }
+            J0 = fma(lt[j], r0, J0);
+            A = fma(lt[j], r1, A);
+          }
+          double *row = RW + tid * FR;
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            row[i] = ls[i];
+            row[N + i] = lt[i];
+          }
+          row[2 * N] = W * (kp.sigma * J0 - sg * A * kp.i2h);
+          row[2 * N + 1] = -W * sg * J0 * kp.i2h;
+        }
+      }
+      __syncthreads();
+      for (int it = tid; it < nsc * NN; it += TH) {
+        const int k = it / NN, ij = it - k * NN, f = kth(k);
+        const int i = ij % N, j = ij / N;
+        const long long lo = cum[f] > c0 ? cum[f] : c0, hi = cum[f + 1] < c0 + FCH ? cum[f + 1] : c0 + FCH;
+        double f1 = F1a[f * NN + ij], f2 = F2a[f * NN + ij];
+        for (int r = (int)(lo - c0); r < (int)(hi - c0); ++r) {
+          const double *row = RW + r * FR;
+          const double psi = row[i] * row[N + j];
+          f1 = fma(psi, row[2 * N], f1);
+          f2 = fma(psi, row[2 * N + 1], f2);
+        }
+        F1a[f * NN + ij] = f1;
+        F2a[f * NN + ij] = f2;
+      }
+      __syncthreads();
+    }
+    // v = Rb + every cut face's line coefficients: DoF (a, b, c) lies on line t of
+    // axis dd at position m (B::line's numbering: t = (b, c), (a, c), (a, b))
+    for (int l = tid; l < N3; l += TH) {
+      const int a = l % N, bb = (l / N) % N, c = l / NN;
+      double r = Rb[B::pad(l)];
+#pragma unroll
+      for (int f = 0; f < 6; ++f) {
+        if (!((scm >> f) & 1u)) continue;
+        const int dd = f >> 1, side = f & 1;
+        const int m = dd == 0 ? a : (dd == 1 ? bb : c);
+        const int t = dd == 0 ? bb + N * c : (dd == 1 ? a + N * c : a + N * bb);
+        const double dw = side ? R.d1[m] : R.d0[m];
+        r = fma(dw, F2a[f * NN + t], r);
+        if (m == (side ? N - 1 : 0)) r += F1a[f * NN + t];
+      }
+      vb[l] = r;
+    }
+    return;
+  }
+  if constexpr (!C::BFACE)  // face by face (structured and cut faces, or cut faces only)
   for (int f = 0; f < 6; ++f) {
     bool gp, ss, sc;
     if (!face_on(f, gp, ss, sc)) continue;
