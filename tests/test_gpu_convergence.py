@@ -1,0 +1,103 @@
+"""The CUDA path against mathematics at sizes the oracle cannot assemble (SURVEY §8(c)
+Q11 on the GPU, the DG convergence study).
+
+The manufactured solution u = cos(om R) - cos(om r) (-Laplace u = f on the ball, u = 0
+on the sphere) is solved on 16^3 / 32^3 / 64^3 meshes -- the last one is the
+C2 mesh of the headline benchmark -- with the library's own solver (p-multigrid PCG on
+`cutfem_apply`, include/cutfem.h cutfem_mg_*).  Only the load vector and the L2 error
+come from the oracle (both are per-cell quadratures, seconds at these sizes); the
+operator is never assembled on the CPU.  The property that holds at any size: the L2
+error falls with order >= p + 0.7 (the bound of the CPU pin Q11), and at the sizes the
+CPU pin reaches (16^3, 32^3; tests/golden/q11_oracle_l2_errors.jsonl, written by
+tools/q11_full.py, which calls only the oracle) it equals the error of the
+oracle's own discrete solution -- the same discrete problem solved by two
+independent implementations.  A wrong term, weight or face in any kernel family
+(structured tiles, cut cells, faces between them) breaks the order or the value.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import Oracle  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def cf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_07911_b200 as m
+    m.load()
+    return m
+
+
+def level_degrees(p):
+    d = [p]
+    while d[0] > 1:
+        d.insert(0, max(1, d[0] // 2))
+    return d
+
+
+def solve_manufactured_gpu(cf, cutgen_mod, N, p, tol=1e-10, iters=600):
+    """Relative L2 error of the GPU solution of the manufactured problem on N^3."""
+    R, om = 0.7, math.pi
+    c = np.array(cutgen_mod.SPHERE["center"])
+    degs = level_degrees(p)
+    kw = dict(sipg_gamma=10.0 * p ** 2, nitsche_tau=10.0 * p ** 2)  # every level: the finest penalties (A27)
+    probs = [cutgen_mod.generate(cutgen_mod.SPHERE, N, -1.0, 1.0, q, **kw) for q in degs]
+    P = probs[-1]
+
+    def rr(x):
+        return np.linalg.norm(x - c, axis=-1)
+
+    def f(x):
+        r = rr(x)
+        return -om ** 2 * (np.cos(om * r) + 2 * np.sinc(om * r / math.pi))
+
+    def uex(x):
+        return math.cos(om * R) - np.cos(om * rr(x))
+
+    O = Oracle(P)
+    b = torch.from_numpy(O.rhs(f)).cuda()
+    ops = [cf.CutFEM(Q) for Q in probs]
+    mg = cf.CutFEMMG(ops, inner="block", smooth_degree=4, eig_iters=20)
+    x, hist = mg.pcg(b, iters=iters, tol=tol)
+    assert hist[-1] <= tol * float(b.norm()) * 1.0001, (N, p, len(hist), hist[-1] / float(b.norm()))
+    # the residual the solver reports is the true one (recomputed with one apply)
+    r = b - ops[-1].apply(x)
+    assert float(r.norm()) <= 10 * tol * float(b.norm())
+    err = O.l2_error(x.cpu().numpy(), uex)
+    del mg
+    for o in ops:
+        o.close()
+    return err, len(hist) - 1
+
+
+def cpu_pin_errors():
+    """The oracle's own errors on 8^3 / 16^3 / 32^3 (tools/q11_full.py, oracle only)."""
+    out = {}
+    with open(os.path.join(ROOT, "tests", "golden", "q11_oracle_l2_errors.jsonl")) as fh:
+        for line in fh:
+            d = json.loads(line)
+            out[d["p"]] = dict(zip(d["meshes"], d["l2_rel_err"]))
+    return out
+
+
+@pytest.mark.parametrize("p,meshes", [(1, (16, 32, 64)), (2, (16, 32, 64)), (3, (16, 32, 64)), (4, (8, 16, 32))])
+def test_dg_manufactured_convergence_gpu(cf, cutgen_mod, p, meshes):
+    errs = [solve_manufactured_gpu(cf, cutgen_mod, N, p)[0] for N in meshes]
+    for k in range(len(meshes) - 1):
+        rate = math.log(errs[k] / errs[k + 1]) / math.log(meshes[k + 1] / meshes[k])
+        assert rate >= p + 0.7, (p, meshes, errs, rate)
+    # same discrete problem as the oracle's CSR solve where that exists
+    pins = cpu_pin_errors().get(p, {})
+    for N, e in zip(meshes, errs):
+        if N in pins:
+            assert abs(e - pins[N]) <= 1e-4 * pins[N], (p, N, e, pins[N])
