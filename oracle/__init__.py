@@ -18,10 +18,13 @@ cell matrix, Q2 face closed form, Q3 GP closed form order by order, Q4 "level
 set misses the mesh" = standard SIPG, Q5 axis-aligned plane = sum of Kronecker
 products (every term, cut faces included), Q6 exact identities, Q7 symmetry,
 Q8 SPD, Q9 quadrature moments, Q10 tensor rule as cut rule, Q11 convergence
-order, Q12 CSR = blockwise (DESIGN.md §4 maps every function to its pin).
-"parity unpinned": the absolute value of curved-interface contributions has no
-closed form; it is pinned exactly on the plane (Q5) and indirectly on curved
-interfaces (Q6, Q7, Q8, Q9, Q11).
+order, Q12 CSR = blockwise, Q13 the sphere's cut-cell volume + Nitsche terms
+against the Gamma-function closed form of a(q, r) for global polynomials
+(DESIGN.md §4 maps every function to its pin).
+"parity unpinned": only the absolute value of the cut-FACE SIPG term between two
+cells cut by a CURVED interface for discontinuous input (no closed form); that
+code path is pinned exactly on the plane (Q5), its face areas on the sphere by
+the per-cell divergence theorem (Q9), and it is covered indirectly by Q7, Q8, Q11.
 """
 from .basis import Basis1D  # noqa: F401
 from .operator import Oracle  # noqa: F401

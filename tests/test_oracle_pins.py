@@ -605,3 +605,97 @@ def test_oracle_spmv_c_matches_scipy(cutgen_mod):
     for nt in (1, 3):
         y, _ = spmv.spmv(M, u, nthreads=nt)
         assert np.abs(y - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+# -------------------------------------------------------------------- Q13
+def _ball_moment(e, R, surface):
+    """Integral of X^a Y^b Z^c over the sphere |X| = R (surface) or the ball |X| <= R:
+    2 G((a+1)/2) G((b+1)/2) G((c+1)/2) / G((a+b+c+3)/2) R^(a+b+c+2) for even exponents
+    (0 otherwise); the ball integral is the radial integral of that, R / (a+b+c+3) times it."""
+    if any(k % 2 for k in e):
+        return 0.0
+    s = sum(e)
+    m = 2.0 * math.gamma((e[0] + 1) / 2) * math.gamma((e[1] + 1) / 2) * math.gamma((e[2] + 1) / 2) \
+        / math.gamma((s + 3) / 2) * R ** (s + 2)
+    return m if surface else m * R / (s + 3)
+
+
+def _pmul(f, g):
+    out = {}
+    for ea, ca in f.items():
+        for eb, cb in g.items():
+            k = (ea[0] + eb[0], ea[1] + eb[1], ea[2] + eb[2])
+            out[k] = out.get(k, 0.0) + ca * cb
+    return out
+
+
+def _pdiff(f, d):
+    out = {}
+    for e, c in f.items():
+        if e[d] > 0:
+            k = tuple(e[i] - (i == d) for i in range(3))
+            out[k] = out.get(k, 0.0) + c * e[d]
+    return out
+
+
+def _padd(f, g, s=1.0):
+    out = dict(f)
+    for e, c in g.items():
+        out[e] = out.get(e, 0.0) + s * c
+    return out
+
+
+def _pint(f, R, surface):
+    return sum(c * _ball_moment(e, R, surface) for e, c in f.items())
+
+
+def _peval(f, X):
+    return sum(c * X[..., 0] ** e[0] * X[..., 1] ** e[1] * X[..., 2] ** e[2] for e, c in f.items())
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_q13_curved_interface_closed_form(cutgen_mod, p):
+    """The absolute value of the curved-interface terms (cut-cell volume + Nitsche on a
+    sphere) against a closed form: for GLOBAL polynomials q, r of degree <= p every jump
+    vanishes (SIPG, ghost penalty: 0) and eq:bilinear_dg reduces to
+        a(q, r) = int_B grad q . grad r - int_S (d_n q r + q d_n r) + tau/h int_S q r
+    over the ball B and sphere S, whose monomial moments are Gamma-function closed forms
+    (n = X / R on S).  The only error is the generated quadrature's, which Q9 bounds and
+    which falls with h; a wrong sign, a dropped tau/h, a flipped normal or a missing weight
+    in the oracle's cut-cell volume or Nitsche code is O(1)."""
+    R = 0.7
+    c = np.array(cutgen_mod.SPHERE["center"])
+    rng = np.random.default_rng(13)
+    mons = [(a, b, d) for a in range(p + 1) for b in range(p + 1) for d in range(p + 1) if a + b + d <= p]
+    q = {e: float(rng.standard_normal()) for e in mons}
+    r = {e: float(rng.standard_normal()) for e in mons}
+    Xn = {(1, 0, 0): 1.0 / R}, {(0, 1, 0): 1.0 / R}, {(0, 0, 1): 1.0 / R}  # the normal's components on S
+    grad = lambda f: [_pdiff(f, d) for d in range(3)]  # noqa: E731
+    gq, gr = grad(q), grad(r)
+    vol = {}
+    dnq, dnr = {}, {}
+    for d in range(3):
+        vol = _padd(vol, _pmul(gq[d], gr[d]))
+        dnq = _padd(dnq, _pmul(gq[d], Xn[d]))
+        dnr = _padd(dnr, _pmul(gr[d], Xn[d]))
+    nodes = gll_np(p)
+    Z, Y, X = np.meshgrid(nodes, nodes, nodes, indexing="ij")
+    loc = np.stack([X.ravel(), Y.ravel(), Z.ravel()], 1)
+    errs = []
+    for N in (8, 16):
+        P = cutgen_mod.generate(cutgen_mod.SPHERE, N, -1.0, 1.0, p)
+        tau = P.nitsche_tau / P.h
+        exact = _pint(vol, R, False) - _pint(_padd(_pmul(dnq, r), _pmul(q, dnr)), R, True) \
+            + tau * _pint(_pmul(q, r), R, True)
+        scale = abs(_pint(vol, R, False)) + tau * abs(_pint(_pmul(q, q), R, True))
+        xs = np.asarray(P.lower) + P.h * (P.active_ijk[:, None, :] + loc[None]) - c
+        O = Oracle(P)
+        got = float(_peval(r, xs).reshape(-1) @ O.apply(_peval(q, xs).reshape(-1)))
+        errs.append(abs(got - exact) / scale)
+        if N == 8:  # fault injection: flipped interface normals (the consistency terms change sign)
+            P.srf_pts[:, 3:6] *= -1.0
+            bad = float(_peval(r, xs).reshape(-1) @ Oracle(P).apply(_peval(q, xs).reshape(-1)))
+            cons = _pint(_padd(_pmul(dnq, r), _pmul(q, dnr)), R, True)
+            assert abs((bad - got) - 2.0 * cons) <= 5e-3 * abs(cons) and abs(cons) > 1e-3 * scale / tau
+    # measured: p = 1 6.7e-5 -> 7.9e-6 (the (p+1)-point rules: ~h^3), p = 2 1.9e-6 -> 3.4e-8, p = 3 7.0e-7 -> 2.4e-9
+    assert errs[1] <= (2e-5 if p == 1 else 1e-7) and errs[1] <= errs[0] / 4, errs
