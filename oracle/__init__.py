@@ -21,10 +21,9 @@ Q8 SPD, Q9 quadrature moments, Q10 tensor rule as cut rule, Q11 convergence
 order, Q12 CSR = blockwise, Q13 the sphere's cut-cell volume + Nitsche terms
 against the Gamma-function closed form of a(q, r) for global polynomials
 (DESIGN.md §4 maps every function to its pin).
-"parity unpinned": only the absolute value of the cut-FACE SIPG term between two
-cells cut by a CURVED interface for discontinuous input (no closed form); that
-code path is pinned exactly on the plane (Q5), its face areas on the sphere by
-the per-cell divergence theorem (Q9), and it is covered indirectly by Q7, Q8, Q11.
+Q14 the cut-face SIPG next to the sphere against 1-D polynomial integrals (broken
+polynomials across a mesh plane: the faces in it tile a disk).  No function of this
+package is left "parity unpinned".
 """
 from .basis import Basis1D  # noqa: F401
 from .operator import Oracle  # noqa: F401
