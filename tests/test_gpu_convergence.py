@@ -13,6 +13,9 @@ tools/q11_full.py, which calls only the oracle) it equals the error of the
 oracle's own discrete solution -- the same discrete problem solved by two
 independent implementations.  A wrong term, weight or face in any kernel family
 (structured tiles, cut cells, faces between them) breaks the order or the value.
+Measured (profiles/r02e_gpu_convergence.jsonl): p = 3 on 64^3 3.24e-7 (order 4.72), the
+16^3 / 32^3 errors equal the oracle's to 6+ digits; p = 4 is pre-asymptotic on 8^3 (order 4.54
+from 8^3 to 16^3, 4.93 from 16^3 to 32^3), so its meshes start at 16^3.
 """
 import json
 import math
@@ -91,7 +94,7 @@ def cpu_pin_errors():
     return out
 
 
-@pytest.mark.parametrize("p,meshes", [(1, (16, 32, 64)), (2, (16, 32, 64)), (3, (16, 32, 64)), (4, (8, 16, 32))])
+@pytest.mark.parametrize("p,meshes", [(1, (16, 32, 64)), (2, (16, 32, 64)), (3, (16, 32, 64)), (4, (16, 32))])
 def test_dg_manufactured_convergence_gpu(cf, cutgen_mod, p, meshes):
     res = [solve_manufactured_gpu(cf, cutgen_mod, N, p) for N in meshes]
     errs = [e for e, _ in res]
