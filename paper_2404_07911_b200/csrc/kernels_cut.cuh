@@ -930,6 +930,12 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
 
 
 // ======================================================= cut cells, p = 1, 2 (k_cut1)
+#ifndef CUT1_LD128
+#define CUT1_LD128 0  // own block and result through 128-bit loads / stores
+#endif
+#ifndef CUT1_NBREG
+#define CUT1_NBREG 0  // structured faces: the neighbour block in registers (128-bit loads) instead of per-line loads
+#endif
 // One THREAD (p = 1) or a thread PAIR (p = 2) per cut cell (k_cell's layout for the
 // uncut cells): at p = 1, 2 a cut cell has ~30 / ~85 points and 8 / 27 DoFs, so a warp
 // per cell (k_cutp) spends most of its time in per-cell work done by a few lanes
@@ -975,8 +981,11 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
   double uo[N3], acc[N3];
   {
     const double *ub = u + (size_t)d.blk * N3;
+    if constexpr (CUT1_LD128) load_block<N>(ub, uo);  // 128-bit loads (kernels_tile.cuh)
+    else {
 #pragma unroll
-    for (int k = 0; k < N3; ++k) uo[k] = __ldg(ub + k);
+      for (int k = 0; k < N3; ++k) uo[k] = __ldg(ub + k);
+    }
   }
   // n = 3: the cut faces' point ranges requested now (consumed in step 4, so the dependent
   // loads stay off that step's critical path; C3 p=2 apply 213 -> 210 us).  n = 2: at the
@@ -1000,13 +1009,16 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
     if (!(g || sp) || (F % TPC) != kk) return;
     any_st = true;
     const double *nbp = u + (size_t)d.nb[F] * N3;
+    double nbv[CUT1_NBREG ? N3 : 1];
+    if constexpr (CUT1_NBREG) load_block<N>(nbp, nbv);  // the neighbour block by 128-bit loads
 #pragma unroll
     for (int t = 0; t < NN; ++t) {
       double o[N], n_[N], out[N];
 #pragma unroll
       for (int m = 0; m < N; ++m) {
         o[m] = uo[lix<N, D>(t, m)];
-        n_[m] = __ldg(nbp + lix<N, D>(t, m));
+        if constexpr (CUT1_NBREG) n_[m] = nbv[lix<N, D>(t, m)];
+        else n_[m] = __ldg(nbp + lix<N, D>(t, m));
         out[m] = 0.0;
       }
       if (g) {
@@ -1222,7 +1234,22 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
   }
   if (!valid) return;
   double *vb = v + (size_t)d.blk * N3;
+  if constexpr (CUT1_LD128) {
+    // 128-bit stores on the 16-byte aligned part of the block (all of it at even n^3), the
+    // pairs dealt round-robin to the cell's lanes (every lane holds the full sum)
+    constexpr int H = N3 / 2;
+    const bool par = (N3 % 2) && ((reinterpret_cast<uintptr_t>(vb) >> 3) & 1u) != 0;
+    double2 *q = reinterpret_cast<double2 *>(vb + (par ? 1 : 0));
 #pragma unroll
-  for (int k = 0; k < N3; ++k)
-    if (TPC == 1 || k % TPC == kk) vb[k] = acc[k];
+    for (int i = 0; i < H; ++i)
+      if (TPC == 1 || i % TPC == kk)
+        q[i] = par ? make_double2(acc[2 * i + 1], acc[(2 * i + 2) % N3]) : make_double2(acc[2 * i], acc[2 * i + 1]);
+    if constexpr (N3 % 2 == 1) {
+      if (kk == 0) vb[par ? 0 : N3 - 1] = par ? acc[0] : acc[N3 - 1];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < N3; ++k)
+      if (TPC == 1 || k % TPC == kk) vb[k] = acc[k];
+  }
 }
