@@ -931,10 +931,10 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
 
 // ======================================================= cut cells, p = 1, 2 (k_cut1)
 #ifndef CUT1_LD128
-#define CUT1_LD128 0  // own block and result through 128-bit loads / stores
+#define CUT1_LD128 1  // own block and result through 128-bit loads / stores
 #endif
 #ifndef CUT1_NBREG
-#define CUT1_NBREG 0  // structured faces: the neighbour block in registers (128-bit loads) instead of per-line loads
+#define CUT1_NBREG 1  // structured faces: the neighbour block in registers (128-bit loads) instead of per-line loads
 #endif
 // One THREAD (p = 1) or a thread PAIR (p = 2) per cut cell (k_cell's layout for the
 // uncut cells): at p = 1, 2 a cut cell has ~30 / ~85 points and 8 / 27 DoFs, so a warp
@@ -1234,6 +1234,13 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
   }
   if (!valid) return;
   double *vb = v + (size_t)d.blk * N3;
+  if constexpr (CUT1_LD128 && CELL_LD256 && TPC == 1 && (N3 % 4) == 0) {
+    if ((reinterpret_cast<uintptr_t>(vb) & 31) == 0) {
+#pragma unroll
+      for (int k = 0; k < N3; k += 4) stg256(vb + k, acc[k], acc[k + 1], acc[k + 2], acc[k + 3]);
+      return;
+    }
+  }
   if constexpr (CUT1_LD128) {
     // 128-bit stores on the 16-byte aligned part of the block (all of it at even n^3), the
     // pairs dealt round-robin to the cell's lanes (every lane holds the full sum)

@@ -812,9 +812,27 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
 #ifndef CELL_LD128
 #define CELL_LD128 1  // k_cell<3>: 128-bit loads / stores on the 16-byte aligned part of the 216-byte blocks
 #endif
+#ifndef CELL_LD256
+#define CELL_LD256 0  // n = 2: the 64-byte blocks through 256-bit loads / stores when 32-byte aligned
+#endif
+// sm_100: 256-bit global accesses (LDG.E.ENL2.256 / STG.E.ENL2.256), 32-byte aligned
+__device__ __forceinline__ void ldg256(const double *p, double &a, double &b, double &c, double &d) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ void stg256(double *p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 template <int N>
 __device__ __forceinline__ void load_block(const double *__restrict__ p, double (&x)[N * N * N]) {
   constexpr int N3 = N * N * N;
+  if constexpr (CELL_LD256 && (N3 % 4) == 0) {
+    if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {  // (uniform: blocks are 32-byte multiples)
+#pragma unroll
+      for (int k = 0; k < N3; k += 4) ldg256(p + k, x[k], x[k + 1], x[k + 2], x[k + 3]);
+      return;
+    }
+  }
   if constexpr ((N3 % 2) == 0) {
 #pragma unroll
     for (int k = 0; k < N3; k += 2) {
@@ -988,6 +1006,13 @@ __global__ void __launch_bounds__(128) k_cell(const double *__restrict__ u, doub
   if (!valid) return;
   double *vb = v + (size_t)d.blk * N3;
   constexpr int H = TPC == 2 ? ((N3 / 2 + 1) & ~1) : N3;  // the pair splits the store (even cut)
+  if constexpr (CELL_LD256 && TPC == 1 && (N3 % 4) == 0) {
+    if ((reinterpret_cast<uintptr_t>(vb) & 31) == 0) {
+#pragma unroll
+      for (int k = 0; k < N3; k += 4) stg256(vb + k, w[k], w[k + 1], w[k + 2], w[k + 3]);
+      return;
+    }
+  }
   if constexpr ((N3 % 2) == 0) {
 #pragma unroll
     for (int k = 0; k < N3; k += 2)
