@@ -813,7 +813,7 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
 #define CELL_LD128 1  // k_cell<3>: 128-bit loads / stores on the 16-byte aligned part of the 216-byte blocks
 #endif
 #ifndef CELL_LD256
-#define CELL_LD256 0  // n = 2: the 64-byte blocks through 256-bit loads / stores when 32-byte aligned
+#define CELL_LD256 1  // n = 2: the 64-byte blocks through 256-bit loads / stores when 32-byte aligned
 #endif
 // sm_100: 256-bit global accesses (LDG.E.ENL2.256 / STG.E.ENL2.256), 32-byte aligned
 __device__ __forceinline__ void ldg256(const double *p, double &a, double &b, double &c, double &d) {

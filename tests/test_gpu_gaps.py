@@ -147,6 +147,30 @@ def test_misaligned_pointer_rejected(cf, cutgen_mod):
         op.apply(buf[1:P.n_dofs + 1])
 
 
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_vectors_16_byte_aligned_only(cf, cutgen_mod, p):
+    """The pointer contract is 16-byte alignment (include/cutfem.h): vectors that are 16- but
+    not 32-byte aligned (torch views shifted by two doubles) take the narrower load / store
+    paths of k_cell / k_cut1 (256-bit accesses need 32 bytes) and must give the same bits."""
+    P = cutgen_mod.generate(cutgen_mod.SPHERE, 9, -1.0, 1.0, p)
+    op = cf.CutFEM(P)
+    u = torch.from_numpy(P.seeded_u(5)).cuda()
+    v0 = op.apply(u).clone()
+    ub = torch.zeros(P.n_dofs + 4, dtype=torch.float64, device="cuda")
+    vb = torch.zeros(P.n_dofs + 4, dtype=torch.float64, device="cuda")
+    for su, sv in ((2, 0), (0, 2), (2, 2)):
+        uu, vv = ub[su:su + P.n_dofs], vb[sv:sv + P.n_dofs]
+        assert uu.data_ptr() % 32 == 8 * su % 32 and vv.data_ptr() % 32 == 8 * sv % 32
+        uu.copy_(u)
+        vb.fill_(7.0)
+        op.apply(uu, vv)
+        torch.cuda.synchronize()
+        assert torch.equal(vv, v0), (p, su, sv)
+        # nothing written outside the vector
+        assert float(vb[:sv].abs().sum()) == 7.0 * sv and float(vb[sv + P.n_dofs:].abs().sum()) == 7.0 * (4 - sv)
+    check(P, v0.cpu().numpy(), P.seeded_u(5))
+
+
 @pytest.mark.parametrize("p,nparts", [(2, 2), (3, 3), (5, 2)])
 def test_nccl_loopback_halo(cf, cutgen_mod, p, nparts):
     """The NCCL halo exchange on a real (1-rank) communicator: every slab's handle
