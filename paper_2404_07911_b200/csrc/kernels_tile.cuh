@@ -809,9 +809,6 @@ __global__ void __launch_bounds__(128) k_uncw(const double *__restrict__ u, doub
 #ifndef CELL_G3
 #define CELL_G3 1
 #endif
-#ifndef CELL_LD256N3
-#define CELL_LD256N3 0  // n = 3: 256-bit loads / stores with a 4-way alignment select
-#endif
 #ifndef CELL_LD128
 #define CELL_LD128 1  // k_cell<3>: 128-bit loads / stores on the 16-byte aligned part of the 216-byte blocks
 #endif
@@ -843,26 +840,6 @@ __device__ __forceinline__ void load_block(const double *__restrict__ p, double 
       x[k] = t.x;
       x[k + 1] = t.y;
     }
-  } else if constexpr (CELL_LD256N3 && N3 == 27) {
-    // n = 3 with 256-bit loads: pre = the doubles before the first 32-byte boundary (0..3); the
-    // 24 values from there through six 256-bit loads, the other three (pre at the front, 3 - pre
-    // at the back) through 64-bit loads; a 4-way select per value puts them in place
-    const unsigned pre = (4u - (unsigned)((reinterpret_cast<uintptr_t>(p) >> 3) & 3u)) & 3u;
-    const double *q = p + pre;
-    double V[24], S[3];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) ldg256(q + 4 * i, V[4 * i], V[4 * i + 1], V[4 * i + 2], V[4 * i + 3]);
-#pragma unroll
-    for (int j = 0; j < 3; ++j) S[j] = __ldg(p + ((unsigned)j < pre ? j : 24 + j));
-    const bool b0 = pre & 1u, b1 = pre & 2u;
-#pragma unroll
-    for (int k = 0; k < N3; ++k) {
-      const double c0 = k < 24 ? V[k < 24 ? k : 0] : S[k >= 24 ? k - 24 : 0];
-      const double c1 = k < 1 ? S[0] : (k < 25 ? V[(k >= 1 && k < 25) ? k - 1 : 0] : S[k >= 24 ? k - 24 : 0]);
-      const double c2 = k < 2 ? S[k < 2 ? k : 0] : (k < 26 ? V[(k >= 2 && k < 26) ? k - 2 : 0] : S[2]);
-      const double c3 = k < 3 ? S[k < 3 ? k : 0] : V[k >= 3 ? k - 3 : 0];
-      x[k] = b1 ? (b0 ? c3 : c2) : (b0 ? c1 : c0);
-    }
   } else if constexpr (CELL_LD128) {
     // odd N3 (n = 3): a block is only 8-byte aligned.  Its 16-byte aligned part (N3 - 1
     // values from p + par, par = the parity of the block's address in doubles) goes through
@@ -892,27 +869,6 @@ template <int N>
 __device__ __forceinline__ void store_block(double *__restrict__ p, const double (&w)[N * N * N]) {
   constexpr int N3 = N * N * N, H = N3 / 2;
   static_assert(N3 % 2 == 1, "odd blocks only");
-  if constexpr (CELL_LD256N3 && N3 == 27) {
-    const unsigned pre = (4u - (unsigned)((reinterpret_cast<uintptr_t>(p) >> 3) & 3u)) & 3u;
-    const bool b0 = pre & 1u, b1 = pre & 2u;
-    double *q = p + pre;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      double o[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int m = 4 * i + e;  // V[m] = w[m + pre]
-        o[e] = b1 ? (b0 ? w[m + 3] : w[m + 2]) : (b0 ? w[m + 1] : w[m]);
-      }
-      stg256(q + 4 * i, o[0], o[1], o[2], o[3]);
-    }
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const bool front = (unsigned)j < pre;
-      p[front ? j : 24 + j] = front ? w[j] : w[24 + j];
-    }
-    return;
-  }
   const bool par = ((reinterpret_cast<uintptr_t>(p) >> 3) & 1u) != 0;
   double2 *q = reinterpret_cast<double2 *>(p + (par ? 1 : 0));
 #pragma unroll
