@@ -933,6 +933,9 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
 #ifndef CUT1_LD128
 #define CUT1_LD128 1  // own block and result through 128-bit loads / stores
 #endif
+#ifndef CUT1_PT256
+#define CUT1_PT256 0  // point rows through 256-bit loads
+#endif
 #ifndef CUT1_NBREG
 #define CUT1_NBREG 1  // structured faces: the neighbour block in registers (128-bit loads) instead of per-line loads
 #endif
@@ -1134,28 +1137,36 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
       }
     }
   };
+  // point rows are 32 (volume, cut face) / 64 bytes (interface) in cudaMalloc'ed arrays:
+  // one / two 256-bit loads per point (CUT1_PT256; the kernel is bound by the number of
+  // load instructions in flight)
+  auto ld_row = [](const double *r, double2 &a, double2 &b) {
+    if constexpr (CUT1_PT256) ldg256(r, a.x, a.y, b.x, b.y);
+    else {
+      a = __ldg(reinterpret_cast<const double2 *>(r));
+      b = __ldg(reinterpret_cast<const double2 *>(r) + 1);
+    }
+  };
   if (cell_on && kk < d.nv) {
-    const double2 *p = reinterpret_cast<const double2 *>(vol_pts + 4 * d.vb);
-    double2 a = __ldg(p + 2 * kk), b = __ldg(p + 2 * kk + 1);
+    const double *p = vol_pts + 4 * d.vb;
+    double2 a, b;
+    ld_row(p + 4 * kk, a, b);
     for (int q = kk; q < d.nv; q += TPC) {
       const double2 ca = a, cb = b;
-      if (q + TPC < d.nv) {  // the next point's row in flight while this one is evaluated
-        a = __ldg(p + 2 * (q + TPC));
-        b = __ldg(p + 2 * (q + TPC) + 1);
-      }
+      if (q + TPC < d.nv) ld_row(p + 4 * (q + TPC), a, b);  // the next point's row in flight while this one is evaluated
       point(ca.x, ca.y, cb.x, cb.y, false, 0.0, 0.0, 0.0);
     }
   }
   if (nit_on && kk < d.ns) {
-    const double2 *p = reinterpret_cast<const double2 *>(srf_pts + 8 * d.sb);
-    double2 a = __ldg(p + 4 * kk), b = __ldg(p + 4 * kk + 1), c = __ldg(p + 4 * kk + 2), e = __ldg(p + 4 * kk + 3);
+    const double *p = srf_pts + 8 * d.sb;
+    double2 a, b, c, e;
+    ld_row(p + 8 * kk, a, b);
+    ld_row(p + 8 * kk + 4, c, e);
     for (int q = kk; q < d.ns; q += TPC) {
       const double2 ca = a, cb = b, cc = c, ce = e;
       if (q + TPC < d.ns) {
-        a = __ldg(p + 4 * (q + TPC));
-        b = __ldg(p + 4 * (q + TPC) + 1);
-        c = __ldg(p + 4 * (q + TPC) + 2);
-        e = __ldg(p + 4 * (q + TPC) + 3);
+        ld_row(p + 8 * (q + TPC), a, b);
+        ld_row(p + 8 * (q + TPC) + 4, c, e);
       }
       point(ca.x, ca.y, cb.x, ce.x, true, cb.y, cc.x, cc.y);
     }
@@ -1182,17 +1193,11 @@ __global__ void __launch_bounds__(128) k_cut1(const double *__restrict__ u, doub
       const double sg = SS ? 1.0 : -1.0;
       const int64_t pb = HOIST ? fpb[F] : sf_ptr[d.sf[F]], pe = HOIST ? fpe[F] : sf_ptr[d.sf[F] + 1];
       double2 nst = make_double2(0.5, 0.5), nw = make_double2(0.0, 0.0);
-      if (pb + kk < pe) {
-        nst = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * (pb + kk)));
-        nw = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * (pb + kk)) + 1);
-      }
+      if (pb + kk < pe) ld_row(sf_pts + 4 * (pb + kk), nst, nw);
       for (int64_t q = pb + kk; q < pe; q += TPC) {
         const double2 st = nst;
         const double W = nw.x;
-        if (q + TPC < pe) {  // the next point's row in flight while this one is evaluated
-          nst = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * (q + TPC)));
-          nw = __ldg(reinterpret_cast<const double2 *>(sf_pts + 4 * (q + TPC)) + 1);
-        }
+        if (q + TPC < pe) ld_row(sf_pts + 4 * (q + TPC), nst, nw);  // the next point's row in flight
         double ls[N], lt[N];
         basis_v_sym<N>(R, st.x, ls);
         basis_v_sym<N>(R, st.y, lt);
