@@ -934,7 +934,7 @@ __global__ void CUTP_BOUNDS k_cutp(const double *__restrict__ u, double *__restr
 #define CUT1_LD128 1  // own block and result through 128-bit loads / stores
 #endif
 #ifndef CUT1_PT256
-#define CUT1_PT256 0  // point rows through 256-bit loads
+#define CUT1_PT256 1  // point rows through 256-bit loads
 #endif
 #ifndef CUT1_NBREG
 #define CUT1_NBREG 1  // structured faces: the neighbour block in registers (128-bit loads) instead of per-line loads
